@@ -1,0 +1,175 @@
+/* bpqn.h -- C ABI of libbpqn, the B200 (sm_100a) hot path of arXiv 2604.10089
+ * ("A Bifidelity Proximal Quasi-Newton Method for Dense Rigid Body Suspension
+ * Collision Resolution"): the LCP matrix-vector product w = D^T M D lambda with a
+ * boundary-integral Stokes mobility solve inside, and the paper's Mono-PQN /
+ * Bi-PQN LCP solvers on top of it.
+ *
+ * Citations: PAPER.md line numbers (P:n); the discretisation the paper leaves
+ * open is fixed by the readings R1..R30 in DESIGN.md ("Readings").
+ *
+ * Conventions (all entry points):
+ *  - Arrays are fp64 unless marked i32.  "_dev" = device pointer (e.g. a torch
+ *    tensor's data_ptr()), "_host" = host pointer.  Vectors of rigid-body
+ *    quantities are ordered (Fx,Fy,Fz,Tx,Ty,Tz) / (Ux,Uy,Uz,Ox,Oy,Oz) per sphere
+ *    (P:71), row-major [Np][6].  Surface densities are [N][3] row-major with node
+ *    index m*Nq + k*2p + l (sphere m, polar ring k from the north pole, azimuth l).
+ *  - Ownership: the caller allocates and owns every I/O buffer.  The library owns
+ *    its workspace (allocated in bpqn_geometry_init, grown in bpqn_contacts) and
+ *    frees it in bpqn_geometry_destroy.  The hot calls allocate nothing.
+ *  - Streams: all device work is enqueued on `stream` (a cudaStream_t passed as
+ *    void*, NULL = legacy default stream).  Calls that return host scalars
+ *    (stats, reports, counts) synchronise that stream before returning.
+ *  - Threads: a handle is single-owner (not thread-safe); distinct handles may be
+ *    used concurrently from different threads.
+ *  - Errors: every call returns an int status (BPQN_OK = 0 on success) and sets
+ *    a thread-local message readable with bpqn_last_error().  There is no CPU
+ *    fallback: without a usable CUDA device every call returns BPQN_ERR_CUDA.
+ */
+#ifndef BPQN_H
+#define BPQN_H
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  BPQN_OK = 0,
+  BPQN_ERR_INVALID = 1,   /* null pointer, bad size, p < 2, a <= 0, mu <= 0, overlap, lambda < 0 */
+  BPQN_ERR_CUDA = 2,      /* CUDA runtime error (message has the CUDA string) */
+  BPQN_ERR_OOM = 3,       /* device allocation failed */
+  BPQN_ERR_NOCONV = 4,    /* GMRES or PQN reached max iterations; outputs hold the last iterate */
+  BPQN_ERR_STALLED = 5,   /* PQN step length vanished twice (after one memory reset) */
+  BPQN_ERR_NAN = 6,       /* NaN/Inf detected */
+  BPQN_ERR_CAPACITY = 7   /* more contacts than max_contacts (count is still returned) */
+};
+
+typedef struct bpqn_geom* bpqn_geom_t;   /* one discretisation (fidelity) over one set of spheres */
+
+/* Discretisation options; NULL -> defaults.  p_s: order of the rotated singular
+ * self grid (default 2p, R6).  d_near: target-to-sphere distance below which the
+ * refined near rule replaces the coarse rule (default 4 pi a / p, R8).
+ * near_n1/near_n2/near_nphi: refined-rule node counts (defaults 2p+16, p+8, 4p). */
+typedef struct {
+  int p_s;
+  double d_near;
+  int near_n1, near_n2, near_nphi;
+  int build_single_layer; /* 1 (default): also precompute S-kernel near/self data */
+} bpqn_disc_opts;
+
+/* GMRES options (R9).  NULL -> tol 1e-12 (relative residual), restart 50, max 1000. */
+typedef struct {
+  double tol;
+  int restart;
+  int max_iters;
+} bpqn_gmres_opts;
+
+typedef struct {
+  int iters;          /* total GMRES iterations (operator applications in the Krylov loop) */
+  int restarts;
+  double rel_resid;   /* final relative residual estimate */
+  double ms;          /* device time of the whole call (CUDA events) */
+} bpqn_gmres_stats;
+
+typedef struct {
+  int method;                 /* 0 = Mono-PQN (Alg. 1), 1 = Bi-PQN (Alg. 3) */
+  int k_max;                  /* outer iteration cap (default 200) */
+  double eps_kkt_abs;         /* ||min(x, Ax+b)||_2 stop, default 1e-10 */
+  double eps_kkt_rel;         /* relative KKT stop; <= 0 disables (default 0) */
+  double tau;                 /* forward step (R11, default 1) */
+  int refresh_period;         /* gradient-cache refresh (R18, default 20) */
+  double sub_eps_factor;      /* Bi-PQN subproblem tolerance factor (R22, default 1e-2) */
+  int sub_k_max;              /* Bi-PQN subproblem iteration cap (default 50) */
+  double prox_tol;            /* Alg. 4 tolerance; <= 0 -> 1e-12 max(1, |x~|_inf) */
+  int prox_jmax;              /* Alg. 4 iteration cap (default 100) */
+  double curv_skip;           /* BFGS curvature skip threshold (R16, default 1e-12) */
+  bpqn_gmres_opts gm_hi, gm_lo;
+  double cost_ratio;          /* t_lo/t_hi for E-MVPs; <= 0 -> measured */
+} bpqn_solve_opts;
+
+typedef struct {
+  int iterations, hi_mvps, lo_mvps, gmres_iters_hi, gmres_iters_lo;
+  double e_mvps, cost_ratio, kkt_abs, kkt_rel, objective, ms_total, ms_hi, ms_lo;
+  int termination;            /* 0 KKT_ABS, 1 KKT_REL, 2 MAX_ITER, 3 STALLED */
+} bpqn_report;
+
+/* Defaults for the option structs above. */
+void bpqn_default_disc_opts(bpqn_disc_opts* o);
+void bpqn_default_gmres_opts(bpqn_gmres_opts* o);
+void bpqn_default_solve_opts(bpqn_solve_opts* o);
+
+/* Build one discretisation of Np spheres of radius a in fluid of viscosity mu at
+ * SH order p (grids R10, projection R7, self quadrature R5/R6, near rule R8):
+ * grids, SH analysis, the per-sphere self operators E (FP64 tensor-core GEMM
+ * operands) and the per-incidence near-correction matrices; workspace for GMRES.
+ * centers_host [Np][3].  Fails with BPQN_ERR_INVALID if two spheres overlap. */
+int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius,
+                       double mu, int p, const bpqn_disc_opts* opts, void* stream);
+int bpqn_geometry_destroy(bpqn_geom_t g);
+
+/* Sizes of a geometry: N surface nodes, Nq nodes per sphere, near incidences,
+ * bytes of device memory held. */
+int bpqn_geometry_info(bpqn_geom_t g, int* n_nodes, int* nq, long long* n_incidences,
+                       long long* device_bytes);
+
+/* Contact detection (R20): pairs i<j with gap |c_j-c_i| - 2a < gap_threshold,
+ * lexicographic.  Writes up to max_contacts entries: pairs_dev [max][2] i32,
+ * normals_dev [max][3] (n = (c_j-c_i)/|c_j-c_i|), gaps_dev [max]; *n_contacts_host
+ * = total count (BPQN_ERR_CAPACITY if it exceeds max_contacts).  Stores the set in
+ * the handle as the contact set of bpqn_lcp_mvp. */
+int bpqn_contacts(bpqn_geom_t g, double gap_threshold, int max_contacts, int* n_contacts_host,
+                  int* pairs_dev, double* normals_dev, double* gaps_dev, void* stream);
+
+/* Install an explicit contact set (e.g. the hi-fidelity set into the lo-fidelity
+ * handle, required by Bi-PQN).  Device arrays as in bpqn_contacts. */
+int bpqn_set_contacts(bpqn_geom_t g, int n_contacts, const int* pairs_dev, const double* normals_dev,
+                      const double* gaps_dev, void* stream);
+
+/* u = S_full[f] + D_full[q] at all N nodes (the discrete layer operator, O6).
+ * f_dev or q_dev may be NULL (treated as zero).  All [N][3]. */
+int bpqn_layer_apply(bpqn_geom_t g, const double* f_dev, const double* q_dev, double* u_dev, void* stream);
+
+/* Tangential Janus slip (R13): u_s = -B (a_m - (xi.a_m) xi) where xi.a_m > 0, else 0.
+ * axes_host [Np][3] unit axes; slip_dev [N][3]. */
+int bpqn_janus_slip(bpqn_geom_t g, const double* axes_host, double B, double* slip_dev, void* stream);
+
+/* Mobility (Fig. 1): (U, Omega) = M_slip(F, T; u_s) by the
+ * completed double-layer BIE (R1-R4) solved with device GMRES from q0 = 0.
+ * ft_dev [Np][6], slip_dev [N][3] or NULL, uo_dev [Np][6].  st may be NULL. */
+int bpqn_mobility_apply(bpqn_geom_t g, const double* ft_dev, const double* slip_dev, double* uo_dev,
+                        const bpqn_gmres_opts* gm, bpqn_gmres_stats* st, void* stream);
+
+/* LCP MVP: w = D^T M D lambda for the handle's contact set.
+ * lambda_dev, w_dev [Nc]. */
+int bpqn_lcp_mvp(bpqn_geom_t g, const double* lambda_dev, double* w_dev, const bpqn_gmres_opts* gm,
+                 bpqn_gmres_stats* st, void* stream);
+
+/* b = (Phi + dt D^T U_nc)/dt with U_nc = M_slip(F_nc, 0; u_s) (R14).
+ * fnc_dev [Np][3], slip_dev [N][3] or NULL, b_dev [Nc]. */
+int bpqn_lcp_b(bpqn_geom_t g, const double* fnc_dev, const double* slip_dev, double dt, double* b_dev,
+               const bpqn_gmres_opts* gm, bpqn_gmres_stats* st, void* stream);
+
+/* LCP solve 0 <= A x + b  _|_  x >= 0, A = D^T M D by Mono-PQN
+ * (lo == NULL or o->method == 0) or Bi-PQN (lo = coarser-p handle over the same
+ * spheres with the same contact set).  b_dev [Nc]; lambda_dev [Nc]: in = x_init
+ * (>= 0), out = solution.  rep may be NULL. */
+int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* lambda_dev,
+                   const bpqn_solve_opts* o, bpqn_report* rep, void* stream);
+
+/* Same solvers on explicit dense operators (test-only; SPEC.md worked examples):
+ * A_host, Ahat_host [n][n] row-major (Ahat NULL -> Mono-PQN), b_host, x_host [n]. */
+int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, const double* b_host,
+                         double* x_host, const bpqn_solve_opts* o, bpqn_report* rep);
+
+/* Thread-local message for the last non-zero return. */
+const char* bpqn_last_error(void);
+
+/* Kernel-level profiling hooks (bench.py): time of the last operator pieces (ms)
+ * and the number of kernels launched since the last reset. */
+int bpqn_profile_get(bpqn_geom_t g, double* ms_allpairs, double* ms_near, double* ms_self,
+                     long long* allpairs_launches, long long* kernel_launches);
+int bpqn_profile_reset(bpqn_geom_t g, int enable_events);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* BPQN_H */

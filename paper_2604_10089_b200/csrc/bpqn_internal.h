@@ -1,0 +1,162 @@
+// Internal declarations of libbpqn (B200 / sm_100a).  Not part of the C ABI.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/bpqn.h"
+
+namespace bpqn {
+
+// ---------------------------------------------------------------- errors
+void set_error(const std::string& msg);
+struct Error {
+  int code;
+  std::string msg;
+};
+#define BPQN_CUDA(call)                                                                      \
+  do {                                                                                       \
+    cudaError_t e_ = (call);                                                                 \
+    if (e_ != cudaSuccess)                                                                   \
+      throw ::bpqn::Error{e_ == cudaErrorMemoryAllocation ? BPQN_ERR_OOM : BPQN_ERR_CUDA,    \
+                          std::string(#call) + ": " + cudaGetErrorString(e_)};               \
+  } while (0)
+#define BPQN_CHECK_LAUNCH() BPQN_CUDA(cudaGetLastError())
+#define BPQN_REQUIRE(cond, msg)                                  \
+  do {                                                           \
+    if (!(cond)) throw ::bpqn::Error{BPQN_ERR_INVALID, (msg)};   \
+  } while (0)
+
+// ---------------------------------------------------------------- device buffer
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    BPQN_CUDA(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void ensure(size_t count) {
+    if (count > n) alloc(count);
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+// ---------------------------------------------------------------- geometry
+// Host-side description of the order-p grid (reading R10): (p+1) Gauss-Legendre
+// nodes in t = cos(theta) (descending), 2p equispaced phi.
+struct Grid {
+  int p = 0, nq = 0;
+  std::vector<double> t, omega, theta, phi;  // [p+1], [p+1], [p+1], [2p]
+  std::vector<double> xi;                    // [nq][3] unit normals
+  std::vector<double> w;                     // [nq] area weights (a^2 omega pi/p)
+};
+void gauss_legendre_desc(int n, std::vector<double>& t, std::vector<double>& w);
+void build_grid(int p, double a, Grid& g);
+int sh_count(int p);  // dim V_p = p^2 + 2p
+
+struct Profile {
+  bool events = false;
+  cudaEvent_t e[8] = {};
+  double ms_allpairs = 0, ms_near = 0, ms_self = 0;
+  long long allpairs_launches = 0, launches = 0;
+};
+
+struct Geom {
+  int np = 0, p = 0, nq = 0, n = 0, nb = 0;
+  double a = 1, mu = 1, d_near = 0;
+  int p_s = 0, n1 = 0, n2 = 0, nphi = 0;
+  bool single_layer = true;
+  int sms = 148;
+  std::vector<double> centers;  // host [np][3]
+  Grid grid;
+
+  // static node data
+  DBuf<double> X;        // [N][3] node positions
+  DBuf<double> src;      // [N][8] {y0,y1,y2,w, n0,n1,n2,0}
+  DBuf<double> centers_d;// [np][3]
+  DBuf<double> xi_d;     // [nq][3]
+  DBuf<double> w_d;      // [nq]
+  DBuf<double> analysis; // [nb][nq] SH analysis (projection = Ynodes * analysis)
+
+  // self operators, row-major [3nq][3nq]
+  DBuf<double> E_S;   // S_self - naive same-sphere Stokeslet
+  DBuf<double> E_L;   // D_self - naive same-sphere stresslet (layer operator)
+  DBuf<double> E_A;   // E_L - I/2 + Pi_R (GMRES operator)
+
+  // near incidences (sorted by target); matrices [n_inc][3][3nq] per kernel kind
+  long long n_inc = 0;
+  DBuf<int> inc_t, inc_m;        // [n_inc]
+  DBuf<int> nt_list, nt_ptr;     // near targets (unique) and CSR into incidences
+  int n_near_targets = 0;
+  DBuf<double> M_S, M_D;         // [n_inc][3][3nq]
+
+  // contacts
+  int nc = 0, nc_cap = 0;
+  DBuf<int> pairs;        // [cap][2]
+  DBuf<double> normals;   // [cap][3]
+  DBuf<double> gaps;      // [cap]
+
+  // workspaces
+  DBuf<double> far;      // [N][3] all-pairs accumulator
+  DBuf<double> nearout;  // [N][3]
+  DBuf<double> rhs, sol, tmp, tmp2;  // [N][3]
+  DBuf<double> V;        // GMRES basis [(m+1)][3N]
+  DBuf<double> red;      // reduction scratch
+  DBuf<double> scal;     // device scalars
+  DBuf<double> ft, uo;   // [np][6]
+  double* host_scal = nullptr;  // pinned
+  int gm_restart = 0;
+
+  Profile prof;
+  ~Geom();
+};
+
+// ---------------------------------------------------------------- kernels / passes
+enum Mode { MODE_S = 0, MODE_D = 1, MODE_SD = 2 };
+
+void precompute(Geom& g, cudaStream_t st);  // self E matrices + near matrices
+
+// out = Layer(sigmaS, sigmaD) with the given self matrix (E), mode selects the kernels.
+// Es used for sigS, Ed for sigD (either may be null when the density is null).
+void apply_operator(Geom& g, const double* sigS, const double* sigD, const double* Es, const double* Ed,
+                    double* out, cudaStream_t st);
+
+void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st);
+void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st);
+void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
+                      double* out, int accumulate, cudaStream_t st);
+
+// GMRES on A_op q = rhs (A_op = E_A + coarse + near); returns stats.
+int gmres_solve(Geom& g, const double* rhs, double* x, const bpqn_gmres_opts& o, bpqn_gmres_stats& st,
+                cudaStream_t s);
+
+// small kernels (contacts.cu)
+void launch_pt(Geom& g, const double* ft, double* f, cudaStream_t st);
+void launch_rigid_readout(Geom& g, const double* q, double* uo, cudaStream_t st);  // uo = -(Ubar, Obar)
+void launch_d_scatter(Geom& g, const double* lam, double* ft, cudaStream_t st);
+void launch_dt_gather(Geom& g, const double* uo, double* w, double dt_scale, const double* add,
+                      cudaStream_t st);
+void launch_axpby(double* y, double a, const double* x, double b, size_t n, cudaStream_t st);
+void launch_slip(Geom& g, const double* axes_dev, double B, double* slip, cudaStream_t st);
+int detect_contacts(Geom& g, double thr, int max_contacts, int* pairs, double* normals, double* gaps,
+                    cudaStream_t st);
+
+}  // namespace bpqn
+
+// the opaque C handle is a Geom
+struct bpqn_geom : public bpqn::Geom {};

@@ -1,0 +1,572 @@
+// C ABI of libbpqn (declarations and contracts in include/bpqn.h).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "bpqn_internal.h"
+#include "pqn.h"
+
+namespace bpqn {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+Geom::~Geom() {
+  if (host_scal) cudaFreeHost(host_scal);
+  for (auto& e : prof.e)
+    if (e) cudaEventDestroy(e);
+}
+
+template <class F>
+static int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return BPQN_ERR_INVALID;
+  }
+}
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static void upload(DBuf<double>& d, const std::vector<double>& h, cudaStream_t st) {
+  d.alloc(h.size());
+  if (!h.empty()) BPQN_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+}
+static void upload_i(DBuf<int>& d, const std::vector<int>& h, cudaStream_t st) {
+  d.alloc(std::max<size_t>(h.size(), 1));
+  if (!h.empty()) BPQN_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * 4, cudaMemcpyHostToDevice, st));
+}
+
+static bpqn_gmres_opts gm_or_default(const bpqn_gmres_opts* gm) {
+  bpqn_gmres_opts o;
+  bpqn_default_gmres_opts(&o);
+  if (gm) o = *gm;
+  if (o.restart <= 0) o.restart = 50;
+  if (o.max_iters <= 0) o.max_iters = 1000;
+  if (!(o.tol > 0)) o.tol = 1e-12;
+  return o;
+}
+
+// (U, Omega) = M_slip(ft; slip) -> uo (device); returns GMRES status
+static int mobility(Geom& g, const double* ft, const double* slip, double* uo, const bpqn_gmres_opts& o,
+                    bpqn_gmres_stats& st, cudaStream_t s) {
+  BPQN_REQUIRE(g.E_S.p, "geometry built without single-layer data (build_single_layer = 0)");
+  launch_pt(g, ft, g.tmp.p, s);
+  apply_operator(g, g.tmp.p, nullptr, g.E_S.p, nullptr, g.rhs.p, s);
+  const size_t n3 = 3 * (size_t)g.n;
+  if (slip) launch_axpby(g.rhs.p, 1.0, slip, -1.0, n3, s);
+  else launch_axpby(g.rhs.p, 0.0, g.rhs.p, -1.0, n3, s);
+  int rc = gmres_solve(g, g.rhs.p, g.sol.p, o, st, s);
+  launch_rigid_readout(g, g.sol.p, uo, s);
+  return rc;
+}
+
+static int lcp_mvp(Geom& g, const double* lam, double* w, const bpqn_gmres_opts& o, bpqn_gmres_stats& st,
+                   cudaStream_t s) {
+  BPQN_REQUIRE(g.nc > 0, "no contacts installed (call bpqn_contacts or bpqn_set_contacts)");
+  launch_d_scatter(g, lam, g.ft.p, s);
+  int rc = mobility(g, g.ft.p, nullptr, g.uo.p, o, st, s);
+  launch_dt_gather(g, g.uo.p, w, 1.0, nullptr, s);
+  return rc;
+}
+
+}  // namespace bpqn
+
+using namespace bpqn;
+
+extern "C" {
+
+const char* bpqn_last_error(void) { return g_err.c_str(); }
+
+void bpqn_default_disc_opts(bpqn_disc_opts* o) {
+  if (!o) return;
+  o->p_s = 0;
+  o->d_near = 0.0;
+  o->near_n1 = 0;
+  o->near_n2 = 0;
+  o->near_nphi = 0;
+  o->build_single_layer = 1;
+}
+
+void bpqn_default_gmres_opts(bpqn_gmres_opts* o) {
+  if (!o) return;
+  o->tol = 1e-12;
+  o->restart = 50;
+  o->max_iters = 1000;
+}
+
+void bpqn_default_solve_opts(bpqn_solve_opts* o) {
+  if (!o) return;
+  o->method = 0;
+  o->k_max = 200;
+  o->eps_kkt_abs = 1e-10;
+  o->eps_kkt_rel = 0.0;
+  o->tau = 1.0;
+  o->refresh_period = 20;
+  o->sub_eps_factor = 1e-2;
+  o->sub_k_max = 50;
+  o->prox_tol = 0.0;
+  o->prox_jmax = 100;
+  o->curv_skip = 1e-12;
+  bpqn_default_gmres_opts(&o->gm_hi);
+  bpqn_default_gmres_opts(&o->gm_lo);
+  o->cost_ratio = 0.0;
+}
+
+int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius, double mu,
+                       int p, const bpqn_disc_opts* opts, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(out && centers_host, "null pointer");
+    BPQN_REQUIRE(n_spheres >= 1, "n_spheres must be >= 1");
+    BPQN_REQUIRE(p >= 2, "p must be >= 2");
+    BPQN_REQUIRE(radius > 0 && mu > 0, "radius and mu must be > 0");
+    *out = nullptr;
+    int dev = 0;
+    BPQN_CUDA(cudaGetDevice(&dev));
+    cudaDeviceProp prop;
+    BPQN_CUDA(cudaGetDeviceProperties(&prop, dev));
+    cudaStream_t st = S(stream);
+    auto g = new bpqn_geom();
+    try {
+      g->sms = prop.multiProcessorCount;
+      g->np = n_spheres;
+      g->p = p;
+      g->a = radius;
+      g->mu = mu;
+      bpqn_disc_opts o;
+      bpqn_default_disc_opts(&o);
+      if (opts) o = *opts;
+      g->p_s = o.p_s > 0 ? o.p_s : 2 * p;
+      g->d_near = o.d_near > 0 ? o.d_near : 4.0 * M_PI * radius / p;
+      g->n1 = o.near_n1 > 0 ? o.near_n1 : 2 * p + 16;
+      g->n2 = o.near_n2 > 0 ? o.near_n2 : p + 8;
+      g->nphi = o.near_nphi > 0 ? o.near_nphi : 4 * p;
+      g->single_layer = o.build_single_layer != 0;
+      g->centers.assign(centers_host, centers_host + 3 * (size_t)n_spheres);
+      for (int i = 0; i < n_spheres; ++i)
+        for (int j = i + 1; j < n_spheres; ++j) {
+          double dx = g->centers[3 * j] - g->centers[3 * i], dy = g->centers[3 * j + 1] - g->centers[3 * i + 1],
+                 dz = g->centers[3 * j + 2] - g->centers[3 * i + 2];
+          double d = std::sqrt(dx * dx + dy * dy + dz * dz);
+          BPQN_REQUIRE(d - 2 * radius > 0, "spheres " + std::to_string(i) + " and " + std::to_string(j) + " overlap");
+        }
+      build_grid(p, radius, g->grid);
+      g->nq = g->grid.nq;
+      g->n = g->np * g->nq;
+      g->nb = sh_count(p);
+      const int nq = g->nq, N = g->n;
+      std::vector<double> X(3 * (size_t)N), src(8 * (size_t)N);
+      for (int m = 0; m < g->np; ++m)
+        for (int k = 0; k < nq; ++k) {
+          size_t i = (size_t)m * nq + k;
+          for (int c = 0; c < 3; ++c) {
+            X[3 * i + c] = g->centers[3 * m + c] + radius * g->grid.xi[3 * k + c];
+            src[8 * i + c] = X[3 * i + c];
+            src[8 * i + 4 + c] = g->grid.xi[3 * k + c];
+          }
+          src[8 * i + 3] = g->grid.w[k];
+          src[8 * i + 7] = 0.0;
+        }
+      upload(g->X, X, st);
+      upload(g->src, src, st);
+      upload(g->centers_d, g->centers, st);
+      upload(g->xi_d, g->grid.xi, st);
+      upload(g->w_d, g->grid.w, st);
+      // near incidences (target i, sphere m): |x_i - c_m| - a < d_near (R8), sorted by (i, m)
+      std::vector<std::pair<int, int>> inc;
+      for (int n = 0; n < g->np; ++n)
+        for (int m = 0; m < g->np; ++m) {
+          if (m == n) continue;
+          double dx = g->centers[3 * m] - g->centers[3 * n], dy = g->centers[3 * m + 1] - g->centers[3 * n + 1],
+                 dz = g->centers[3 * m + 2] - g->centers[3 * n + 2];
+          if (std::sqrt(dx * dx + dy * dy + dz * dz) - 2 * radius >= g->d_near) continue;
+          for (int k = 0; k < nq; ++k) {
+            size_t i = (size_t)n * nq + k;
+            double rx = X[3 * i] - g->centers[3 * m], ry = X[3 * i + 1] - g->centers[3 * m + 1],
+                   rz = X[3 * i + 2] - g->centers[3 * m + 2];
+            if (std::sqrt(rx * rx + ry * ry + rz * rz) - radius < g->d_near) inc.emplace_back((int)i, m);
+          }
+        }
+      std::sort(inc.begin(), inc.end());
+      g->n_inc = (long long)inc.size();
+      std::vector<int> it(inc.size()), im(inc.size()), ntl, ntp;
+      for (size_t k = 0; k < inc.size(); ++k) {
+        it[k] = inc[k].first;
+        im[k] = inc[k].second;
+        if (k == 0 || inc[k].first != inc[k - 1].first) {
+          ntl.push_back(inc[k].first);
+          ntp.push_back((int)k);
+        }
+      }
+      ntp.push_back((int)inc.size());
+      g->n_near_targets = (int)ntl.size();
+      upload_i(g->inc_t, it, st);
+      upload_i(g->inc_m, im, st);
+      upload_i(g->nt_list, ntl, st);
+      upload_i(g->nt_ptr, ntp, st);
+      size_t n3 = 3 * (size_t)N;
+      g->far.alloc(n3);
+      g->nearout.alloc(n3);
+      g->rhs.alloc(n3);
+      g->sol.alloc(n3);
+      g->tmp.alloc(n3);
+      g->tmp2.alloc(n3);
+      g->ft.alloc(6 * (size_t)g->np);
+      g->uo.alloc(6 * (size_t)g->np);
+      BPQN_CUDA(cudaMallocHost(&g->host_scal, 64 * sizeof(double)));
+      for (auto& e : g->prof.e) BPQN_CUDA(cudaEventCreate(&e));
+      precompute(*g, st);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_geometry_destroy(bpqn_geom_t g) {
+  return guarded([&]() -> int {
+    delete g;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_geometry_info(bpqn_geom_t g, int* n_nodes, int* nq, long long* n_incidences, long long* device_bytes) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    if (n_nodes) *n_nodes = g->n;
+    if (nq) *nq = g->nq;
+    if (n_incidences) *n_incidences = g->n_inc;
+    if (device_bytes) {
+      long long b = 0;
+      b += g->X.bytes() + g->src.bytes() + g->analysis.bytes() + g->E_S.bytes() + g->E_L.bytes() + g->E_A.bytes();
+      b += g->M_S.bytes() + g->M_D.bytes() + g->V.bytes() + g->far.bytes() * 6;
+      *device_bytes = b;
+    }
+    return BPQN_OK;
+  });
+}
+
+int bpqn_contacts(bpqn_geom_t g, double thr, int max_contacts, int* n_contacts_host, int* pairs_dev,
+                  double* normals_dev, double* gaps_dev, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && n_contacts_host, "null pointer");
+    BPQN_REQUIRE(max_contacts >= 0, "max_contacts < 0");
+    cudaStream_t st = S(stream);
+    int cap = (int)std::min<long long>((long long)g->np * (g->np - 1) / 2, 1 << 26);
+    g->pairs.ensure(2 * (size_t)std::max(cap, 1));
+    g->normals.ensure(3 * (size_t)std::max(cap, 1));
+    g->gaps.ensure((size_t)std::max(cap, 1));
+    int nc = detect_contacts(*g, thr, cap, g->pairs.p, g->normals.p, g->gaps.p, st);
+    g->nc = nc;
+    *n_contacts_host = nc;
+    int ncopy = std::min(nc, max_contacts);
+    if (ncopy > 0) {
+      BPQN_REQUIRE(pairs_dev && normals_dev && gaps_dev, "null output pointer");
+      BPQN_CUDA(cudaMemcpyAsync(pairs_dev, g->pairs.p, 2 * sizeof(int) * ncopy, cudaMemcpyDeviceToDevice, st));
+      BPQN_CUDA(cudaMemcpyAsync(normals_dev, g->normals.p, 3 * sizeof(double) * ncopy, cudaMemcpyDeviceToDevice, st));
+      BPQN_CUDA(cudaMemcpyAsync(gaps_dev, g->gaps.p, sizeof(double) * ncopy, cudaMemcpyDeviceToDevice, st));
+    }
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    if (nc > max_contacts) {
+      set_error("more contacts than max_contacts");
+      return BPQN_ERR_CAPACITY;
+    }
+    return BPQN_OK;
+  });
+}
+
+int bpqn_set_contacts(bpqn_geom_t g, int n_contacts, const int* pairs_dev, const double* normals_dev,
+                      const double* gaps_dev, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    BPQN_REQUIRE(n_contacts >= 0, "n_contacts < 0");
+    cudaStream_t st = S(stream);
+    g->pairs.ensure(2 * (size_t)std::max(n_contacts, 1));
+    g->normals.ensure(3 * (size_t)std::max(n_contacts, 1));
+    g->gaps.ensure((size_t)std::max(n_contacts, 1));
+    if (n_contacts > 0) {
+      BPQN_REQUIRE(pairs_dev && normals_dev && gaps_dev, "null pointer");
+      BPQN_CUDA(cudaMemcpyAsync(g->pairs.p, pairs_dev, 2 * sizeof(int) * n_contacts, cudaMemcpyDeviceToDevice, st));
+      BPQN_CUDA(cudaMemcpyAsync(g->normals.p, normals_dev, 3 * sizeof(double) * n_contacts, cudaMemcpyDeviceToDevice, st));
+      BPQN_CUDA(cudaMemcpyAsync(g->gaps.p, gaps_dev, sizeof(double) * n_contacts, cudaMemcpyDeviceToDevice, st));
+    }
+    g->nc = n_contacts;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_layer_apply(bpqn_geom_t g, const double* f_dev, const double* q_dev, double* u_dev, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && u_dev, "null pointer");
+    cudaStream_t st = S(stream);
+    if (!f_dev && !q_dev) {
+      BPQN_CUDA(cudaMemsetAsync(u_dev, 0, 3 * sizeof(double) * (size_t)g->n, st));
+      return BPQN_OK;
+    }
+    BPQN_REQUIRE(!f_dev || g->E_S.p, "geometry built without single-layer data");
+    apply_operator(*g, f_dev, q_dev, g->E_S.p, g->E_L.p, u_dev, st);
+    return BPQN_OK;
+  });
+}
+
+int bpqn_janus_slip(bpqn_geom_t g, const double* axes_host, double B, double* slip_dev, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && axes_host && slip_dev, "null pointer");
+    cudaStream_t st = S(stream);
+    DBuf<double> ax;
+    ax.alloc(3 * (size_t)g->np);
+    BPQN_CUDA(cudaMemcpyAsync(ax.p, axes_host, 3 * sizeof(double) * g->np, cudaMemcpyHostToDevice, st));
+    launch_slip(*g, ax.p, B, slip_dev, st);
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    return BPQN_OK;
+  });
+}
+
+int bpqn_mobility_apply(bpqn_geom_t g, const double* ft_dev, const double* slip_dev, double* uo_dev,
+                        const bpqn_gmres_opts* gm, bpqn_gmres_stats* st, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && ft_dev && uo_dev, "null pointer");
+    bpqn_gmres_stats tmp{};
+    int rc = mobility(*g, ft_dev, slip_dev, uo_dev, gm_or_default(gm), tmp, S(stream));
+    BPQN_CUDA(cudaStreamSynchronize(S(stream)));
+    if (st) *st = tmp;
+    if (rc) set_error("GMRES did not converge / NaN");
+    return rc;
+  });
+}
+
+int bpqn_lcp_mvp(bpqn_geom_t g, const double* lambda_dev, double* w_dev, const bpqn_gmres_opts* gm,
+                 bpqn_gmres_stats* st, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && lambda_dev && w_dev, "null pointer");
+    bpqn_gmres_stats tmp{};
+    int rc = lcp_mvp(*g, lambda_dev, w_dev, gm_or_default(gm), tmp, S(stream));
+    BPQN_CUDA(cudaStreamSynchronize(S(stream)));
+    if (st) *st = tmp;
+    if (rc) set_error("GMRES did not converge / NaN");
+    return rc;
+  });
+}
+
+int bpqn_lcp_b(bpqn_geom_t g, const double* fnc_dev, const double* slip_dev, double dt, double* b_dev,
+               const bpqn_gmres_opts* gm, bpqn_gmres_stats* st, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && fnc_dev && b_dev, "null pointer");
+    BPQN_REQUIRE(dt > 0, "dt must be > 0");
+    BPQN_REQUIRE(g->nc > 0, "no contacts installed");
+    cudaStream_t s = S(stream);
+    BPQN_CUDA(cudaMemsetAsync(g->ft.p, 0, 6 * sizeof(double) * g->np, s));
+    BPQN_CUDA(cudaMemcpy2DAsync(g->ft.p, 6 * sizeof(double), fnc_dev, 3 * sizeof(double), 3 * sizeof(double),
+                                g->np, cudaMemcpyDeviceToDevice, s));
+    bpqn_gmres_stats tmp{};
+    int rc = mobility(*g, g->ft.p, slip_dev, g->uo.p, gm_or_default(gm), tmp, s);
+    launch_dt_gather(*g, g->uo.p, b_dev, 1.0, nullptr, s);
+    launch_axpby(b_dev, 1.0 / dt, g->gaps.p, 1.0, g->nc, s);
+    BPQN_CUDA(cudaStreamSynchronize(s));
+    if (st) *st = tmp;
+    if (rc) set_error("GMRES did not converge / NaN");
+    return rc;
+  });
+}
+
+static PqnOpts to_pqn(const bpqn_solve_opts& o) {
+  PqnOpts q;
+  q.k_max = o.k_max;
+  q.eps_abs = o.eps_kkt_abs;
+  q.eps_rel = o.eps_kkt_rel;
+  q.tau = o.tau;
+  q.refresh = o.refresh_period;
+  q.sub_eps_factor = o.sub_eps_factor;
+  q.sub_k_max = o.sub_k_max;
+  q.prox_tol = o.prox_tol;
+  q.prox_jmax = o.prox_jmax;
+  q.curv = o.curv_skip;
+  return q;
+}
+
+int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* lambda_dev,
+                   const bpqn_solve_opts* opts, bpqn_report* rep, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(hi && b_dev && lambda_dev, "null pointer");
+    bpqn_solve_opts o;
+    bpqn_default_solve_opts(&o);
+    if (opts) o = *opts;
+    const bool bi = lo && o.method == 1;
+    if (bi) BPQN_REQUIRE(lo->nc == hi->nc, "Bi-PQN needs the same contact set on both fidelities");
+    cudaStream_t s = S(stream);
+    const int nc = hi->nc;
+    BPQN_REQUIRE(nc > 0, "no contacts installed");
+    std::vector<double> b(nc), x0(nc);
+    BPQN_CUDA(cudaMemcpyAsync(b.data(), b_dev, 8 * nc, cudaMemcpyDeviceToHost, s));
+    BPQN_CUDA(cudaMemcpyAsync(x0.data(), lambda_dev, 8 * nc, cudaMemcpyDeviceToHost, s));
+    BPQN_CUDA(cudaStreamSynchronize(s));
+    for (double v : x0) BPQN_REQUIRE(v >= 0, "x_init must be >= 0");
+    DBuf<double> dv, dw;
+    dv.alloc(nc);
+    dw.alloc(nc);
+    bpqn_gmres_opts ghi = gm_or_default(&o.gm_hi), glo = gm_or_default(&o.gm_lo);
+    double ms_hi = 0, ms_lo = 0;
+    int it_hi = 0, it_lo = 0, n_hi = 0, n_lo = 0;
+    int gm_fail = 0;
+    auto make = [&](Geom* g, const bpqn_gmres_opts& gm, double& ms, int& its, int& cnt) -> MvpFn {
+      return [&, g, gm](const std::vector<double>& v, std::vector<double>& out, std::vector<double>* aux) {
+        BPQN_CUDA(cudaMemcpyAsync(dv.p, v.data(), 8 * nc, cudaMemcpyHostToDevice, s));
+        bpqn_gmres_stats st{};
+        auto t0 = std::chrono::steady_clock::now();
+        int rc = lcp_mvp(*g, dv.p, dw.p, gm, st, s);
+        out.resize(nc);
+        BPQN_CUDA(cudaMemcpyAsync(out.data(), dw.p, 8 * nc, cudaMemcpyDeviceToHost, s));
+        BPQN_CUDA(cudaStreamSynchronize(s));
+        auto t1 = std::chrono::steady_clock::now();
+        ms += std::chrono::duration<double, std::milli>(t1 - t0).count();
+        its += st.iters;
+        cnt++;
+        if (rc) gm_fail = rc;
+        (void)aux;
+      };
+    };
+    MvpFn fhi = make(hi, ghi, ms_hi, it_hi, n_hi);
+    auto t0 = std::chrono::steady_clock::now();
+    PqnOpts q = to_pqn(o);
+    std::vector<double> x;
+    int iters = 0, term = 2, hi_mvps = 0, lo_mvps = 0;
+    double kkt = 0, kkt_rel = 0;
+    if (bi) {
+      MvpFn flo = make(lo, glo, ms_lo, it_lo, n_lo);
+      BiResult r = bi_pqn(fhi, flo, b, x0, q);
+      x = r.x;
+      iters = r.iterations;
+      term = r.termination;
+      hi_mvps = r.hi_mvps;
+      lo_mvps = r.lo_mvps;
+      kkt = r.kkt;
+      kkt_rel = r.kkt_rel;
+    } else {
+      MonoResult r = mono_pqn(fhi, b, x0, q, nullptr, nullptr, nullptr);
+      x = r.x;
+      iters = r.iterations;
+      term = r.termination;
+      hi_mvps = r.mvps;
+      kkt = r.kkt;
+      kkt_rel = r.kkt_rel;
+    }
+    auto t1 = std::chrono::steady_clock::now();
+    BPQN_CUDA(cudaMemcpyAsync(lambda_dev, x.data(), 8 * nc, cudaMemcpyHostToDevice, s));
+    BPQN_CUDA(cudaStreamSynchronize(s));
+    if (rep) {
+      rep->iterations = iters;
+      rep->hi_mvps = hi_mvps;
+      rep->lo_mvps = lo_mvps;
+      rep->gmres_iters_hi = it_hi;
+      rep->gmres_iters_lo = it_lo;
+      double t_hi = n_hi ? ms_hi / n_hi : 0, t_lo = n_lo ? ms_lo / n_lo : 0;
+      double ratio = o.cost_ratio > 0 ? o.cost_ratio : (t_hi > 0 ? t_lo / t_hi : 0);
+      rep->cost_ratio = ratio;
+      rep->e_mvps = hi_mvps + lo_mvps * ratio;
+      rep->kkt_abs = kkt;
+      rep->kkt_rel = kkt_rel;
+      rep->objective = 0;
+      rep->ms_total = std::chrono::duration<double, std::milli>(t1 - t0).count();
+      rep->ms_hi = ms_hi;
+      rep->ms_lo = ms_lo;
+      rep->termination = term;
+    }
+    if (gm_fail) {
+      set_error("an inner GMRES solve did not converge");
+      return gm_fail;
+    }
+    if (term == 3) {
+      set_error("PQN stalled");
+      return BPQN_ERR_STALLED;
+    }
+    if (term == 2) {
+      set_error("PQN reached k_max");
+      return BPQN_ERR_NOCONV;
+    }
+    return BPQN_OK;
+  });
+}
+
+int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const double* b_host, double* x_host,
+                         const bpqn_solve_opts* opts, bpqn_report* rep) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(A && b_host && x_host && n > 0, "null pointer / bad size");
+    bpqn_solve_opts o;
+    bpqn_default_solve_opts(&o);
+    if (opts) o = *opts;
+    auto dense = [n](const double* M) -> MvpFn {
+      return [M, n](const std::vector<double>& v, std::vector<double>& out, std::vector<double>*) {
+        out.assign(n, 0.0);
+        for (int i = 0; i < n; ++i) {
+          double s = 0;
+          for (int j = 0; j < n; ++j) s += M[(size_t)i * n + j] * v[j];
+          out[i] = s;
+        }
+      };
+    };
+    std::vector<double> b(b_host, b_host + n), x0(x_host, x_host + n);
+    PqnOpts q = to_pqn(o);
+    int term;
+    if (Ahat && o.method == 1) {
+      BiResult r = bi_pqn(dense(A), dense(Ahat), b, x0, q);
+      std::copy(r.x.begin(), r.x.end(), x_host);
+      term = r.termination;
+      if (rep) {
+        *rep = bpqn_report{};
+        rep->iterations = r.iterations;
+        rep->hi_mvps = r.hi_mvps;
+        rep->lo_mvps = r.lo_mvps;
+        rep->kkt_abs = r.kkt;
+        rep->termination = term;
+      }
+    } else {
+      MonoResult r = mono_pqn(dense(A), b, x0, q, nullptr, nullptr, nullptr);
+      std::copy(r.x.begin(), r.x.end(), x_host);
+      term = r.termination;
+      if (rep) {
+        *rep = bpqn_report{};
+        rep->iterations = r.iterations;
+        rep->hi_mvps = r.mvps;
+        rep->kkt_abs = r.kkt;
+        rep->termination = term;
+      }
+    }
+    if (term == 3) return BPQN_ERR_STALLED;
+    if (term == 2) return BPQN_ERR_NOCONV;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_profile_get(bpqn_geom_t g, double* ms_allpairs, double* ms_near, double* ms_self,
+                     long long* allpairs_launches, long long* kernel_launches) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    if (ms_allpairs) *ms_allpairs = g->prof.ms_allpairs;
+    if (ms_near) *ms_near = g->prof.ms_near;
+    if (ms_self) *ms_self = g->prof.ms_self;
+    if (allpairs_launches) *allpairs_launches = g->prof.allpairs_launches;
+    if (kernel_launches) *kernel_launches = g->prof.launches;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_profile_reset(bpqn_geom_t g, int enable_events) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    g->prof.ms_allpairs = g->prof.ms_near = g->prof.ms_self = 0;
+    g->prof.allpairs_launches = g->prof.launches = 0;
+    g->prof.events = enable_events != 0;
+    return BPQN_OK;
+  });
+}
+
+}  // extern "C"

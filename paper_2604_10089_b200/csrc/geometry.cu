@@ -1,0 +1,586 @@
+// P0: geometry precompute for libbpqn (B200 / sm_100a).
+//
+// Builds, for one discretisation (readings R5-R8, R10):
+//  * the order-p grid (Gauss-Legendre in cos(theta) x trapezoid in phi),
+//  * the SH analysis matrix of the projection onto V_p (R7: quadrature analysis
+//    with the cos(p phi) sectoral coefficient halved, App. A.3 of SURVEY),
+//  * the per-sphere self operators E_S, E_L, E_A  (rotated singular grid, R5/R6;
+//    computed for one target per polar ring and expanded by the exact z-rotation
+//    symmetry of the grid),
+//  * the near-incidence correction matrices M_S, M_D (refined sinh-graded polar
+//    rule minus the coarse rule, R8), one [3][3nq] block per (target, sphere).
+// The paper names none of this (PAPER.md P:425-426 only gives the dof count and
+// cost); it is the discretisation frozen in DESIGN.md, implemented independently
+// of the CPU oracle.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "bpqn_internal.h"
+
+namespace bpqn {
+
+static const double PI = 3.14159265358979323846;
+
+// ------------------------------------------------------------------ host grids
+// Gauss-Legendre nodes by Newton iteration on P_n (own implementation), DESCENDING.
+void gauss_legendre_desc(int n, std::vector<double>& t, std::vector<double>& w) {
+  t.assign(n, 0.0);
+  w.assign(n, 0.0);
+  for (int i = 0; i < n; ++i) {
+    double x = std::cos(PI * (i + 0.75) / (n + 0.5));
+    double dp = 0;
+    for (int it = 0; it < 100; ++it) {
+      double p0 = 1.0, p1 = x;
+      for (int k = 2; k <= n; ++k) {
+        double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+        p0 = p1;
+        p1 = p2;
+      }
+      double pn = (n == 0) ? 1.0 : (n == 1 ? x : p1);
+      double pm1 = (n == 1) ? 1.0 : p0;
+      dp = n * (x * pn - pm1) / (x * x - 1.0);
+      double dx = pn / dp;
+      x -= dx;
+      if (std::fabs(dx) < 1e-16) {
+        // one more evaluation for the derivative at the converged node
+        p0 = 1.0;
+        p1 = x;
+        for (int k = 2; k <= n; ++k) {
+          double p2 = ((2.0 * k - 1.0) * x * p1 - (k - 1.0) * p0) / k;
+          p0 = p1;
+          p1 = p2;
+        }
+        pn = (n == 1) ? x : p1;
+        pm1 = (n == 1) ? 1.0 : p0;
+        dp = n * (x * pn - pm1) / (x * x - 1.0);
+        break;
+      }
+    }
+    t[i] = x;
+    w[i] = 2.0 / ((1.0 - x * x) * dp * dp);
+  }
+  // symmetrise (nodes come in +- pairs)
+  for (int i = 0; i < n / 2; ++i) {
+    double tt = 0.5 * (t[i] - t[n - 1 - i]);
+    double ww = 0.5 * (w[i] + w[n - 1 - i]);
+    t[i] = tt;
+    t[n - 1 - i] = -tt;
+    w[i] = w[n - 1 - i] = ww;
+  }
+  if (n % 2) t[n / 2] = 0.0;
+}
+
+void build_grid(int p, double a, Grid& g) {
+  g.p = p;
+  g.nq = (p + 1) * 2 * p;
+  gauss_legendre_desc(p + 1, g.t, g.omega);
+  g.theta.resize(p + 1);
+  for (int k = 0; k <= p; ++k) g.theta[k] = std::acos(g.t[k]);
+  g.phi.resize(2 * p);
+  for (int l = 0; l < 2 * p; ++l) g.phi[l] = PI * l / p;
+  g.xi.resize(3 * g.nq);
+  g.w.resize(g.nq);
+  for (int k = 0; k <= p; ++k)
+    for (int l = 0; l < 2 * p; ++l) {
+      int i = k * 2 * p + l;
+      double st = std::sqrt(std::max(0.0, 1.0 - g.t[k] * g.t[k]));
+      g.xi[3 * i] = st * std::cos(g.phi[l]);
+      g.xi[3 * i + 1] = st * std::sin(g.phi[l]);
+      g.xi[3 * i + 2] = g.t[k];
+      g.w[i] = a * a * g.omega[k] * PI / p;
+    }
+}
+
+int sh_count(int p) { return p * p + 2 * p; }
+
+// ------------------------------------------------------------------ device SH
+// Real orthonormal SH of V_p at a unit vector eta, one m-column at a time:
+//   Y^c_lm = sqrt(2 - d_m0) c_m Re[(x + i y)^m] R_lm(z),  Y^s_lm = sqrt2 c_m Im[...] R_lm(z)
+// with c_m = Q_mm / sin^m (Q normalised on the sphere) and R_lm = Q_lm/Q_mm by the
+// three-term recurrence.  Basis index: cos-type m = 0..p, l = m..p first
+// (offset m(p+1) - m(m-1)/2), then sin-type m = 1..p-1, l = m..p (sin p phi dropped).
+struct ShTables {
+  const double* ra;  // [(p+1)*(p+1)] recurrence a_lm at l*(p+1)+m
+  const double* rb;  // b_lm
+  const double* cm;  // [p+1]
+};
+
+__host__ __device__ inline int sh_cos_index(int p, int l, int m) { return m * (p + 1) - m * (m - 1) / 2 + (l - m); }
+__host__ __device__ inline int sh_sin_index(int p, int l, int m) {
+  int nc = (p + 1) * (p + 2) / 2;
+  int mm = m - 1;  // m >= 1
+  return nc + mm * p - mm * (mm - 1) / 2 + (l - m);
+}
+
+// writes Y for column m into out[idx*stride]
+__device__ void sh_column(int p, int m, double ex, double ey, double ez, const ShTables& T, double* out,
+                          int stride) {
+  // (x + i y)^m
+  double re = 1.0, im = 0.0;
+  for (int k = 0; k < m; ++k) {
+    double nr = re * ex - im * ey;
+    im = re * ey + im * ex;
+    re = nr;
+  }
+  const double s2 = 1.4142135623730951;
+  double cc = (m == 0) ? T.cm[0] : s2 * T.cm[m] * re;
+  double ss = s2 * T.cm[m] * im;
+  double rm2 = 0.0, rm1 = 0.0;
+  for (int l = m; l <= p; ++l) {
+    double r;
+    if (l == m) r = 1.0;
+    else if (l == m + 1) r = T.ra[l * (p + 1) + m] * ez;
+    else r = T.ra[l * (p + 1) + m] * (ez * rm1 - T.rb[l * (p + 1) + m] * rm2);
+    rm2 = rm1;
+    rm1 = r;
+    out[(size_t)sh_cos_index(p, l, m) * stride] = cc * r;
+    if (m >= 1 && m < p) out[(size_t)sh_sin_index(p, l, m) * stride] = ss * r;
+  }
+}
+
+static void sh_tables_host(int p, std::vector<double>& ra, std::vector<double>& rb, std::vector<double>& cm) {
+  ra.assign((p + 1) * (p + 1), 0.0);
+  rb.assign((p + 1) * (p + 1), 0.0);
+  cm.assign(p + 1, 0.0);
+  cm[0] = 1.0 / std::sqrt(4.0 * PI);
+  for (int m = 1; m <= p; ++m) cm[m] = cm[m - 1] * std::sqrt((2.0 * m + 1.0) / (2.0 * m));
+  for (int m = 0; m <= p; ++m)
+    for (int l = m + 1; l <= p; ++l) {
+      if (l == m + 1) {
+        ra[l * (p + 1) + m] = std::sqrt(2.0 * m + 3.0);
+      } else {
+        ra[l * (p + 1) + m] = std::sqrt((4.0 * l * l - 1.0) / ((double)l * l - (double)m * m));
+        rb[l * (p + 1) + m] =
+            std::sqrt(((l - 1.0) * (l - 1.0) - (double)m * m) / (4.0 * (l - 1.0) * (l - 1.0) - 1.0));
+      }
+    }
+}
+
+// analysis[b][j] = Y_b(xi_j) * omega_unit_j / G_bb (G = 2 for the cos(p phi) sectoral)
+__global__ void k_analysis(int p, int nq, const double* xi, const double* wunit, ShTables T, double* Yn,
+                           double* A, int nb) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nq) return;
+  double ex = xi[3 * j], ey = xi[3 * j + 1], ez = xi[3 * j + 2];
+  for (int m = 0; m <= p; ++m) sh_column(p, m, ex, ey, ez, T, Yn + j, nq);
+  int bnyq = sh_cos_index(p, p, p);
+  for (int b = 0; b < nb; ++b) A[(size_t)b * nq + j] = Yn[(size_t)b * nq + j] * wunit[j] * (b == bnyq ? 0.5 : 1.0);
+}
+
+// ------------------------------------------------------------------ quadrature -> rows
+// One CTA per quadrature problem.  kind 0: self rule for polar ring k (target at
+// (theta_k, phi = 0) on a sphere at the origin); kind 1: near rule for incidence
+// (target x_i, source sphere m).  Produces, for every source node j of the sphere,
+//   rowS[a][3j+c] = sum_s w_s G(x - y_s)[a][c]  Pi_j(eta_s)
+//   rowD[a][3j+c] = sum_s w_s K_D(x, y_s)[a][c] Pi_j(eta_s)
+// minus (kind 1) the coarse-rule terms w_j K(x - y_j) that the all-pairs kernel adds.
+struct QuadParams {
+  int p, nq, nb, kind;
+  double a, mu;
+  // self rule
+  int ns_t, ns_p;          // theta' nodes (p_s+1), phi' nodes (2 p_s)
+  const double* gl_self_t; // GL nodes on [-1,1] for theta' (p_s+1)
+  const double* gl_self_w;
+  const double* theta_ring;// [p+1]
+  // near rule
+  int n1, n2, nphi;
+  double theta_c;
+  const double* gl1_t; const double* gl1_w;
+  const double* gl2_t; const double* gl2_w;
+  const int* inc_t; const int* inc_m;
+  const double* X;         // [N][3]
+  const double* centers;   // [np][3]
+  // common
+  const double* xi;        // [nq][3]
+  const double* w;         // [nq]
+  const double* A;         // [nb][nq]
+  ShTables T;
+  double* outS;            // [nprob][3][3nq]
+  double* outD;
+  int want_s;
+};
+
+constexpr int QT = 256;      // threads
+constexpr int QPC = 16;      // points per chunk
+
+__device__ inline void rot_apply(const double R[9], double x, double y, double z, double& ox, double& oy,
+                                 double& oz) {
+  ox = R[0] * x + R[1] * y + R[2] * z;
+  oy = R[3] * x + R[4] * y + R[5] * z;
+  oz = R[6] * x + R[7] * y + R[8] * z;
+}
+
+__global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
+  extern __shared__ double sm[];
+  const int prob = blockIdx.x;
+  const int nb = P.nb, nq = P.nq, p = P.p;
+  // smem layout
+  double* sth = sm;                      // sin theta'     [ntheta <= 128]
+  double* cth = sth + 128;               // cos theta'
+  double* thw = cth + 128;               // theta' weights (incl. sin, a^2, dphi)
+  double* cph = thw + 128;               // cos phi'       [nphi <= 256]
+  double* sph = cph + 256;
+  double* Kc = sph + 256;                // [QPC][12]
+  double* Ys = Kc + QPC * 12;            // [QPC][nb]
+  double* Tm = Ys + QPC * nb;            // [12][nb]
+  __shared__ double R[9], tx[3], tc[3];
+  __shared__ int ntheta, nphi;
+
+  if (threadIdx.x == 0) {
+    double ex, ey, ez, cx = 0, cy = 0, cz = 0, x0, x1, x2;
+    if (P.kind == 0) {
+      double t = P.theta_ring[prob];
+      double c = cos(t), s = sin(t);
+      // R = R_y(theta_k)
+      R[0] = c; R[1] = 0; R[2] = s; R[3] = 0; R[4] = 1; R[5] = 0; R[6] = -s; R[7] = 0; R[8] = c;
+      x0 = P.a * s; x1 = 0; x2 = P.a * c;
+      ntheta = P.ns_t;
+      nphi = P.ns_p;
+    } else {
+      int i = P.inc_t[prob], m = P.inc_m[prob];
+      x0 = P.X[3 * i]; x1 = P.X[3 * i + 1]; x2 = P.X[3 * i + 2];
+      cx = P.centers[3 * m]; cy = P.centers[3 * m + 1]; cz = P.centers[3 * m + 2];
+      double rx = x0 - cx, ry = x1 - cy, rz = x2 - cz;
+      double d = sqrt(rx * rx + ry * ry + rz * rz);
+      ex = rx / d; ey = ry / d; ez = rz / d;
+      double te = acos(fmin(1.0, fmax(-1.0, ez)));
+      double pe = atan2(ey, ex);
+      double ct = cos(te), st = sin(te), cp = cos(pe), sp = sin(pe);
+      // R = R_z(pe) R_y(te)
+      R[0] = cp * ct; R[1] = -sp; R[2] = cp * st;
+      R[3] = sp * ct; R[4] = cp;  R[5] = sp * st;
+      R[6] = -st;     R[7] = 0;   R[8] = ct;
+      ntheta = P.n1 + P.n2;
+      nphi = P.nphi;
+    }
+    tx[0] = x0; tx[1] = x1; tx[2] = x2;
+    tc[0] = cx; tc[1] = cy; tc[2] = cz;
+  }
+  __syncthreads();
+  const int nth = ntheta, nph = nphi;
+  // theta' nodes and weights, phi' trig
+  for (int k = threadIdx.x; k < nth; k += QT) {
+    double tt, ww;
+    if (P.kind == 0) {
+      double t = P.gl_self_t[k], w = P.gl_self_w[k];
+      tt = 0.5 * PI * (t + 1.0);
+      ww = 0.5 * PI * w;
+    } else {
+      double rx = tx[0] - tc[0], ry = tx[1] - tc[1], rz = tx[2] - tc[2];
+      double delta = (sqrt(rx * rx + ry * ry + rz * rz) - P.a) / P.a;
+      if (k < P.n1) {
+        double S = asinh(P.theta_c / delta);
+        double s = 0.5 * S * (P.gl1_t[k] + 1.0);
+        tt = delta * sinh(s);
+        ww = 0.5 * S * P.gl1_w[k] * delta * cosh(s);
+      } else {
+        int kk = k - P.n1;
+        tt = P.theta_c + 0.5 * (PI - P.theta_c) * (P.gl2_t[kk] + 1.0);
+        ww = 0.5 * (PI - P.theta_c) * P.gl2_w[kk];
+      }
+    }
+    sth[k] = sin(tt);
+    cth[k] = cos(tt);
+    thw[k] = ww * sth[k] * P.a * P.a * (2.0 * PI / nph);
+  }
+  for (int l = threadIdx.x; l < nph; l += QT) {
+    double ph = 2.0 * PI * l / nph;
+    cph[l] = cos(ph);
+    sph[l] = sin(ph);
+  }
+  __syncthreads();
+
+  // accumulator tiles: 3 kk-blocks (4 each) x nb/2 b-blocks
+  const int nbb = (nb + 1) / 2;
+  const int ntile = 3 * nbb;
+  constexpr int MAXT = 4;  // tiles per thread (nb <= 2*QT*MAXT/3 ... checked on host)
+  double acc[MAXT][8];
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u)
+#pragma unroll
+    for (int v = 0; v < 8; ++v) acc[u][v] = 0.0;
+
+  const double cS = 1.0 / (8.0 * PI * P.mu);
+  const double cD = -3.0 / (4.0 * PI);
+  const int npts = nth * nph;
+  for (int s0 = 0; s0 < npts; s0 += QPC) {
+    // phase A1: points and kernels
+    for (int s = threadIdx.x; s < QPC; s += QT) {
+      int sg = s0 + s;
+      double k12[12];
+      double ex = 0, ey = 0, ez = 1;
+      if (sg < npts) {
+        int it = sg / nph, ip = sg - it * nph;
+        double st = sth[it], ct = cth[it];
+        rot_apply(R, st * cph[ip], st * sph[ip], ct, ex, ey, ez);
+        double wq = thw[it];
+        double r0 = tx[0] - (tc[0] + P.a * ex), r1 = tx[1] - (tc[1] + P.a * ey), r2 = tx[2] - (tc[2] + P.a * ez);
+        double rr = r0 * r0 + r1 * r1 + r2 * r2;
+        double ir = 1.0 / sqrt(rr), ir2 = ir * ir, ir3 = ir * ir2;
+        double gs = cS * wq;
+        // G: (I/rho + r r^T/rho^3) ; order xx,xy,xz,yy,yz,zz
+        k12[0] = gs * (ir + r0 * r0 * ir3); k12[1] = gs * r0 * r1 * ir3; k12[2] = gs * r0 * r2 * ir3;
+        k12[3] = gs * (ir + r1 * r1 * ir3); k12[4] = gs * r1 * r2 * ir3; k12[5] = gs * (ir + r2 * r2 * ir3);
+        double rn = r0 * ex + r1 * ey + r2 * ez;
+        double kd = cD * wq * rn * ir3 * ir2;
+        k12[6] = kd * r0 * r0; k12[7] = kd * r0 * r1; k12[8] = kd * r0 * r2;
+        k12[9] = kd * r1 * r1; k12[10] = kd * r1 * r2; k12[11] = kd * r2 * r2;
+      } else {
+        for (int q = 0; q < 12; ++q) k12[q] = 0.0;
+      }
+      for (int q = 0; q < 12; ++q) Kc[s * 12 + q] = k12[q];
+      // stash unit point in Ys row tail-free scratch: recompute in A2 instead
+    }
+    // phase A2: SH columns, work item = (s, m)
+    for (int wi = threadIdx.x; wi < QPC * (p + 1); wi += QT) {
+      int s = wi / (p + 1), m = wi - s * (p + 1);
+      int sg = s0 + s;
+      double ex = 0, ey = 0, ez = 1;
+      if (sg < npts) {
+        int it = sg / nph, ip = sg - it * nph;
+        double st = sth[it], ct = cth[it];
+        rot_apply(R, st * cph[ip], st * sph[ip], ct, ex, ey, ez);
+      }
+      sh_column(p, m, ex, ey, ez, P.T, Ys + s * nb, 1);
+    }
+    __syncthreads();
+    // phase B: acc += Kc^T Ys over this chunk
+#pragma unroll
+    for (int u = 0; u < MAXT; ++u) {
+      int tile = threadIdx.x + u * QT;
+      if (tile < ntile) {
+        int kb = tile / nbb, bb = tile - kb * nbb;
+        int b0 = 2 * bb;
+        bool two = (b0 + 1) < nb;
+        for (int s = 0; s < QPC; ++s) {
+          double y0 = Ys[s * nb + b0];
+          double y1 = two ? Ys[s * nb + b0 + 1] : 0.0;
+          const double* kr = Kc + s * 12 + 4 * kb;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            acc[u][2 * q] = fma(kr[q], y0, acc[u][2 * q]);
+            acc[u][2 * q + 1] = fma(kr[q], y1, acc[u][2 * q + 1]);
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // write T [12][nb]
+#pragma unroll
+  for (int u = 0; u < MAXT; ++u) {
+    int tile = threadIdx.x + u * QT;
+    if (tile < ntile) {
+      int kb = tile / nbb, bb = tile - kb * nbb;
+      int b0 = 2 * bb;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        Tm[(4 * kb + q) * nb + b0] = acc[u][2 * q];
+        if (b0 + 1 < nb) Tm[(4 * kb + q) * nb + b0 + 1] = acc[u][2 * q + 1];
+      }
+    }
+  }
+  __syncthreads();
+  // phase C: rows over source nodes j
+  const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};  // (a,c) -> packed symmetric index
+  double* oS = P.outS + (size_t)prob * 9 * nq;
+  double* oD = P.outD + (size_t)prob * 9 * nq;
+  for (int j = threadIdx.x; j < nq; j += QT) {
+    double r12[12];
+#pragma unroll
+    for (int q = 0; q < 12; ++q) r12[q] = 0.0;
+    for (int b = 0; b < nb; ++b) {
+      double av = P.A[(size_t)b * nq + j];
+#pragma unroll
+      for (int q = 0; q < 12; ++q) r12[q] = fma(Tm[q * nb + b], av, r12[q]);
+    }
+    if (P.kind == 1) {
+      // subtract the coarse rule for source node j of sphere m (what the all-pairs kernel adds)
+      double yx = tc[0] + P.a * P.xi[3 * j], yy = tc[1] + P.a * P.xi[3 * j + 1], yz = tc[2] + P.a * P.xi[3 * j + 2];
+      double r0 = tx[0] - yx, r1 = tx[1] - yy, r2 = tx[2] - yz;
+      double rr = r0 * r0 + r1 * r1 + r2 * r2;
+      double ir = 1.0 / sqrt(rr), ir2 = ir * ir, ir3 = ir * ir2;
+      double wq = P.w[j];
+      double gs = cS * wq;
+      r12[0] -= gs * (ir + r0 * r0 * ir3); r12[1] -= gs * r0 * r1 * ir3; r12[2] -= gs * r0 * r2 * ir3;
+      r12[3] -= gs * (ir + r1 * r1 * ir3); r12[4] -= gs * r1 * r2 * ir3; r12[5] -= gs * (ir + r2 * r2 * ir3);
+      double rn = r0 * P.xi[3 * j] + r1 * P.xi[3 * j + 1] + r2 * P.xi[3 * j + 2];
+      double kd = cD * wq * rn * ir3 * ir2;
+      r12[6] -= kd * r0 * r0; r12[7] -= kd * r0 * r1; r12[8] -= kd * r0 * r2;
+      r12[9] -= kd * r1 * r1; r12[10] -= kd * r1 * r2; r12[11] -= kd * r2 * r2;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        if (P.want_s) oS[(size_t)a * 3 * nq + 3 * j + c] = r12[sym[3 * a + c]];
+        oD[(size_t)a * 3 * nq + 3 * j + c] = r12[6 + sym[3 * a + c]];
+      }
+  }
+}
+
+// ------------------------------------------------------------------ self expansion
+// E_S[3i+a][3j+c] = (Rz(phi_l) Sring[k] Rz(phi_l)^T)[a][c] at j' = (k_j, l_j - l) - naive_S(i,j)
+// E_L likewise with Dring and naive_D; E_A = E_L - I/2 + Pi_R.
+__global__ void k_self_expand(int p, int nq, double a, double mu, const double* xi, const double* w,
+                              const double* phi, const double* Sring, const double* Dring, double* ES,
+                              double* EL, double* EA, int want_s) {
+  size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)nq * nq) return;
+  int i = (int)(idx / nq), j = (int)(idx % nq);
+  int tp = 2 * p;
+  int ki = i / tp, li = i % tp;
+  int kj = j / tp, lj = j % tp;
+  int jr = kj * tp + ((lj - li) % tp + tp) % tp;
+  double c = cos(phi[li]), s = sin(phi[li]);
+  double Rz[9] = {c, -s, 0, s, c, 0, 0, 0, 1};
+  const double PIl = 3.14159265358979323846;
+  const double cS = 1.0 / (8.0 * PIl * mu), cD = -3.0 / (4.0 * PIl);
+  double xi0 = a * xi[3 * i], xi1 = a * xi[3 * i + 1], xi2 = a * xi[3 * i + 2];
+  double yj0 = a * xi[3 * j], yj1 = a * xi[3 * j + 1], yj2 = a * xi[3 * j + 2];
+  double r[3] = {xi0 - yj0, xi1 - yj1, xi2 - yj2};
+  double rr = r[0] * r[0] + r[1] * r[1] + r[2] * r[2];
+  double nG[9] = {0}, nD[9] = {0};
+  if (i != j) {
+    double ir = 1.0 / sqrt(rr), ir3 = ir / rr;
+    double rn = (r[0] * xi[3 * j] + r[1] * xi[3 * j + 1] + r[2] * xi[3 * j + 2]);
+    for (int u = 0; u < 3; ++u)
+      for (int v = 0; v < 3; ++v) {
+        nG[3 * u + v] = cS * w[j] * ((u == v ? ir : 0.0) + r[u] * r[v] * ir3);
+        nD[3 * u + v] = cD * w[j] * rn * r[u] * r[v] * ir3 / rr;
+      }
+  }
+  for (int which = 0; which < 2; ++which) {
+    if (which == 0 && !want_s) continue;
+    const double* ring = (which == 0 ? Sring : Dring) + (size_t)ki * 9 * nq;
+    double B[9];
+    for (int u = 0; u < 3; ++u)
+      for (int v = 0; v < 3; ++v) B[3 * u + v] = ring[(size_t)u * 3 * nq + 3 * jr + v];
+    // Rz B Rz^T
+    double T1[9], Rt[9];
+    for (int u = 0; u < 3; ++u)
+      for (int v = 0; v < 3; ++v) {
+        double acc = 0;
+        for (int q = 0; q < 3; ++q) acc += Rz[3 * u + q] * B[3 * q + v];
+        T1[3 * u + v] = acc;
+      }
+    for (int u = 0; u < 3; ++u)
+      for (int v = 0; v < 3; ++v) {
+        double acc = 0;
+        for (int q = 0; q < 3; ++q) acc += T1[3 * u + q] * Rz[3 * v + q];
+        Rt[3 * u + v] = acc;
+      }
+    size_t ld = 3 * (size_t)nq;
+    if (which == 0) {
+      for (int u = 0; u < 3; ++u)
+        for (int v = 0; v < 3; ++v) ES[(3 * (size_t)i + u) * ld + 3 * j + v] = Rt[3 * u + v] - nG[3 * u + v];
+    } else {
+      double ri_rj = xi0 * yj0 + xi1 * yj1 + xi2 * yj2;
+      double ri[3] = {xi0, xi1, xi2}, rj[3] = {yj0, yj1, yj2};
+      double cu = w[j] / (4.0 * PIl * a * a), co = 3.0 * w[j] / (8.0 * PIl * a * a * a * a);
+      for (int u = 0; u < 3; ++u)
+        for (int v = 0; v < 3; ++v) {
+          double el = Rt[3 * u + v] - nD[3 * u + v];
+          EL[(3 * (size_t)i + u) * ld + 3 * j + v] = el;
+          double pir = (u == v ? cu + co * ri_rj : 0.0) - co * rj[u] * ri[v];
+          double half = (i == j && u == v) ? 0.5 : 0.0;
+          EA[(3 * (size_t)i + u) * ld + 3 * j + v] = el - half + pir;
+        }
+    }
+  }
+}
+
+// ------------------------------------------------------------------ driver
+void precompute(Geom& g, cudaStream_t st) {
+  const int p = g.p, nq = g.nq, nb = g.nb;
+  BPQN_REQUIRE(3 * ((nb + 1) / 2) <= QT * 4, "p too large for k_quad_rows tiles (p <= 26)");
+  BPQN_REQUIRE(g.nphi <= 256 && 2 * g.p_s <= 256 && g.n1 + g.n2 <= 128 && g.p_s + 1 <= 128,
+               "quadrature node counts exceed kernel limits");
+  std::vector<double> ra, rb, cm;
+  sh_tables_host(p, ra, rb, cm);
+  DBuf<double> d_ra, d_rb, d_cm;
+  d_ra.alloc(ra.size()); d_rb.alloc(rb.size()); d_cm.alloc(cm.size());
+  BPQN_CUDA(cudaMemcpyAsync(d_ra.p, ra.data(), ra.size() * 8, cudaMemcpyHostToDevice, st));
+  BPQN_CUDA(cudaMemcpyAsync(d_rb.p, rb.data(), rb.size() * 8, cudaMemcpyHostToDevice, st));
+  BPQN_CUDA(cudaMemcpyAsync(d_cm.p, cm.data(), cm.size() * 8, cudaMemcpyHostToDevice, st));
+  ShTables T{d_ra.p, d_rb.p, d_cm.p};
+
+  // analysis matrix
+  std::vector<double> wunit(nq);
+  for (int i = 0; i < nq; ++i) wunit[i] = g.grid.w[i] / (g.a * g.a);
+  DBuf<double> d_wunit, Yn;
+  d_wunit.alloc(nq);
+  Yn.alloc((size_t)nb * nq);
+  BPQN_CUDA(cudaMemcpyAsync(d_wunit.p, wunit.data(), nq * 8, cudaMemcpyHostToDevice, st));
+  g.analysis.alloc((size_t)nb * nq);
+  k_analysis<<<(nq + 127) / 128, 128, 0, st>>>(p, nq, g.xi_d.p, d_wunit.p, T, Yn.p, g.analysis.p, nb);
+  BPQN_CHECK_LAUNCH();
+
+  // GL tables
+  std::vector<double> t_s, w_s, t1, w1, t2, w2;
+  gauss_legendre_desc(g.p_s + 1, t_s, w_s);
+  gauss_legendre_desc(g.n1, t1, w1);
+  gauss_legendre_desc(g.n2, t2, w2);
+  DBuf<double> dts, dws, dt1, dw1, dt2, dw2, dth;
+  auto up = [&](DBuf<double>& d, const std::vector<double>& h) {
+    d.alloc(h.size());
+    BPQN_CUDA(cudaMemcpyAsync(d.p, h.data(), h.size() * 8, cudaMemcpyHostToDevice, st));
+  };
+  up(dts, t_s); up(dws, w_s); up(dt1, t1); up(dw1, w1); up(dt2, t2); up(dw2, w2); up(dth, g.grid.theta);
+  DBuf<double> dphi;
+  up(dphi, g.grid.phi);
+
+  QuadParams P{};
+  P.p = p; P.nq = nq; P.nb = nb; P.a = g.a; P.mu = g.mu;
+  P.ns_t = g.p_s + 1; P.ns_p = 2 * g.p_s;
+  P.gl_self_t = dts.p; P.gl_self_w = dws.p; P.theta_ring = dth.p;
+  P.n1 = g.n1; P.n2 = g.n2; P.nphi = g.nphi; P.theta_c = 1.0;
+  P.gl1_t = dt1.p; P.gl1_w = dw1.p; P.gl2_t = dt2.p; P.gl2_w = dw2.p;
+  P.X = g.X.p; P.centers = g.centers_d.p;
+  P.xi = g.xi_d.p; P.w = g.w_d.p; P.A = g.analysis.p; P.T = T;
+  size_t smem = (128 + 128 + 128 + 256 + 256 + QPC * 12 + (size_t)QPC * nb + 12 * (size_t)nb) * sizeof(double);
+  BPQN_CUDA(cudaFuncSetAttribute(k_quad_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+
+  // self rings
+  DBuf<double> Sring, Dring;
+  Sring.alloc((size_t)(p + 1) * 9 * nq);
+  Dring.alloc((size_t)(p + 1) * 9 * nq);
+  P.kind = 0; P.outS = Sring.p; P.outD = Dring.p; P.want_s = 1;
+  k_quad_rows<<<p + 1, QT, smem, st>>>(P);
+  BPQN_CHECK_LAUNCH();
+  size_t ne = (size_t)3 * nq * 3 * nq;
+  if (g.single_layer) g.E_S.alloc(ne);
+  g.E_L.alloc(ne);
+  g.E_A.alloc(ne);
+  size_t nn = (size_t)nq * nq;
+  k_self_expand<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p, nq, g.a, g.mu, g.xi_d.p, g.w_d.p, dphi.p,
+                                                             Sring.p, Dring.p, g.E_S.p, g.E_L.p, g.E_A.p,
+                                                             g.single_layer ? 1 : 0);
+  BPQN_CHECK_LAUNCH();
+
+  // near incidences
+  if (g.n_inc > 0) {
+    size_t per = (size_t)9 * nq;
+    g.M_D.alloc((size_t)g.n_inc * per);
+    if (g.single_layer) g.M_S.alloc((size_t)g.n_inc * per);
+    P.kind = 1; P.inc_t = g.inc_t.p; P.inc_m = g.inc_m.p;
+    P.want_s = g.single_layer ? 1 : 0;
+    // batch to keep grids modest
+    const long long batch = 65535;
+    for (long long b0 = 0; b0 < g.n_inc; b0 += batch) {
+      long long nbt = std::min(batch, g.n_inc - b0);
+      QuadParams Q = P;
+      Q.inc_t = g.inc_t.p + b0;
+      Q.inc_m = g.inc_m.p + b0;
+      Q.outD = g.M_D.p + b0 * per;
+      Q.outS = g.single_layer ? g.M_S.p + b0 * per : g.M_D.p + b0 * per;  // unused when !want_s
+      k_quad_rows<<<(unsigned)nbt, QT, smem, st>>>(Q);
+      BPQN_CHECK_LAUNCH();
+    }
+  }
+  BPQN_CUDA(cudaStreamSynchronize(st));
+}
+
+}  // namespace bpqn

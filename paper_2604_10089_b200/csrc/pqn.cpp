@@ -1,0 +1,471 @@
+// H1: host-side Mono-PQN / Bi-PQN (the paper's outer loop) for libbpqn.
+//
+// Alg. 1 Mono-PQN, Alg. 2 optimal over-relaxation
+// (P:372-388), Alg. 3 Bi-PQN, Prop. 1 / Alg. 4 weighted prox via
+// semi-smooth Newton, unrolled full-memory BFGS (App. D.1
+// P:802-810), cached low-fidelity secant (App. D.2).  Readings R11
+// (x~ = x - tau H g), R15 (prox residual with the +[a; a~] term), R16-R19, R22.
+//
+// Runs on the host: Nc <= 540 and rank r <= ~60 make every step O(Nc r^2) ~ tens of
+// microseconds, against an MVP of milliseconds to seconds; one Nc-vector crosses
+// PCIe per MVP.  C^{-1} = (D + UU^T)^{-1} is applied by the Woodbury identity.
+#include <algorithm>
+#include <cmath>
+#include <functional>
+#include <limits>
+#include <stdexcept>
+#include <vector>
+
+#include "pqn.h"
+
+namespace bpqn {
+
+using Vec = std::vector<double>;
+
+static double dot(const Vec& a, const Vec& b) {
+  double s = 0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+static double nrm(const Vec& a) { return std::sqrt(dot(a, a)); }
+
+// dense LU solve (partial pivoting) of a small system; returns false if singular
+static bool lu_solve(std::vector<double> A, int n, Vec& b) {
+  std::vector<int> piv(n);
+  for (int k = 0; k < n; ++k) {
+    int pm = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(A[i * n + k]) > std::fabs(A[pm * n + k])) pm = i;
+    if (A[pm * n + k] == 0.0) return false;
+    if (pm != k) {
+      for (int j = 0; j < n; ++j) std::swap(A[k * n + j], A[pm * n + j]);
+      std::swap(b[k], b[pm]);
+    }
+    for (int i = k + 1; i < n; ++i) {
+      double f = A[i * n + k] / A[k * n + k];
+      for (int j = k; j < n; ++j) A[i * n + j] -= f * A[k * n + j];
+      b[i] -= f * b[k];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < n; ++j) s -= A[i * n + j] * b[j];
+    b[i] = s / A[i * n + i];
+  }
+  return true;
+}
+
+double kkt_abs(const Vec& x, const Vec& g) {
+  double s = 0;
+  for (size_t i = 0; i < x.size(); ++i) {
+    double m = std::min(x[i], g[i]);
+    s += m * m;
+  }
+  return std::sqrt(s);
+}
+
+// ------------------------------------------------------------------ BFGS
+void Bfgs::clear() {
+  U.clear();
+  V.clear();
+  S.clear();
+  Y.clear();
+}
+Vec Bfgs::B(const Vec& x) const {
+  Vec out = x;
+  for (auto& u : U) {
+    double c = dot(u, x);
+    for (size_t i = 0; i < out.size(); ++i) out[i] += c * u[i];
+  }
+  for (auto& v : V) {
+    double c = dot(v, x);
+    for (size_t i = 0; i < out.size(); ++i) out[i] -= c * v[i];
+  }
+  return out;
+}
+Vec Bfgs::H(const Vec& g) const {
+  Vec q = g;
+  std::vector<double> al(S.size());
+  for (int k = (int)S.size() - 1; k >= 0; --k) {
+    double rho = 1.0 / dot(Y[k], S[k]);
+    al[k] = rho * dot(S[k], q);
+    for (size_t i = 0; i < q.size(); ++i) q[i] -= al[k] * Y[k][i];
+  }
+  for (size_t k = 0; k < S.size(); ++k) {
+    double rho = 1.0 / dot(Y[k], S[k]);
+    double be = rho * dot(Y[k], q);
+    for (size_t i = 0; i < q.size(); ++i) q[i] += S[k][i] * (al[k] - be);
+  }
+  return q;
+}
+bool Bfgs::update(const Vec& s, const Vec& y, const Vec* Bs_in, double curv) {
+  double ys = dot(y, s);
+  if (!std::isfinite(ys)) throw std::runtime_error("NaN in BFGS update");
+  if (ys <= curv * nrm(s) * nrm(y)) return false;
+  Vec Bs = Bs_in ? *Bs_in : B(s);
+  double sBs = dot(s, Bs);
+  if (!(sBs > 0)) return false;
+  Vec u(s.size()), v(s.size());
+  double a = 1.0 / std::sqrt(ys), b = 1.0 / std::sqrt(sBs);
+  for (size_t i = 0; i < s.size(); ++i) {
+    u[i] = a * y[i];
+    v[i] = b * Bs[i];
+  }
+  U.push_back(u);
+  V.push_back(v);
+  S.push_back(s);
+  Y.push_back(y);
+  return true;
+}
+
+// ------------------------------------------------------------------ weighted prox
+// prox^B_{x>=0}(x~), B = I + UU^T - VV^T (D = I in both solvers, R19)
+Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters) {
+  const int n = (int)xt.size();
+  const int r = (int)q.U.size();
+  if (r == 0) {
+    Vec z(n);
+    for (int i = 0; i < n; ++i) z[i] = std::max(xt[i], 0.0);
+    if (iters) *iters = 0;
+    return z;
+  }
+  if (tol <= 0) {
+    double mx = 1.0;
+    for (double v : xt) mx = std::max(mx, std::fabs(v));
+    tol = 1e-12 * mx;
+  }
+  // Woodbury: C^{-1} V = V - U (I + U^T U)^{-1} U^T V
+  std::vector<double> K(r * r);
+  for (int i = 0; i < r; ++i)
+    for (int j = 0; j < r; ++j) K[i * r + j] = dot(q.U[i], q.U[j]) + (i == j ? 1.0 : 0.0);
+  std::vector<Vec> CV(r, Vec(n));
+  for (int c = 0; c < r; ++c) {
+    Vec rhs(r);
+    for (int i = 0; i < r; ++i) rhs[i] = dot(q.U[i], q.V[c]);
+    if (!lu_solve(K, r, rhs)) throw std::runtime_error("singular Woodbury core");
+    for (int e = 0; e < n; ++e) {
+      double s = q.V[c][e];
+      for (int i = 0; i < r; ++i) s -= q.U[i][e] * rhs[i];
+      CV[c][e] = s;
+    }
+  }
+  const int d = 2 * r;
+  Vec al(d, 0.0);  // [alpha; alpha~]
+  auto residual = [&](const Vec& a, Vec& L, Vec& z, std::vector<char>& act) {
+    Vec y = xt;
+    for (int c = 0; c < r; ++c)
+      for (int e = 0; e < n; ++e) y[e] += CV[c][e] * a[r + c];
+    z.assign(n, 0.0);
+    act.assign(n, 0);
+    for (int e = 0; e < n; ++e) {
+      double v = y[e];
+      for (int c = 0; c < r; ++c) v -= q.U[c][e] * a[c];
+      if (v > 0) {
+        z[e] = v;
+        act[e] = 1;
+      }
+    }
+    L.assign(d, 0.0);
+    for (int c = 0; c < r; ++c) {
+      double s1 = 0, s2 = 0;
+      for (int e = 0; e < n; ++e) {
+        s1 += q.U[c][e] * (y[e] - z[e]);
+        s2 += q.V[c][e] * (xt[e] - z[e]);
+      }
+      L[c] = a[c] + s1;
+      L[r + c] = a[r + c] + s2;
+    }
+  };
+  auto infn = [](const Vec& v) {
+    double m = 0;
+    for (double x : v) m = std::max(m, std::fabs(x));
+    return m;
+  };
+  Vec L, z;
+  std::vector<char> act;
+  residual(al, L, z, act);
+  double nr = infn(L);
+  int j = 0;
+  for (j = 0; j < jmax && nr > tol; ++j) {
+    // J = [[U^T Lam U, U^T (I-Lam) CV], [V^T Lam U, -V^T Lam CV]] + I
+    std::vector<double> J(d * d, 0.0);
+    for (int a = 0; a < r; ++a)
+      for (int b = 0; b < r; ++b) {
+        double uu = 0, ucv = 0, vu = 0, vcv = 0;
+        for (int e = 0; e < n; ++e) {
+          if (act[e]) {
+            uu += q.U[a][e] * q.U[b][e];
+            vu += q.V[a][e] * q.U[b][e];
+            vcv += q.V[a][e] * CV[b][e];
+          } else {
+            ucv += q.U[a][e] * CV[b][e];
+          }
+        }
+        J[a * d + b] = uu;
+        J[a * d + r + b] = ucv;
+        J[(r + a) * d + b] = vu;
+        J[(r + a) * d + r + b] = -vcv;
+      }
+    for (int i = 0; i < d; ++i) J[i * d + i] += 1.0;
+    Vec step = L;
+    if (!lu_solve(J, d, step)) {
+      double jn = 0;
+      for (double v : J) jn = std::max(jn, std::fabs(v));
+      for (int i = 0; i < d; ++i) J[i * d + i] += 1e-10 * jn * d;
+      step = L;
+      if (!lu_solve(J, d, step)) break;
+    }
+    double t = 1.0;
+    bool ok = false;
+    Vec a2(d), L2, z2;
+    std::vector<char> act2;
+    double n2 = nr;
+    for (int h = 0; h < 30; ++h) {
+      for (int i = 0; i < d; ++i) a2[i] = al[i] - t * step[i];
+      residual(a2, L2, z2, act2);
+      n2 = infn(L2);
+      if (n2 < nr || n2 <= tol) {
+        ok = true;
+        break;
+      }
+      t *= 0.5;
+    }
+    if (!ok) break;
+    double smax = t * infn(step);
+    al = a2;
+    L = L2;
+    z = z2;
+    act = act2;
+    nr = n2;
+    if (smax < tol) {
+      ++j;
+      break;
+    }
+  }
+  if (iters) *iters = j;
+  return z;
+}
+
+// ------------------------------------------------------------------ Alg. 2
+double optimal_eta(const Vec& x, const Vec& p, const Vec& g, const Vec& Ap, std::vector<char>& bind) {
+  double pAp = dot(p, Ap), pg = dot(p, g);
+  double eu = pAp > 0 ? -pg / pAp : std::numeric_limits<double>::infinity();
+  double eh = std::numeric_limits<double>::infinity();
+  for (size_t i = 0; i < x.size(); ++i)
+    if (p[i] < 0) eh = std::min(eh, -x[i] / p[i]);
+  bind.assign(x.size(), 0);
+  if (eh < eu) {
+    for (size_t i = 0; i < x.size(); ++i)
+      if (p[i] < 0 && -x[i] / p[i] == eh) bind[i] = 1;
+    return eh;
+  }
+  return eu;
+}
+
+// ------------------------------------------------------------------ Alg. 1
+MonoResult mono_pqn(const MvpFn& mvp, const Vec& b, const Vec& x0, const PqnOpts& o, const Vec* g0,
+                    const Vec* aux0, const std::vector<std::pair<Vec, Vec>>* seed) {
+  const size_t n = b.size();
+  MonoResult R;
+  R.x = x0;
+  Vec Ax(n), aux(n);
+  bool track = false;
+  if (!g0) {
+    mvp(R.x, Ax, &aux);
+    R.mvps++;
+    R.g.resize(n);
+    for (size_t i = 0; i < n; ++i) R.g[i] = Ax[i] + b[i];
+    R.aux = aux;
+    track = true;
+  } else {
+    R.g = *g0;
+    if (aux0) {
+      R.aux = *aux0;
+      track = true;
+    }
+  }
+  Bfgs q;
+  if (seed)
+    for (auto& sy : *seed) q.update(sy.first, sy.second, nullptr, o.curv);
+  double prev = -1;
+  bool reset_done = false;
+  R.termination = 2;
+  int k;
+  for (k = 0; k < o.k_max; ++k) {
+    double e = kkt_abs(R.x, R.g);
+    double rel = prev < 0 ? std::numeric_limits<double>::infinity()
+                          : (std::max(e, prev) > 0 ? std::fabs(e - prev) / std::max(e, prev) : 0.0);
+    prev = e;
+    R.kkt = e;
+    R.kkt_rel = rel;
+    if (e <= o.eps_abs) {
+      R.termination = 0;
+      break;
+    }
+    if (o.eps_rel > 0 && rel <= o.eps_rel) {
+      R.termination = 1;
+      break;
+    }
+    Vec hg = q.H(R.g), xt(n);
+    for (size_t i = 0; i < n; ++i) xt[i] = R.x[i] - o.tau * hg[i];
+    int pit = 0;
+    Vec xh = weighted_prox(q, xt, o.prox_tol, o.prox_jmax, &pit);
+    Vec p(n);
+    for (size_t i = 0; i < n; ++i) p[i] = xh[i] - R.x[i];
+    Vec Ap(n), auxp(n);
+    mvp(p, Ap, &auxp);
+    R.mvps++;
+    std::vector<char> bind;
+    double eta = optimal_eta(R.x, p, R.g, Ap, bind);
+    if (!(eta > 0 && std::isfinite(eta)) || dot(p, R.g) >= 0) {
+      if (reset_done) {
+        R.termination = 3;
+        break;
+      }
+      q.clear();
+      reset_done = true;
+      continue;
+    }
+    reset_done = false;
+    for (size_t i = 0; i < n; ++i) {
+      R.x[i] += eta * p[i];
+      if (bind[i]) R.x[i] = 0.0;
+      R.g[i] += eta * Ap[i];
+      if (track) R.aux[i] += eta * auxp[i];
+    }
+    R.iterations++;
+    Vec s(n), y(n);
+    for (size_t i = 0; i < n; ++i) {
+      s[i] = eta * p[i];
+      y[i] = eta * Ap[i];
+    }
+    q.update(s, y, nullptr, o.curv);
+    if (o.refresh > 0 && R.iterations % o.refresh == 0) {
+      mvp(R.x, Ax, &aux);
+      R.mvps++;
+      for (size_t i = 0; i < n; ++i) R.g[i] = Ax[i] + b[i];
+      if (track) R.aux = aux;
+    }
+  }
+  if (k == o.k_max) R.kkt = kkt_abs(R.x, R.g);
+  for (size_t i = 0; i < q.S.size(); ++i) R.pairs.emplace_back(q.S[i], q.Y[i]);
+  return R;
+}
+
+// ------------------------------------------------------------------ Alg. 3
+BiResult bi_pqn(const MvpFn& hi, const MvpFn& lo, const Vec& b, const Vec& x_init, const PqnOpts& o) {
+  const size_t n = b.size();
+  BiResult R;
+  // low-fidelity initialisation: lo MVP returns A^ v, aux = A^ v
+  MvpFn lo_aux = [&](const Vec& v, Vec& out, Vec* aux) {
+    lo(v, out, nullptr);
+    if (aux) *aux = out;
+  };
+  MonoResult r0 = mono_pqn(lo_aux, b, x_init, o, nullptr, nullptr, nullptr);
+  R.lo_mvps += r0.mvps;
+  Vec x = r0.x, Ahat_x = r0.aux;
+  std::vector<std::pair<Vec, Vec>> low = r0.pairs;
+  Vec g(n);
+  hi(x, g, nullptr);
+  R.hi_mvps++;
+  for (size_t i = 0; i < n; ++i) g[i] += b[i];
+  std::vector<Vec> U, V;
+  auto Bhi = [&](const Vec& v, const Vec& Ahat_v) {
+    Vec out = Ahat_v;
+    for (auto& u : U) {
+      double c = dot(u, v);
+      for (size_t i = 0; i < n; ++i) out[i] += c * u[i];
+    }
+    for (auto& w : V) {
+      double c = dot(w, v);
+      for (size_t i = 0; i < n; ++i) out[i] -= c * w[i];
+    }
+    return out;
+  };
+  double prev = -1;
+  R.termination = 2;
+  int k;
+  for (k = 0; k < o.k_max; ++k) {
+    double e = kkt_abs(x, g);
+    double rel = prev < 0 ? std::numeric_limits<double>::infinity()
+                          : (std::max(e, prev) > 0 ? std::fabs(e - prev) / std::max(e, prev) : 0.0);
+    prev = e;
+    R.kkt = e;
+    R.kkt_rel = rel;
+    if (e <= o.eps_abs) {
+      R.termination = 0;
+      break;
+    }
+    if (o.eps_rel > 0 && rel <= o.eps_rel) {
+      R.termination = 1;
+      break;
+    }
+    Vec Bx = Bhi(x, Ahat_x), c(n);
+    for (size_t i = 0; i < n; ++i) c[i] = g[i] - Bx[i];
+    int sub_lo = 0;
+    MvpFn sub = [&](const Vec& v, Vec& out, Vec* aux) {
+      Vec Av(n);
+      lo(v, Av, nullptr);
+      sub_lo++;
+      out = Bhi(v, Av);
+      if (aux) *aux = Av;
+    };
+    PqnOpts so = o;
+    so.eps_abs = o.sub_eps_factor * o.eps_abs;
+    so.eps_rel = 0;
+    so.k_max = o.sub_k_max;
+    MonoResult rs = mono_pqn(sub, c, x, so, &g, &Ahat_x, &low);
+    R.lo_mvps += sub_lo;
+    R.sub_iterations.push_back(rs.iterations);
+    Vec p(n);
+    for (size_t i = 0; i < n; ++i) p[i] = rs.x[i] - x[i];
+    Vec Ap(n);
+    hi(p, Ap, nullptr);
+    R.hi_mvps++;
+    std::vector<char> bind;
+    double eta = optimal_eta(x, p, g, Ap, bind);
+    if (!(eta > 0 && std::isfinite(eta))) {
+      R.termination = 3;
+      break;
+    }
+    Vec s(n), y(n), Ahat_s(n);
+    for (size_t i = 0; i < n; ++i) {
+      x[i] += eta * p[i];
+      if (bind[i]) x[i] = 0.0;
+      g[i] += eta * Ap[i];
+      s[i] = eta * p[i];
+      y[i] = eta * Ap[i];
+      Ahat_s[i] = eta * (rs.aux[i] - Ahat_x[i]);
+    }
+    R.iterations++;
+    Vec Bs = Bhi(s, Ahat_s);
+    double ys = dot(y, s), sBs = dot(s, Bs);
+    low = rs.pairs;
+    if (ys > o.curv * nrm(s) * nrm(y) && sBs > 0) {
+      Vec u(n), v(n);
+      for (size_t i = 0; i < n; ++i) {
+        u[i] = y[i] / std::sqrt(ys);
+        v[i] = Bs[i] / std::sqrt(sBs);
+      }
+      U.push_back(u);
+      V.push_back(v);
+      for (auto& sy : low) {
+        double cu = dot(u, sy.first), cv = dot(v, sy.first);
+        for (size_t i = 0; i < n; ++i) sy.second[i] += -cu * u[i] + cv * v[i];
+      }
+    }
+    for (size_t i = 0; i < n; ++i) Ahat_x[i] += Ahat_s[i];
+    if (o.refresh > 0 && R.iterations % o.refresh == 0) {
+      hi(x, g, nullptr);
+      R.hi_mvps++;
+      for (size_t i = 0; i < n; ++i) g[i] += b[i];
+    }
+  }
+  if (k == o.k_max) R.kkt = kkt_abs(x, g);
+  R.x = x;
+  R.g = g;
+  R.init_iterations = r0.iterations;
+  return R;
+}
+
+}  // namespace bpqn

@@ -4,4 +4,4 @@ Holds NONE of the method's arithmetic (no grids, kernels, contacts or solvers):
 only the seeded random draws and the five BASELINE.json configurations.  This is
 the one module both ``oracle/`` (via tests) and the product harness may import.
 """
-from .configs import CONFIGS, make_config, lambda_test, layer_densities  # noqa: F401
+from .configs import CONFIGS, ft_test, lambda_test, layer_densities, make_config  # noqa: F401

@@ -77,3 +77,9 @@ def lambda_test(c, nc, k=0):
     """k-th seeded MVP test vector, U(0,1)^nc."""
     rng = np.random.default_rng(20260000 + c + 2000 + k)
     return rng.uniform(0.0, 1.0, size=nc)
+
+
+def ft_test(c, npart):
+    """Seeded force/torque test vector [Np,6] N(0,1) for mobility parity."""
+    rng = np.random.default_rng(20260000 + c + 3000)
+    return rng.standard_normal((npart, 6))
