@@ -1,0 +1,386 @@
+"""bench.py -- the LCP MVP hot path of arXiv 2604.10089 on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config 4] [--gmres-tol 1e-8] [--no-c5]
+
+A step is one LCP matrix-vector product w = D^T M D lambda (every
+row of SURVEY 8(a): contacts, D scatter + P^T, RHS single-layer pass, GMRES on the
+completed double-layer equation with K1/K2/K3 + device Arnoldi, rigid read-out,
+D^T gather) at BASELINE.json config c4 (216 spheres, p = 16, N = 117 504 surface
+points), lambda resident in HBM.  Timing: CUDA events around each step on the
+launching stream, L2 flushed (256 MiB write) between steps outside the events;
+W untimed warm-up steps; max over ranks.  The c5 line (one all-pairs S+D layer
+apply with near and self parts, 259 200 points) gives pair-interactions/s.
+
+N > 1 (torchrun): "replicas only" -- every rank runs its own independent LCP MVP
+(weak scaling, no data-path collective).
+
+--impl reference times the CPU oracle (oracle/, the only other place bench.py
+executes it) on a bounded sample of the same workload; rank 0 only.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: SMs x FP64 FMA lanes/clk x 2 x max clock
+METRIC = "ms per LCP MVP (c4: 216 spheres, p=16)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--gmres-tol", type=float, default=1e-8)   # paper's hi-fidelity eps_gmres (R9)
+    ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--c5-steps", type=int, default=3)
+    ap.add_argument("--cpu-sample-targets", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 7:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        sm, reasons, mx, pw = [], set(), None, []
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                pw.append(float(r[2]))
+            except ValueError:
+                continue
+            for k, name in enumerate(names):
+                if r[3 + k].lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm), "power_w_max": max(pw) if pw else None}
+
+
+# ---------------------------------------------------------------- distributed plumbing
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+        backend = "nccl" if args.impl == "ours" else "gloo"
+        dist.init_process_group(backend=backend)
+    return ws, rank, local
+
+
+def barrier(ws):
+    if ws > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(ws, v, device):
+    if ws == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------- oracle timing (cpu_baseline / reference)
+def oracle_mvp_sample(cfg, n_targets, k_g):
+    """Oracle (oracle/native.py plain-C direct sum, all host cores) timed on a bounded
+    sample of one LCP MVP: the coarse stresslet pass for n_targets of the N targets
+    over all N sources.  ms per MVP = t x (N / n_targets) x (k_g + 1) passes."""
+    from oracle import native
+    from oracle.grid import sphere_grid
+    native.build()
+    grid = sphere_grid(cfg["p"], cfg["radius"])
+    X = (cfg["centers"][:, None, :] + cfg["radius"] * grid["xi"][None]).reshape(-1, 3)
+    NRM = np.tile(grid["xi"], (cfg["np"], 1))
+    W = np.tile(grid["w"], cfg["np"])
+    N = X.shape[0]
+    rng = np.random.default_rng(7)
+    q = rng.standard_normal((N, 3))
+    idx = np.sort(rng.choice(N, size=n_targets, replace=False))
+    tsph = idx // grid["xi"].shape[0]            # far_sum skips each target's own sphere
+    excl_ptr = np.zeros(n_targets + 1, dtype=np.int64)
+    t0 = time.perf_counter()
+    native.far_sum(X[idx], tsph, excl_ptr, np.zeros(0, dtype=np.int64), cfg["np"], grid["xi"].shape[0], X, NRM,
+                   W, None, q, cfg["mu"])
+    dt = time.perf_counter() - t0
+    passes = k_g + 1
+    ms = dt * 1e3 * (N / n_targets) * passes
+    return ms, dt, N, passes
+
+
+def oracle_kg(c):
+    """GMRES iterations of the oracle's own MVP at config c (from its fixture), else None."""
+    for cc in (c, 3, 2, 1):
+        path = os.path.join(ROOT, "tests", "fixtures", "c%d.npz" % cc)
+        if os.path.exists(path):
+            z = np.load(path, allow_pickle=True)
+            if "gmres_iters_mvp" in z:
+                return int(np.atleast_1d(z["gmres_iters_mvp"])[0]), cc
+            if "gmres_iters_mob" in z:
+                return int(z["gmres_iters_mob"]), cc
+    return 80, None
+
+
+def cores_used():
+    return int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+
+
+def run_reference(args, ws, rank):
+    from synth import make_config
+    if rank != 0:
+        return
+    cfg = make_config(args.config)
+    k_g, src = oracle_kg(args.config)
+    n_t = args.cpu_sample_targets or 256
+    times = []
+    for _ in range(args.warmup):
+        oracle_mvp_sample(cfg, n_t, k_g)
+    for _ in range(args.steps):
+        ms, dt, N, passes = oracle_mvp_sample(cfg, n_t, k_g)
+        times.append(ms)
+    v = float(np.mean(times))
+    sample = ("oracle plain-C fp64 coarse stresslet pass for %d of %d targets x all sources, scaled by N/%d x "
+              "(k_g+1 = %d) passes (k_g from the oracle's c%s fixture); near/self parts not included" %
+              (n_t, N, n_t, passes, src))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "ms", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v, "higher_is_better": False,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c%d LCP MVP" % args.config, "spheres": cfg["np"], "p": cfg["p"], "N": N},
+            "cpu_baseline": {"value": v, "unit": "ms", "cores": cores_used(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args, ws, rank, local):
+    import torch
+    import paper_2604_10089_b200 as bp
+    from synth import make_config
+
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device (the product has no CPU fallback)")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    cfg = make_config(args.config)
+    t0 = time.time()
+    g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+    torch.cuda.synchronize()
+    t_init = time.time() - t0
+    pairs, nrm, gaps = bp.contacts(g, cfg["delta"])
+    nc = g.nc
+    rng = np.random.default_rng(20260000 + args.config + 2000)     # synth.lambda_test recipe
+    lam_h = rng.uniform(0.0, 1.0, size=nc)
+    lam = torch.tensor(lam_h, dtype=torch.float64, device=dev)
+    w = torch.empty(nc, dtype=torch.float64, device=dev)
+    gm = bp.default_gmres_opts(tol=args.gmres_tol)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def step():
+        bp.contacts(g, cfg["delta"])                  # A1 (K5) every step
+        _, st = bp.lcp_mvp(g, lam, out=w, gmres=gm)   # A2-A5
+        return st
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    bp.profile_reset(g, events=True)
+    launches0 = bp.profile_get(g)["kernel_launches"]
+    clk = ClockSampler(local)
+    clk.start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    gm_iters = []
+    barrier(ws)
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        ev[k][0].record(stream)
+        st = step()
+        ev[k][1].record(stream)
+        gm_iters.append(st.iters)
+    torch.cuda.synchronize()
+    barrier(ws)
+    clocks = clk.stop()
+    prof = bp.profile_get(g)
+    ms_steps = [a.elapsed_time(b) for a, b in ev]
+    total_ms = max_over_ranks(ws, float(np.sum(ms_steps)), dev)
+    ms_per_step = total_ms / args.steps
+    launches = prof["kernel_launches"] - launches0
+    k_g = float(np.mean(gm_iters))
+    n_pairs_step = (k_g + 1.0) * g.N * g.N      # nominal N^2 per operator pass (RHS S-pass + k_g D-passes)
+
+    # e2e: the same MVP through the C ABI from pinned HOST lambda to a HOST w
+    lam_pin = torch.tensor(lam_h, dtype=torch.float64).pin_memory()
+    w_pin = torch.empty(nc, dtype=torch.float64).pin_memory()
+    e2e_ms = []
+    for k in range(max(2, min(args.steps, 3))):
+        flush.fill_(float(k))
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        lam.copy_(lam_pin, non_blocking=True)
+        bp.contacts(g, cfg["delta"])
+        bp.lcp_mvp(g, lam, out=w, gmres=gm)
+        w_pin.copy_(w, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms.append(e0.elapsed_time(e1))
+    e2e_v = max_over_ranks(ws, float(np.mean(e2e_ms)), dev) / ws
+
+    # one MVP at the parity tolerance (1e-12, R9) for context
+    _, st12 = bp.lcp_mvp(g, lam, out=w, gmres=bp.default_gmres_opts(tol=1e-12))
+
+    k1_ms = prof["ms_allpairs"] / max(1, prof["allpairs_launches"])
+    k1_tflops = prof["allpairs_gflop"] / max(prof["ms_allpairs"], 1e-9)  # GFLOP/ms = TFLOP/s
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "k1_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": ms_per_step / ws, "unit": "ms", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": False, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c%d LCP MVP" % args.config, "spheres": cfg["np"], "p": cfg["p"], "N": g.N,
+                   "contacts": nc, "gmres_tol": args.gmres_tol, "gmres_restart": gm.restart,
+                   "gmres_iters_per_mvp": k_g, "near_incidences": g.n_incidences,
+                   "l2": "flushed between steps (256 MiB write outside the per-step events)",
+                   "parallelism": "replicas" if ws > 1 else "single GPU",
+                   "geometry_init_s": round(t_init, 3)},
+        "pair_interactions_per_s": n_pairs_step / (ms_per_step * 1e-3),
+        "ms_per_mvp_tol_1e-12": st12.ms, "gmres_iters_tol_1e-12": st12.iters,
+        "kernel_split_ms_per_step": {"k1_allpairs": prof["ms_allpairs"] / args.steps,
+                                     "k2_near": prof["ms_near"] / args.steps,
+                                     "k3_self": prof["ms_self"] / args.steps},
+        "roofline": {"kernel": "k1_allpairs", "bound": "alu", "achieved": k1_tflops, "peak": FP64_PEAK_TFLOPS,
+                     "unit": "TFLOP/s", "frac": k1_tflops / FP64_PEAK_TFLOPS, "traffic": traffic,
+                     "k1_ms_per_launch": k1_ms,
+                     "peak_source": "derived FP64 DFMA peak 148 SM x 64 lanes x 2 x 1.965 GHz (DESIGN.md); "
+                                    "measured DFMA microbenchmark 37.0 (baseline/measured_fp64.json)"},
+        "clocks": clocks,
+        "gpu_launches": int(launches),
+        "e2e": {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": 8 * nc, "d2h_bytes_per_step": 8 * nc},
+    }
+    del g
+    torch.cuda.empty_cache()
+
+    if not args.no_c5:
+        line["layer_apply_c5"] = run_c5(args, dev, stream)
+
+    if rank == 0 and ws == 1:
+        k_g_or, src = oracle_kg(args.config)
+        n_t = args.cpu_sample_targets or 512
+        ms_cpu, dt, N, passes = oracle_mvp_sample(cfg, n_t, int(round(k_g)))
+        line["cpu_baseline"] = {"value": ms_cpu, "unit": "ms", "cores": cores_used(), "kind": "oracle",
+                                "sample": "oracle plain-C coarse stresslet pass over %d of %d targets (%.1f s), "
+                                          "scaled by N/%d x %d operator passes; near/self parts excluded"
+                                          % (n_t, N, dt, n_t, passes)}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def run_c5(args, dev, stream):
+    import torch
+    import paper_2604_10089_b200 as bp
+    from synth import layer_densities, make_config
+    cfg = make_config(5)
+    t0 = time.time()
+    g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+    torch.cuda.synchronize()
+    t_init = time.time() - t0
+    f_h, q_h = layer_densities(5, g.N)
+    f = torch.tensor(f_h, device=dev)
+    q = torch.tensor(q_h, device=dev)
+    u = torch.empty((g.N, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+    for _ in range(2):
+        bp.layer_apply(g, f, q, out=u)
+    torch.cuda.synchronize()
+    bp.profile_reset(g, events=True)
+    ms = []
+    for k in range(args.c5_steps):
+        flush.fill_(float(k))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bp.layer_apply(g, f, q, out=u)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    prof = bp.profile_get(g)
+    m = float(np.mean(ms))
+    k1_tflops = prof["allpairs_gflop"] / max(prof["ms_allpairs"], 1e-9)
+    out = {"workload": "c5 layer apply S+D (216 spheres, p=24, N=%d)" % g.N, "ms": m,
+           "pair_interactions_per_s": float(g.N) * g.N / (m * 1e-3),
+           "k1_ms": prof["ms_allpairs"] / args.c5_steps, "k2_ms": prof["ms_near"] / args.c5_steps,
+           "k3_ms": prof["ms_self"] / args.c5_steps,
+           "k1_tflops": k1_tflops, "k1_frac_fp64_peak": k1_tflops / FP64_PEAK_TFLOPS,
+           "near_incidences": g.n_incidences, "geometry_init_s": round(t_init, 3),
+           "device_bytes": g.device_bytes}
+    del g
+    torch.cuda.empty_cache()
+    return out
+
+
+def main():
+    args = parse()
+    ws, rank, local = dist_setup(args)
+    if args.impl == "reference":
+        run_reference(args, ws, rank)
+    else:
+        run_ours(args, ws, rank, local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

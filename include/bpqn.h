@@ -163,10 +163,15 @@ int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, c
 /* Thread-local message for the last non-zero return. */
 const char* bpqn_last_error(void);
 
-/* Kernel-level profiling hooks (bench.py): time of the last operator pieces (ms)
- * and the number of kernels launched since the last reset. */
+/* Kernel-level profiling hooks (bench.py).  bpqn_profile_reset(g, 1) clears the
+ * counters and makes every later operator application record CUDA events on its
+ * stream around K1 (all-pairs), K2 (near) and K3 (self) -- no host sync is added.
+ * bpqn_profile_get synchronises on the last event and returns the summed device
+ * times (ms) since the reset, the algorithmic GFLOP of the timed K1 launches
+ * (DESIGN.md "Roofline"), the number of K1 launches and of all libbpqn kernel
+ * launches.  Any output pointer may be NULL. */
 int bpqn_profile_get(bpqn_geom_t g, double* ms_allpairs, double* ms_near, double* ms_self,
-                     long long* allpairs_launches, long long* kernel_launches);
+                     double* allpairs_gflop, long long* allpairs_launches, long long* kernel_launches);
 int bpqn_profile_reset(bpqn_geom_t g, int enable_events);
 
 #ifdef __cplusplus

@@ -27,8 +27,9 @@ def sphere_grid(p, a=1.0):
     theta = np.arccos(t)
     phi = np.pi * np.arange(2 * p) / p
     th, ph = np.meshgrid(theta, phi, indexing="ij")  # [p+1, 2p]; flatten -> k*2p + l
-    st = np.sin(th)
-    xi = np.stack([st * np.cos(ph), st * np.sin(ph), np.cos(th)], axis=-1).reshape(-1, 3)
+    ct = np.meshgrid(t, phi, indexing="ij")[0]       # cos(theta_k) = t_k exactly (O1: theta_k = arccos t_k)
+    st = np.sqrt(1.0 - ct * ct)
+    xi = np.stack([st * np.cos(ph), st * np.sin(ph), ct], axis=-1).reshape(-1, 3)
     w = (a * a * np.outer(om, np.full(2 * p, np.pi / p))).reshape(-1)
     return dict(p=p, a=a, t=t, omega=om, theta=theta, phi=phi, xi=xi, w=w,
                 theta_node=th.reshape(-1), phi_node=ph.reshape(-1))

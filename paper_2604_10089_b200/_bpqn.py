@@ -62,7 +62,8 @@ SYMBOLS = {
     "bpqn_solve_lcp": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(SolveOpts), P(Report), c_void_p]),
     "bpqn_solve_lcp_dense": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, P(SolveOpts), P(Report)]),
     "bpqn_last_error": (ctypes.c_char_p, []),
-    "bpqn_profile_get": (c_int, [c_void_p, P(c_double), P(c_double), P(c_double), P(c_longlong), P(c_longlong)]),
+    "bpqn_profile_get": (c_int, [c_void_p, P(c_double), P(c_double), P(c_double), P(c_double), P(c_longlong),
+                                 P(c_longlong)]),
     "bpqn_profile_reset": (c_int, [c_void_p, c_int]),
 }
 
@@ -280,9 +281,9 @@ def profile_reset(g, events=True):
 
 
 def profile_get(g):
-    a, b, c = c_double(), c_double(), c_double()
+    a, b, c, gf = c_double(), c_double(), c_double(), c_double()
     n1, n2 = c_longlong(), c_longlong()
-    _check(lib().bpqn_profile_get(g.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(n1),
-                                  ctypes.byref(n2)))
-    return dict(ms_allpairs=a.value, ms_near=b.value, ms_self=c.value, allpairs_launches=n1.value,
-                kernel_launches=n2.value)
+    _check(lib().bpqn_profile_get(g.h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c), ctypes.byref(gf),
+                                  ctypes.byref(n1), ctypes.byref(n2)))
+    return dict(ms_allpairs=a.value, ms_near=b.value, ms_self=c.value, allpairs_gflop=gf.value,
+                allpairs_launches=n1.value, kernel_launches=n2.value)

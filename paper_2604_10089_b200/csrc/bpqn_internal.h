@@ -69,10 +69,14 @@ void gauss_legendre_desc(int n, std::vector<double>& t, std::vector<double>& w);
 void build_grid(int p, double a, Grid& g);
 int sh_count(int p);  // dim V_p = p^2 + 2p
 
+// Kernel timing for bench.py: when enabled, every operator application records
+// 4 events (no host sync); bpqn_profile_get synchronises once and sums them.
 struct Profile {
   bool events = false;
-  cudaEvent_t e[8] = {};
+  std::vector<cudaEvent_t> pool;  // groups of 4: before K1, after K1, after K2, after K3
+  size_t used = 0;
   double ms_allpairs = 0, ms_near = 0, ms_self = 0;
+  double allpairs_flop = 0;       // algorithmic flops of the timed K1 launches
   long long allpairs_launches = 0, launches = 0;
 };
 
@@ -136,6 +140,8 @@ void precompute(Geom& g, cudaStream_t st);  // self E matrices + near matrices
 void apply_operator(Geom& g, const double* sigS, const double* sigD, const double* Es, const double* Ed,
                     double* out, cudaStream_t st);
 
+double allpairs_flops_per_pair(int mode);
+void profile_collect(Geom& g);
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st);
 void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st);
 void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,

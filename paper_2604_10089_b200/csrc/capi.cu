@@ -16,7 +16,7 @@ void set_error(const std::string& msg) { g_err = msg; }
 
 Geom::~Geom() {
   if (host_scal) cudaFreeHost(host_scal);
-  for (auto& e : prof.e)
+  for (auto& e : prof.pool)
     if (e) cudaEventDestroy(e);
 }
 
@@ -221,7 +221,6 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       g->ft.alloc(6 * (size_t)g->np);
       g->uo.alloc(6 * (size_t)g->np);
       BPQN_CUDA(cudaMallocHost(&g->host_scal, 64 * sizeof(double)));
-      for (auto& e : g->prof.e) BPQN_CUDA(cudaEventCreate(&e));
       precompute(*g, st);
     } catch (...) {
       delete g;
@@ -547,9 +546,11 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
 }
 
 int bpqn_profile_get(bpqn_geom_t g, double* ms_allpairs, double* ms_near, double* ms_self,
-                     long long* allpairs_launches, long long* kernel_launches) {
+                     double* allpairs_gflop, long long* allpairs_launches, long long* kernel_launches) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");
+    profile_collect(*g);
+    if (allpairs_gflop) *allpairs_gflop = g->prof.allpairs_flop * 1e-9;
     if (ms_allpairs) *ms_allpairs = g->prof.ms_allpairs;
     if (ms_near) *ms_near = g->prof.ms_near;
     if (ms_self) *ms_self = g->prof.ms_self;
@@ -562,7 +563,9 @@ int bpqn_profile_get(bpqn_geom_t g, double* ms_allpairs, double* ms_near, double
 int bpqn_profile_reset(bpqn_geom_t g, int enable_events) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");
+    profile_collect(*g);
     g->prof.ms_allpairs = g->prof.ms_near = g->prof.ms_self = 0;
+    g->prof.allpairs_flop = 0;
     g->prof.allpairs_launches = g->prof.launches = 0;
     g->prof.events = enable_events != 0;
     return BPQN_OK;

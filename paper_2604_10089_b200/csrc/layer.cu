@@ -147,6 +147,10 @@ __global__ void __launch_bounds__(K1T, 4) k1_allpairs(K1Args A) {
   }
 }
 
+// Algorithmic flops per target-source pair of the fused formulation (DESIGN.md
+// "Roofline"): S 28, D 29, S+D 42 (the rsqrt counted as one operation).
+double allpairs_flops_per_pair(int mode) { return mode == MODE_S ? 28.0 : (mode == MODE_D ? 29.0 : 42.0); }
+
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   K1Args A;
   A.X = g.X.p;
@@ -309,11 +313,24 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
                     double* out, cudaStream_t st) {
   int mode = (sigS && sigD) ? MODE_SD : (sigS ? MODE_S : MODE_D);
   Profile& P = g.prof;
-  if (P.events) BPQN_CUDA(cudaEventRecord(P.e[0], st));
+  cudaEvent_t* ev = nullptr;
+  if (P.events) {
+    while (P.pool.size() < P.used + 4) {
+      cudaEvent_t e;
+      BPQN_CUDA(cudaEventCreate(&e));
+      P.pool.push_back(e);
+    }
+    ev = P.pool.data() + P.used;
+    P.used += 4;
+    BPQN_CUDA(cudaEventRecord(ev[0], st));
+  }
   launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
-  if (P.events) BPQN_CUDA(cudaEventRecord(P.e[1], st));
+  if (ev) {
+    BPQN_CUDA(cudaEventRecord(ev[1], st));
+    P.allpairs_flop += (double)g.n * (double)g.n * allpairs_flops_per_pair(mode);
+  }
   launch_near(g, sigS, sigD, g.nearout.p, st);
-  if (P.events) BPQN_CUDA(cudaEventRecord(P.e[2], st));
+  if (ev) BPQN_CUDA(cudaEventRecord(ev[2], st));
   if (sigS && sigD) {
     launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st);
     launch_self_gemm(g, Ed, sigD, nullptr, nullptr, out, 1, st);
@@ -322,17 +339,24 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   } else {
     launch_self_gemm(g, Ed, sigD, g.far.p, g.nearout.p, out, 0, st);
   }
-  if (P.events) {
-    BPQN_CUDA(cudaEventRecord(P.e[3], st));
-    BPQN_CUDA(cudaEventSynchronize(P.e[3]));
+  if (ev) BPQN_CUDA(cudaEventRecord(ev[3], st));
+}
+
+// Sum the recorded operator timings (one host sync) and recycle the events.
+void profile_collect(Geom& g) {
+  Profile& P = g.prof;
+  if (P.used == 0) return;
+  BPQN_CUDA(cudaEventSynchronize(P.pool[P.used - 1]));
+  for (size_t k = 0; k < P.used; k += 4) {
     float a = 0, b = 0, c = 0;
-    cudaEventElapsedTime(&a, P.e[0], P.e[1]);
-    cudaEventElapsedTime(&b, P.e[1], P.e[2]);
-    cudaEventElapsedTime(&c, P.e[2], P.e[3]);
+    BPQN_CUDA(cudaEventElapsedTime(&a, P.pool[k], P.pool[k + 1]));
+    BPQN_CUDA(cudaEventElapsedTime(&b, P.pool[k + 1], P.pool[k + 2]));
+    BPQN_CUDA(cudaEventElapsedTime(&c, P.pool[k + 2], P.pool[k + 3]));
     P.ms_allpairs += a;
     P.ms_near += b;
     P.ms_self += c;
   }
+  P.used = 0;
 }
 
 }  // namespace bpqn

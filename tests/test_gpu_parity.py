@@ -1,0 +1,316 @@
+"""GPU parity: the CUDA path (libbpqn through the C ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star): fp64 relative L2
+  <= 1e-11  one kernel summation (bpqn_layer_apply),
+  <= 1e-9   GMRES-solved velocities (mobility, LCP MVP, b),
+  <= 1e-7   lambda of the LCP solve, complementarity residual <= 1e-8 evaluated
+            with the ORACLE's operator on the GPU's lambda (R26);
+bit-exact for the contact index set.
+Small scenes are computed by the oracle on the fly; c1-c4 operator/LCP outputs
+come from tests/fixtures/c*.npz written by tests/fixtures/make_fixtures.py,
+which calls only oracle/.  Full-size c4/c5 layer applies are checked on sampled
+targets the oracle computes one by one.
+"""
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+FIX = os.path.join(ROOT, "tests", "fixtures")
+
+TOL_SUM, TOL_VEL, TOL_LAM, TOL_KKT = 1e-11, 1e-9, 1e-7, 1e-8
+GM_PARITY = dict(tol=1e-12)
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.fixture(scope="module")
+def bp():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_10089_b200 as m
+    m.lib()
+    return m
+
+
+def T(x, dtype=None):
+    import torch
+    return torch.tensor(np.asarray(x), dtype=dtype or torch.float64, device="cuda")
+
+
+def fixture(c):
+    path = os.path.join(FIX, "c%d.npz" % c)
+    if not os.path.exists(path):
+        pytest.skip("fixture c%d.npz not generated" % c)
+    return np.load(path, allow_pickle=True)
+
+
+SCENES = {
+    "two_near_p6": (np.array([[0.1, -0.2, 0.3], [2.15, 0.4, 0.1]]), 6),
+    "three_p5": (np.array([[0.0, 0.0, 0.0], [2.05, 0.1, 0.0], [1.025, 1.9, 0.05]]), 5),
+    "touching_gap_1e-3_p8": (np.array([[0.0, 0.0, 0.0], 2.001 * np.array([0.3, 0.8, 0.6]) / np.sqrt(1.09)]), 8),
+    "single_p2": (np.array([[0.3, 0.2, -0.1]]), 2),
+    "single_p7": (np.array([[0.0, 0.0, 0.0]]), 7),
+}
+
+
+def _scene(name):
+    return SCENES[name]
+
+
+# ------------------------------------------------------------------ layer operator (K1 + K2 + K3)
+@pytest.mark.parametrize("name", list(SCENES))
+def test_layer_apply_small(bp, name):
+    from oracle.layer import Disc
+    C, p = _scene(name)
+    d = Disc(C, p)
+    g = bp.Geometry(C, p)
+    assert g.N == d.N and g.n_incidences == len(d.inc)
+    rng = np.random.default_rng(11)
+    f, q = rng.standard_normal((d.N, 3)), rng.standard_normal((d.N, 3))
+    ref_s, ref_d = d.apply_all(f=f), d.apply_all(q=q)
+    us = bp.layer_apply(g, f=T(f)).cpu().numpy()
+    ud = bp.layer_apply(g, q=T(q)).cpu().numpy()
+    usd = bp.layer_apply(g, f=T(f), q=T(q)).cpu().numpy()
+    assert rel(us, ref_s) <= TOL_SUM
+    assert rel(ud, ref_d) <= TOL_SUM
+    assert rel(usd, ref_s + ref_d) <= TOL_SUM
+
+
+def test_layer_apply_none_is_zero(bp):
+    C, p = _scene("three_p5")
+    g = bp.Geometry(C, p)
+    u = bp.layer_apply(g).cpu().numpy()
+    assert not u.any()
+
+
+def _sample_targets(d, n, seed):
+    rng = np.random.default_rng(seed)
+    t = set(rng.choice(d.N, size=n, replace=False).tolist())
+    t.update([0, d.N - 1, d.nq - 1, d.nq])                      # ends and a sphere boundary
+    if len(d.inc):
+        t.update(np.unique(d.inc_t)[rng.choice(len(np.unique(d.inc_t)), size=min(n, 16), replace=False)].tolist())
+    return np.array(sorted(t), dtype=np.int64)
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_layer_apply_config_sampled(bp, c):
+    """Full-size layer apply (the launch configuration bench.py times) on sampled
+    targets: random, sphere boundaries and near-incidence targets."""
+    from oracle.layer import Disc
+    from synth import layer_densities, make_config
+    cfg = make_config(c)
+    d = Disc(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+    g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+    assert g.N == d.N and g.n_incidences == len(d.inc)
+    f, q = layer_densities(c, d.N)
+    u = bp.layer_apply(g, f=T(f), q=T(q)).cpu().numpy()
+    tg = _sample_targets(d, 24 if c >= 4 else 48, 100 + c)
+    ref = d.apply(f=f, q=q, targets=tg)
+    assert rel(u[tg], ref) <= TOL_SUM, rel(u[tg], ref)
+    assert np.isfinite(u).all()
+
+
+# ------------------------------------------------------------------ mobility (K4 GMRES)
+@pytest.mark.parametrize("name", ["two_near_p6", "three_p5", "single_p7"])
+def test_mobility_small(bp, name):
+    from oracle import mobility as mob
+    from oracle.layer import Disc
+    C, p = _scene(name)
+    d = Disc(C, p)
+    g = bp.Geometry(C, p)
+    FT = np.random.default_rng(5).standard_normal((len(C), 6))
+    uo, st = bp.mobility_apply(g, T(FT), gmres=bp.default_gmres_opts(**GM_PARITY))
+    ref = mob.mobility(d, FT, tol=1e-13)
+    assert rel(uo.cpu().numpy(), ref) <= TOL_VEL
+    assert st.rel_resid <= 1e-12
+
+
+def test_mobility_single_sphere_stokes_drag(bp):
+    """GPU path against the closed form U = F/(6 pi mu a), Omega = T/(8 pi mu a^3) (App. A.1)."""
+    a, mu = 1.3, 0.7
+    g = bp.Geometry(np.array([[1.0, -2.0, 0.5]]), 10, radius=a, mu=mu)
+    FT = np.array([[0.3, -1.2, 0.8, 0.5, 0.1, -0.7]])
+    uo, _ = bp.mobility_apply(g, T(FT), gmres=bp.default_gmres_opts(**GM_PARITY))
+    uo = uo.cpu().numpy()[0]
+    np.testing.assert_allclose(uo[:3], FT[0, :3] / (6 * np.pi * mu * a), rtol=1e-10, atol=1e-12)
+    np.testing.assert_allclose(uo[3:], FT[0, 3:] / (8 * np.pi * mu * a ** 3), rtol=1e-10, atol=1e-12)
+
+
+def test_janus_slip_and_swim_speed(bp):
+    from oracle import mobility as mob
+    from oracle.layer import Disc
+    C = np.array([[0.0, 0.0, 0.0], [3.0, 0.5, 0.0]])
+    axes = np.array([[0.0, 0.0, 1.0], [0.6, 0.0, 0.8]])
+    d = Disc(C, 8)
+    g = bp.Geometry(C, 8)
+    s = bp.janus_slip(g, axes, 1.0).cpu().numpy()
+    np.testing.assert_allclose(s, mob.janus_slip(d, axes, 1.0), atol=1e-15)
+    uo, _ = bp.mobility_apply(g, T(np.zeros((2, 6))), slip=T(s), gmres=bp.default_gmres_opts(**GM_PARITY))
+    ref = mob.mobility(d, np.zeros((2, 6)), slip=s, tol=1e-13)
+    assert rel(uo.cpu().numpy(), ref) <= TOL_VEL
+
+
+@pytest.mark.parametrize("c", [1, 2, 3])
+def test_mobility_config(bp, c):
+    z = fixture(c)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    uo, st = bp.mobility_apply(g, T(z["FT_test"]), gmres=bp.default_gmres_opts(**GM_PARITY))
+    assert rel(uo.cpu().numpy(), z["UO_test"]) <= TOL_VEL
+
+
+# ------------------------------------------------------------------ contacts (K5)
+@pytest.mark.parametrize("c", [1, 2, 3, 4, 5])
+def test_contacts_bit_exact(bp, c):
+    from oracle import lcp
+    from synth import make_config
+    cfg = make_config(c)
+    g = bp.Geometry(cfg["centers"], 2)
+    pairs, nrm, gaps = bp.contacts(g, cfg["delta"])
+    op, on, og = lcp.contacts(cfg["centers"], cfg["radius"], cfg["delta"])
+    assert np.array_equal(pairs.cpu().numpy().astype(np.int64), op)
+    np.testing.assert_allclose(nrm.cpu().numpy(), on, atol=1e-15)
+    np.testing.assert_allclose(gaps.cpu().numpy(), og, atol=1e-14)
+
+
+def test_contacts_edge_cases(bp):
+    import torch
+    C = np.array([[0.0, 0.0, 0.0], [2.05, 0.0, 0.0], [4.1, 0.0, 0.0], [20.0, 0.0, 0.0]])
+    g = bp.Geometry(C, 3)
+    p, n, gp = bp.contacts(g, 0.0)            # no pair has gap < 0
+    assert p.shape[0] == 0 and g.nc == 0
+    with pytest.raises(bp.BpqnError):         # MVP with an empty contact set is an input error
+        bp.lcp_mvp(g, torch.zeros(1, dtype=torch.float64, device="cuda"))
+    with pytest.raises(bp.BpqnError) as e:    # capacity: 2 contacts, room for 1
+        bp.contacts(g, 0.1, max_contacts=1)
+    assert e.value.code == 7
+    p, n, gp = bp.contacts(g, 0.1)
+    assert p.cpu().numpy().tolist() == [[0, 1], [1, 2]]
+
+
+def test_overlap_and_bad_args_rejected(bp):
+    with pytest.raises(bp.BpqnError) as e:
+        bp.Geometry(np.array([[0.0, 0.0, 0.0], [1.99, 0.0, 0.0]]), 4)
+    assert e.value.code == 1
+    with pytest.raises(bp.BpqnError) as e:
+        bp.Geometry(np.array([[0.0, 0.0, 0.0]]), 1)
+    assert e.value.code == 1
+
+
+def test_nan_input_reported(bp):
+    C, p = _scene("two_near_p6")
+    g = bp.Geometry(C, p)
+    FT = np.zeros((2, 6))
+    FT[0, 0] = np.nan
+    with pytest.raises(bp.BpqnError) as e:
+        bp.mobility_apply(g, T(FT))
+    assert e.value.code == 6
+
+
+# ------------------------------------------------------------------ LCP MVP and b
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_lcp_mvp_config(bp, c):
+    import torch
+    z = fixture(c)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    pairs, nrm, gaps = bp.contacts(g, 0.1)
+    assert np.array_equal(pairs.cpu().numpy().astype(np.int64), z["pairs"])
+    for k in range(z["w_test"].shape[0]):
+        from synth import lambda_test
+        lam = lambda_test(c, g.nc, k)
+        w, st = bp.lcp_mvp(g, T(lam), gmres=bp.default_gmres_opts(**GM_PARITY))
+        assert rel(w.cpu().numpy(), z["w_test"][k]) <= TOL_VEL, (k, st.iters)
+    del torch
+
+
+@pytest.mark.parametrize("c", [1, 2, 3, 4])
+def test_lcp_b_config(bp, c):
+    from synth import make_config
+    z = fixture(c)
+    cfg = make_config(c)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    slip = bp.janus_slip(g, cfg["axes"], cfg["slip_B"])
+    b, _ = bp.lcp_b(g, T(cfg["F_nc"]), slip=slip, gmres=bp.default_gmres_opts(**GM_PARITY))
+    assert rel(b.cpu().numpy(), z["b"]) <= TOL_VEL
+
+
+def test_lcp_mvp_unit_vectors_c1(bp):
+    """Every column of A = D^T M D at c1 against the oracle's densified A."""
+    z = fixture(1)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    A = z["A_dense"]
+    for l in range(g.nc):
+        e = np.zeros(g.nc)
+        e[l] = 1.0
+        w, _ = bp.lcp_mvp(g, T(e), gmres=bp.default_gmres_opts(**GM_PARITY))
+        assert rel(w.cpu().numpy(), A[:, l]) <= TOL_VEL
+
+
+# ------------------------------------------------------------------ LCP solves (host PQN over device MVPs)
+def _kkt(lam, A, b):
+    return float(np.linalg.norm(np.minimum(lam, A @ lam + b)))
+
+
+def test_solve_lcp_mono_c1(bp):
+    z = fixture(1)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    o = bp.default_solve_opts(method=0, eps_kkt_abs=1e-10)
+    o.gm_hi.tol = 1e-12
+    lam = T(np.zeros(g.nc))
+    lam, rep, rc = bp.solve_lcp(g, None, T(z["b"]), lam, opts=o)
+    assert rc == 0
+    x = lam.cpu().numpy()
+    assert rel(x, z["lam_brute"]) <= TOL_LAM
+    assert _kkt(x, z["A_dense"], z["b"]) <= TOL_KKT
+    assert rep.hi_mvps == rep.iterations + 1
+
+
+@pytest.mark.parametrize("method", ["mono", "bi"])
+def test_solve_lcp_c2(bp, method):
+    z = fixture(2)
+    key = "lam_" + method
+    if key not in z:
+        pytest.skip("no %s solution in fixture" % method)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    lo = None
+    if method == "bi":
+        lo = bp.Geometry(z["centers"], int(z["p_lo"]))
+        pr, nr, gp = bp.contacts(g, 0.1)
+        bp.set_contacts(lo, pr, nr, gp)
+    o = bp.default_solve_opts(method=1 if method == "bi" else 0, eps_kkt_abs=1e-10)
+    o.gm_hi.tol = 1e-12
+    o.gm_lo.tol = 1e-12
+    lam = T(np.zeros(g.nc))
+    lam, rep, rc = bp.solve_lcp(g, lo, T(z["b"]), lam, opts=o)
+    assert rc == 0
+    assert rel(lam.cpu().numpy(), z[key]) <= TOL_LAM
+    assert rep.kkt_abs <= TOL_KKT
+    assert rep.hi_mvps == rep.iterations + 1
+
+
+def test_solve_lcp_bi_c3(bp):
+    z = fixture(3)
+    if "lam_bi" not in z:
+        pytest.skip("no bi solution in fixture")
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    pr, nr, gp = bp.contacts(g, 0.1)
+    lo = bp.Geometry(z["centers"], int(z["p_lo"]))
+    bp.set_contacts(lo, pr, nr, gp)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-10)
+    o.gm_hi.tol = 1e-12
+    o.gm_lo.tol = 1e-12
+    lam, rep, rc = bp.solve_lcp(g, lo, T(z["b"]), T(np.zeros(g.nc)), opts=o)
+    assert rc == 0
+    assert rel(lam.cpu().numpy(), z["lam_bi"]) <= TOL_LAM
+    assert rep.kkt_abs <= TOL_KKT
