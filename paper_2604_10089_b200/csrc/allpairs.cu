@@ -1,0 +1,319 @@
+// K1: all-pairs coarse-rule Stokeslet / stresslet summation on B200 (sm_100a).
+//
+//   u(x_i) = sum_{j != i} w_j [ G(x_i - y_j) f_j + K_D(x_i, y_j) q_j ]      (O6, coarse part)
+//   G(r)   = (I/rho + r r^T/rho^3) / (8 pi mu),   K_D = -3/(4 pi) (r.n_y) r r^T / rho^5,  r = x - y
+//
+// over ALL node pairs with rho > 0 (the same-sphere and near-pair coarse terms are
+// removed again by K3's E matrices and K2's correction blocks).  The paper treats
+// this operator as a black box (STKFMM far field
+// P:528); the B200 design is DESIGN.md "K1":
+//
+//  * k1_pack writes the sources once per call as 16-byte-aligned records with the
+//    weight and kernel constant folded into the density (S: y, f~; D: y, n, q~;
+//    S+D: y, n, f~, q~), padded to a whole number of source tiles with far-away
+//    zero-strength records -- the main loop has no bounds checks.
+//  * k1_allpairs is persistent: the (target block, source tile) work space is cut
+//    into equal contiguous ranges, one per resident CTA (perfect balance to one
+//    tile, any N).  Source tiles stream through a K1_STAGES-deep shared-memory ring
+//    filled by one thread with TMA bulk copies (cp.async.bulk + mbarrier
+//    complete_tx); all threads read them back as broadcast 16-byte loads.
+//  * each thread owns K1_R targets in registers; a target block's partial sums are
+//    flushed with fp64 atomics when the CTA's range leaves the block (<= 2-3 per CTA).
+//  * rho^-k from one MUFU.RSQ64H seed y (rsqrt.approx.ftz.f64) and the series
+//    (1-e)^(-k/2) = 1 + (k/2) e + (k/2)(k/2+1)/2 e^2, e = 1 - rho^2 y^2 (|e| <= 1.85e-6
+//    = 2^-19 measured, tools/rsq_micro.cu; truncation error < 7|e|^3 ~ 4e-17): rho^-5 costs
+//    6 FP64 instructions instead of the 9 of rsqrt() + powers.  rho = 0 (the target's
+//    own node) zeroes the seed with an integer select, so that pair contributes 0.
+#include <algorithm>
+
+#include "bpqn_internal.h"
+
+namespace bpqn {
+
+static const double PI_A = 3.14159265358979323846;
+
+constexpr int K1_THREADS = 256;
+constexpr int K1_R = 4;                          // targets per thread
+constexpr int K1_TB = K1_THREADS * K1_R;         // targets per block
+constexpr int K1_TS = 64;                        // sources per tile
+constexpr int K1_STAGES = 4;                     // smem ring depth
+
+template <int MODE>
+struct Rec;
+template <>
+struct Rec<MODE_S> { static constexpr int n = 6; };    // y0 y1 y2 f0 f1 f2
+template <>
+struct Rec<MODE_D> { static constexpr int n = 10; };   // y0 y1 y2 n0 n1 n2 q0 q1 q2 pad
+template <>
+struct Rec<MODE_SD> { static constexpr int n = 12; };  // y0 y1 y2 n0 n1 n2 f0 f1 f2 q0 q1 q2
+
+__global__ void k1_pack(int mode, int N, int npad, const double* __restrict__ src, const double* __restrict__ sigS,
+                        const double* __restrict__ sigD, double cS, double cD, double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= npad) return;
+  const int rec = mode == MODE_S ? 6 : (mode == MODE_D ? 10 : 12);
+  double* o = out + (size_t)rec * j;
+  if (j >= N) {  // far away, zero strength
+    o[0] = o[1] = o[2] = 1e30;
+    for (int k = 3; k < rec; ++k) o[k] = 0.0;
+    return;
+  }
+  const double* g = src + 8 * (size_t)j;  // {y, w, n, 0}
+  const double w = g[3];
+  o[0] = g[0];
+  o[1] = g[1];
+  o[2] = g[2];
+  if (mode == MODE_S) {
+    const double c = cS * w;
+    o[3] = c * sigS[3 * (size_t)j];
+    o[4] = c * sigS[3 * (size_t)j + 1];
+    o[5] = c * sigS[3 * (size_t)j + 2];
+  } else {
+    o[3] = g[4];
+    o[4] = g[5];
+    o[5] = g[6];
+    if (mode == MODE_D) {
+      const double c = cD * w;
+      o[6] = c * sigD[3 * (size_t)j];
+      o[7] = c * sigD[3 * (size_t)j + 1];
+      o[8] = c * sigD[3 * (size_t)j + 2];
+      o[9] = 0.0;
+    } else {
+      const double c = cS * w, d = cD * w;
+      o[6] = c * sigS[3 * (size_t)j];
+      o[7] = c * sigS[3 * (size_t)j + 1];
+      o[8] = c * sigS[3 * (size_t)j + 2];
+      o[9] = d * sigD[3 * (size_t)j];
+      o[10] = d * sigD[3 * (size_t)j + 1];
+      o[11] = d * sigD[3 * (size_t)j + 2];
+    }
+  }
+}
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ unsigned smem_addr(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "LAB_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra LAB_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ double rsq_seed(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));  // one MUFU.RSQ64H
+  return y;
+}
+
+// seed y ~ rr^-1/2 with rr == 0 -> y = 0 (integer select, no FP64 compare)
+__device__ __forceinline__ double seed_or_zero(double rr) {
+  const double y = rsq_seed(rr);
+  const int hi = __double2hiint(rr) != 0 ? __double2hiint(y) : 0;
+  return __hiloint2double(hi, __double2hiint(rr) != 0 ? __double2loint(y) : 0);
+}
+
+struct K1Params {
+  const double* X;     // [N][3] targets
+  const double* pk;    // packed sources [npad][REC]
+  double* out;         // [N][3], zeroed, atomically accumulated
+  int N, n_tb, n_st;
+  long long units;     // n_tb * n_st
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
+  constexpr int REC = Rec<MODE>::n;
+  constexpr int TILE_DBL = K1_TS * REC;
+  constexpr unsigned TILE_BYTES = TILE_DBL * 8;
+  __shared__ __align__(128) double ring[K1_STAGES][TILE_DBL];
+  __shared__ __align__(8) uint64_t full[K1_STAGES];
+
+  const long long P_ = gridDim.x;
+  const long long u0 = P.units * blockIdx.x / P_;
+  const long long u1 = P.units * (blockIdx.x + 1) / P_;
+  const int tid = threadIdx.x;
+  if (u0 >= u1) return;
+
+  if (tid == 0) {
+    for (int s = 0; s < K1_STAGES; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < K1_STAGES && u0 + s < u1; ++s) {
+      const long long u = u0 + s;
+      const int st = (int)(u % P.n_st);
+      mbar_expect_tx(&full[s], TILE_BYTES);
+      bulk_g2s(ring[s], P.pk + (size_t)st * TILE_DBL, TILE_BYTES, &full[s]);
+    }
+  }
+
+  double x[K1_R][3], acc[K1_R][3];
+  int cur_tb = -1;
+  for (long long u = u0; u < u1; ++u) {
+    const int i = (int)(u - u0);
+    const int buf = i % K1_STAGES;
+    const unsigned parity = (unsigned)(i / K1_STAGES) & 1u;
+    const int tb = (int)(u / P.n_st);
+    if (tb != cur_tb) {
+      if (cur_tb >= 0) {
+#pragma unroll
+        for (int r = 0; r < K1_R; ++r) {
+          const int t = cur_tb * K1_TB + r * K1_THREADS + tid;
+          if (t < P.N) {
+            atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
+            atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
+            atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
+          }
+        }
+      }
+      cur_tb = tb;
+#pragma unroll
+      for (int r = 0; r < K1_R; ++r) {
+        int t = tb * K1_TB + r * K1_THREADS + tid;
+        t = t < P.N ? t : P.N - 1;
+        x[r][0] = P.X[3 * (size_t)t];
+        x[r][1] = P.X[3 * (size_t)t + 1];
+        x[r][2] = P.X[3 * (size_t)t + 2];
+        acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+      }
+    }
+    mbar_wait(&full[buf], parity);
+    const double* tile = ring[buf];
+#pragma unroll 2
+    for (int k = 0; k < K1_TS; ++k) {
+      const double2* rp = reinterpret_cast<const double2*>(tile + k * REC);
+      double src[REC];
+#pragma unroll
+      for (int h = 0; h < REC / 2; ++h) {
+        const double2 v = rp[h];
+        src[2 * h] = v.x;
+        src[2 * h + 1] = v.y;
+      }
+#pragma unroll
+      for (int r = 0; r < K1_R; ++r) {
+        const double r0 = x[r][0] - src[0], r1 = x[r][1] - src[1], r2 = x[r][2] - src[2];
+        const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+        const double y = seed_or_zero(rr);
+        const double y2 = y * y;
+        const double e = fma(-rr, y2, 1.0);
+        if (MODE == MODE_D) {
+          // rho^-5 = y^5 (1 + 5/2 e + 35/8 e^2)
+          const double rn = fma(r2, src[5], fma(r1, src[4], r0 * src[3]));
+          const double rq = fma(r2, src[8], fma(r1, src[7], r0 * src[6]));
+          const double c5 = fma(e, fma(e, 4.375, 2.5), 1.0);
+          const double y4 = y2 * y2;
+          double t = rn * rq;
+          t = t * y;
+          t = t * y4;
+          t = t * c5;
+          acc[r][0] = fma(r0, t, acc[r][0]);
+          acc[r][1] = fma(r1, t, acc[r][1]);
+          acc[r][2] = fma(r2, t, acc[r][2]);
+        } else {
+          // rho^-1 = y (1 + e/2 + 3/8 e^2)
+          const double s = fma(y * e, fma(e, 0.375, 0.5), y);
+          const double s2 = s * s;
+          const double s3 = s2 * s;
+          if (MODE == MODE_S) {
+            const double rf = fma(r2, src[5], fma(r1, src[4], r0 * src[3]));
+            const double t = rf * s3;
+            acc[r][0] = fma(src[3], s, fma(r0, t, acc[r][0]));
+            acc[r][1] = fma(src[4], s, fma(r1, t, acc[r][1]));
+            acc[r][2] = fma(src[5], s, fma(r2, t, acc[r][2]));
+          } else {
+            const double rn = fma(r2, src[5], fma(r1, src[4], r0 * src[3]));
+            const double rf = fma(r2, src[8], fma(r1, src[7], r0 * src[6]));
+            const double rq = fma(r2, src[11], fma(r1, src[10], r0 * src[9]));
+            const double s5 = s3 * s2;
+            const double t = fma(rf, s3, (rn * rq) * s5);
+            acc[r][0] = fma(src[6], s, fma(r0, t, acc[r][0]));
+            acc[r][1] = fma(src[7], s, fma(r1, t, acc[r][1]));
+            acc[r][2] = fma(src[8], s, fma(r2, t, acc[r][2]));
+          }
+        }
+      }
+    }
+    __syncthreads();  // every thread is done with ring[buf]
+    if (tid == 0 && u + K1_STAGES < u1) {
+      const int st = (int)((u + K1_STAGES) % P.n_st);
+      mbar_expect_tx(&full[buf], TILE_BYTES);
+      bulk_g2s(ring[buf], P.pk + (size_t)st * TILE_DBL, TILE_BYTES, &full[buf]);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < K1_R; ++r) {
+    const int t = cur_tb * K1_TB + r * K1_THREADS + tid;
+    if (t < P.N) {
+      atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
+      atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
+      atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
+    }
+  }
+}
+
+// Algorithmic flops per target-source pair of the fused formulation (DESIGN.md
+// "Roofline"): S 28, D 29, S+D 42 (the rsqrt counted as one operation).
+double allpairs_flops_per_pair(int mode) { return mode == MODE_S ? 28.0 : (mode == MODE_D ? 29.0 : 42.0); }
+
+template <int MODE>
+static int k1_grid(Geom& g) {
+  static int occ[3] = {0, 0, 0};
+  if (!occ[MODE]) {
+    int b = 0;
+    BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_allpairs<MODE>, K1_THREADS, 0));
+    occ[MODE] = std::max(1, b);
+  }
+  return occ[MODE] * g.sms;
+}
+
+void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
+  K1Params P;
+  P.N = g.n;
+  P.n_tb = (g.n + K1_TB - 1) / K1_TB;
+  P.n_st = (g.n + K1_TS - 1) / K1_TS;
+  P.units = (long long)P.n_tb * P.n_st;
+  const int npad = P.n_st * K1_TS;
+  g.packed.ensure((size_t)npad * 12);
+  k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
+                                             -3.0 / (4.0 * PI_A), g.packed.p);
+  BPQN_CHECK_LAUNCH();
+  P.X = g.X.p;
+  P.pk = g.packed.p;
+  P.out = out;
+  BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
+  int grid;
+  if (mode == MODE_D) grid = k1_grid<MODE_D>(g);
+  else if (mode == MODE_S) grid = k1_grid<MODE_S>(g);
+  else grid = k1_grid<MODE_SD>(g);
+  grid = (int)std::min<long long>(grid, P.units);
+  if (mode == MODE_D) k1_allpairs<MODE_D><<<grid, K1_THREADS, 0, st>>>(P);
+  else if (mode == MODE_S) k1_allpairs<MODE_S><<<grid, K1_THREADS, 0, st>>>(P);
+  else k1_allpairs<MODE_SD><<<grid, K1_THREADS, 0, st>>>(P);
+  BPQN_CHECK_LAUNCH();
+  g.prof.allpairs_launches++;
+  g.prof.launches += 2;
+}
+
+}  // namespace bpqn

@@ -116,6 +116,7 @@ struct Geom {
   DBuf<double> gaps;      // [cap]
 
   // workspaces
+  DBuf<double> packed;   // K1 packed source records [npad][<=12]
   DBuf<double> far;      // [N][3] all-pairs accumulator
   DBuf<double> nearout;  // [N][3]
   DBuf<double> rhs, sol, tmp, tmp2;  // [N][3]

@@ -12,174 +12,6 @@
 
 namespace bpqn {
 
-static const double PI_D = 3.14159265358979323846;
-
-// ------------------------------------------------------------------ K1
-// Work item = (source chunk, target block).  A CTA of K1T threads owns K1R targets
-// per thread; sources are staged in shared memory TS at a time, pre-folded with
-// their weight and kernel constant.  Results are added with fp64 atomics (a
-// handful of chunks per target).
-constexpr int K1T = 128;
-constexpr int K1R = 2;
-constexpr int K1TS = 128;
-
-__device__ __forceinline__ double rsqrt_f64(double x) {
-  double y;
-  asm("rsqrt.approx.f64 %0, %1;" : "=d"(y) : "d"(x));  // MUFU.RSQ64H + cubic refinement (ptxas)
-  return y;
-}
-
-struct K1Args {
-  const double* X;      // [N][3] targets
-  const double* src;    // [N][8] {y, w, n, 0}
-  const double* sigS;   // [N][3] single-layer density (S / SD modes)
-  const double* sigD;   // [N][3] double-layer density (D / SD modes)
-  double* out;          // [N][3] (atomic accumulate)
-  int N;
-  int n_tblocks, n_chunks, chunk;
-  double cS, cD;
-};
-
-template <int MODE>
-__global__ void __launch_bounds__(K1T, 4) k1_allpairs(K1Args A) {
-  // per-source smem record: D: y(3) n(3) q~(3) ; S: y(3) f~(3) ; SD: y n f~ q~
-  constexpr int REC = (MODE == MODE_D) ? 9 : (MODE == MODE_S ? 6 : 12);
-  __shared__ double sh[K1TS * REC];
-  const int n_items = A.n_tblocks * A.n_chunks;
-  for (int item = blockIdx.x; item < n_items; item += gridDim.x) {
-    const int ch = item / A.n_tblocks;
-    const int tb = item - ch * A.n_tblocks;
-    double x[K1R][3], u[K1R][3];
-#pragma unroll
-    for (int r = 0; r < K1R; ++r) {
-      int t = tb * (K1T * K1R) + r * K1T + threadIdx.x;
-      int tc = t < A.N ? t : A.N - 1;
-      x[r][0] = A.X[3 * tc];
-      x[r][1] = A.X[3 * tc + 1];
-      x[r][2] = A.X[3 * tc + 2];
-      u[r][0] = u[r][1] = u[r][2] = 0.0;
-    }
-    const int s_begin = ch * A.chunk;
-    const int s_end = min(A.N, s_begin + A.chunk);
-    for (int s0 = s_begin; s0 < s_end; s0 += K1TS) {
-      __syncthreads();
-      for (int k = threadIdx.x; k < K1TS; k += K1T) {
-        int j = s0 + k;
-        double* rec = sh + k * REC;
-        if (j < s_end) {
-          const double* g = A.src + 8 * (size_t)j;
-          double y0 = g[0], y1 = g[1], y2 = g[2], w = g[3];
-          rec[0] = y0; rec[1] = y1; rec[2] = y2;
-          if (MODE == MODE_D) {
-            double c = A.cD * w;
-            rec[3] = g[4]; rec[4] = g[5]; rec[5] = g[6];
-            rec[6] = c * A.sigD[3 * j]; rec[7] = c * A.sigD[3 * j + 1]; rec[8] = c * A.sigD[3 * j + 2];
-          } else if (MODE == MODE_S) {
-            double c = A.cS * w;
-            rec[3] = c * A.sigS[3 * j]; rec[4] = c * A.sigS[3 * j + 1]; rec[5] = c * A.sigS[3 * j + 2];
-          } else {
-            double c = A.cS * w, d = A.cD * w;
-            rec[3] = g[4]; rec[4] = g[5]; rec[5] = g[6];
-            rec[6] = c * A.sigS[3 * j]; rec[7] = c * A.sigS[3 * j + 1]; rec[8] = c * A.sigS[3 * j + 2];
-            rec[9] = d * A.sigD[3 * j]; rec[10] = d * A.sigD[3 * j + 1]; rec[11] = d * A.sigD[3 * j + 2];
-          }
-        } else {
-          rec[0] = rec[1] = rec[2] = 1e30;  // far away, zero strength
-          for (int q = 3; q < REC; ++q) rec[q] = 0.0;
-        }
-      }
-      __syncthreads();
-      const int ns = K1TS;
-#pragma unroll 2
-      for (int k = 0; k < ns; ++k) {
-        const double* rec = sh + k * REC;
-        const double y0 = rec[0], y1 = rec[1], y2 = rec[2];
-#pragma unroll
-        for (int r = 0; r < K1R; ++r) {
-          const double r0 = x[r][0] - y0, r1 = x[r][1] - y1, r2 = x[r][2] - y2;
-          const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
-          double s = rsqrt_f64(rr);
-          s = (__double2hiint(rr) != 0) ? s : 0.0;  // the target's own node: rho = 0
-          if (MODE == MODE_D) {
-            const double rn = fma(r2, rec[5], fma(r1, rec[4], r0 * rec[3]));
-            const double rq = fma(r2, rec[8], fma(r1, rec[7], r0 * rec[6]));
-            const double s2 = s * s;
-            double t = rn * rq;
-            t = t * s2;
-            t = t * s2;
-            t = t * s;
-            u[r][0] = fma(r0, t, u[r][0]);
-            u[r][1] = fma(r1, t, u[r][1]);
-            u[r][2] = fma(r2, t, u[r][2]);
-          } else if (MODE == MODE_S) {
-            const double f0 = rec[3], f1 = rec[4], f2 = rec[5];
-            const double rf = fma(r2, f2, fma(r1, f1, r0 * f0));
-            const double s3 = s * s * s;
-            const double t = rf * s3;
-            u[r][0] = fma(f0, s, fma(r0, t, u[r][0]));
-            u[r][1] = fma(f1, s, fma(r1, t, u[r][1]));
-            u[r][2] = fma(f2, s, fma(r2, t, u[r][2]));
-          } else {
-            const double rn = fma(r2, rec[5], fma(r1, rec[4], r0 * rec[3]));
-            const double f0 = rec[6], f1 = rec[7], f2 = rec[8];
-            const double rf = fma(r2, f2, fma(r1, f1, r0 * f0));
-            const double rq = fma(r2, rec[11], fma(r1, rec[10], r0 * rec[9]));
-            const double s2 = s * s;
-            const double s3 = s2 * s;
-            const double s5 = s3 * s2;
-            const double t = fma(rf, s3, (rn * rq) * s5);
-            u[r][0] = fma(f0, s, fma(r0, t, u[r][0]));
-            u[r][1] = fma(f1, s, fma(r1, t, u[r][1]));
-            u[r][2] = fma(f2, s, fma(r2, t, u[r][2]));
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < K1R; ++r) {
-      int t = tb * (K1T * K1R) + r * K1T + threadIdx.x;
-      if (t < A.N) {
-        atomicAdd(A.out + 3 * t, u[r][0]);
-        atomicAdd(A.out + 3 * t + 1, u[r][1]);
-        atomicAdd(A.out + 3 * t + 2, u[r][2]);
-      }
-    }
-  }
-}
-
-// Algorithmic flops per target-source pair of the fused formulation (DESIGN.md
-// "Roofline"): S 28, D 29, S+D 42 (the rsqrt counted as one operation).
-double allpairs_flops_per_pair(int mode) { return mode == MODE_S ? 28.0 : (mode == MODE_D ? 29.0 : 42.0); }
-
-void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
-  K1Args A;
-  A.X = g.X.p;
-  A.src = g.src.p;
-  A.sigS = sigS;
-  A.sigD = sigD;
-  A.out = out;
-  A.N = g.n;
-  A.n_tblocks = (g.n + K1T * K1R - 1) / (K1T * K1R);
-  // chunking: enough items to fill the GPU several times over, chunk a multiple of K1TS
-  const int resident = g.sms * 4;
-  int want_chunks = std::max(1, (8 * resident + A.n_tblocks - 1) / A.n_tblocks);
-  int chunk = (g.n + want_chunks - 1) / want_chunks;
-  chunk = std::max(K1TS, ((chunk + K1TS - 1) / K1TS) * K1TS);
-  A.chunk = chunk;
-  A.n_chunks = (g.n + chunk - 1) / chunk;
-  A.cS = 1.0 / (8.0 * PI_D * g.mu);
-  A.cD = -3.0 / (4.0 * PI_D);
-  int items = A.n_tblocks * A.n_chunks;
-  int grid = std::min(items, resident);
-  BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
-  if (mode == MODE_D) k1_allpairs<MODE_D><<<grid, K1T, 0, st>>>(A);
-  else if (mode == MODE_S) k1_allpairs<MODE_S><<<grid, K1T, 0, st>>>(A);
-  else k1_allpairs<MODE_SD><<<grid, K1T, 0, st>>>(A);
-  BPQN_CHECK_LAUNCH();
-  g.prof.allpairs_launches++;
-  g.prof.launches++;
-}
-
 // ------------------------------------------------------------------ K2
 // One warp per (near target, component a): sum over the target's incidences of
 // dot(M[inc][a][:], sigma_m[:]) (length 3nq).  Deterministic, no atomics.

@@ -1,0 +1,35 @@
+"""K1/K2/K3 probe for ncu (development aid): layer applies on a BASELINE config.
+
+  python tools/k1_probe.py [--config 4] [--mode d|s|sd] [--reps 3]
+"""
+import argparse
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2604_10089_b200 as bp  # noqa: E402
+from synth import layer_densities, make_config  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", type=int, default=4)
+ap.add_argument("--mode", default="d")
+ap.add_argument("--reps", type=int, default=3)
+a = ap.parse_args()
+cfg = make_config(a.config)
+g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+f, q = layer_densities(a.config, g.N)
+f = torch.tensor(f, device="cuda") if "s" in a.mode else None
+q = torch.tensor(q, device="cuda") if "d" in a.mode else None
+u = torch.empty((g.N, 3), dtype=torch.float64, device="cuda")
+bp.profile_reset(g, events=True)
+for _ in range(a.reps):
+    bp.layer_apply(g, f=f, q=q, out=u)
+torch.cuda.synchronize()
+pr = bp.profile_get(g)
+print("N", g.N, "mode", a.mode, "k1 ms/launch %.3f" % (pr["ms_allpairs"] / a.reps),
+      "TFLOP/s %.2f" % (pr["allpairs_gflop"] / pr["ms_allpairs"]), "k2 %.3f k3 %.3f" % (pr["ms_near"] / a.reps,
+                                                                                     pr["ms_self"] / a.reps))
