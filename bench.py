@@ -43,7 +43,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--gmres-tol", type=float, default=1e-8)   # paper's hi-fidelity eps_gmres (R9)
+    ap.add_argument("--gmres-restart", type=int, default=50)
     ap.add_argument("--no-c5", action="store_true")
+    ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--c5-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-targets", type=int, default=0)
     return ap.parse_args()
@@ -222,7 +224,7 @@ def run_ours(args, ws, rank, local):
     lam_h = rng.uniform(0.0, 1.0, size=nc)
     lam = torch.tensor(lam_h, dtype=torch.float64, device=dev)
     w = torch.empty(nc, dtype=torch.float64, device=dev)
-    gm = bp.default_gmres_opts(tol=args.gmres_tol)
+    gm = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
@@ -277,7 +279,7 @@ def run_ours(args, ws, rank, local):
     e2e_v = max_over_ranks(ws, float(np.mean(e2e_ms)), dev) / ws
 
     # one MVP at the parity tolerance (1e-12, R9) for context
-    _, st12 = bp.lcp_mvp(g, lam, out=w, gmres=bp.default_gmres_opts(tol=1e-12))
+    _, st12 = bp.lcp_mvp(g, lam, out=w, gmres=bp.default_gmres_opts(tol=1e-12, restart=args.gmres_restart))
 
     k1_ms = prof["ms_allpairs"] / max(1, prof["allpairs_launches"])
     k1_tflops = prof["allpairs_gflop"] / max(prof["ms_allpairs"], 1e-9)  # GFLOP/ms = TFLOP/s
@@ -310,6 +312,8 @@ def run_ours(args, ws, rank, local):
         "gpu_launches": int(launches),
         "e2e": {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": 8 * nc, "d2h_bytes_per_step": 8 * nc},
     }
+    if not args.no_solve:
+        line["lcp_solve"] = run_solve(args, cfg, g, pairs, nrm, gaps, dev)
     del g
     torch.cuda.empty_cache()
 
@@ -326,6 +330,48 @@ def run_ours(args, ws, rank, local):
                                           % (n_t, N, dt, n_t, passes)}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def run_solve(args, cfg, g, pairs, nrm, gaps, dev):
+    """One full LCP solve at the bench config: b from the Janus-slip non-collisional
+    mobility solve, then Bi-PQN (Alg. 3) with the low fidelity at p_lo
+    (or Mono-PQN when the config has none), paper-mode tolerances."""
+    import torch
+    import paper_2604_10089_b200 as bp
+    gmo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart)
+    t0 = time.time()
+    lo = None
+    if cfg.get("p_lo"):
+        lo = bp.Geometry(cfg["centers"], cfg["p_lo"], cfg["radius"], cfg["mu"])
+        bp.set_contacts(lo, pairs, nrm, gaps)
+    torch.cuda.synchronize()
+    t_lo_init = time.time() - t0
+    slip = bp.janus_slip(g, cfg["axes"], cfg["slip_B"])
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    b, st_b = bp.lcp_b(g, torch.tensor(cfg["F_nc"], device=dev), slip=slip, gmres=gmo)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_b = e0.elapsed_time(e1)
+    o = bp.default_solve_opts(method=1 if lo is not None else 0, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8)
+    o.gm_hi = gmo
+    o.gm_lo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart)
+    lam = torch.zeros(g.nc, dtype=torch.float64, device=dev)
+    t0 = time.perf_counter()
+    lam, rep, rc = bp.solve_lcp(g, lo, b, lam, opts=o)
+    torch.cuda.synchronize()
+    ms_solve = (time.perf_counter() - t0) * 1e3
+    r = rep.as_dict()
+    out = {"method": "Bi-PQN" if lo is not None else "Mono-PQN", "p_hi": cfg["p"], "p_lo": cfg.get("p_lo"),
+           "ms_b": ms_b, "gmres_iters_b": st_b.iters, "ms_solve": ms_solve, "ms_total": ms_b + ms_solve,
+           "rc": rc, "lo_geometry_init_s": round(t_lo_init, 3),
+           "negative_b_fraction": float((b < 0).double().mean().item()),
+           "active_contacts": int((lam > 0).sum().item())}
+    out.update({k: r[k] for k in ("iterations", "hi_mvps", "lo_mvps", "e_mvps", "cost_ratio", "kkt_abs",
+                                  "gmres_iters_hi", "gmres_iters_lo", "ms_hi", "ms_lo", "termination")})
+    if lo is not None:
+        lo.close()
+    return out
 
 
 def run_c5(args, dev, stream):

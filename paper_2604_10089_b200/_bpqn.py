@@ -21,7 +21,7 @@ class DiscOpts(ctypes.Structure):
 
 
 class GmresOpts(ctypes.Structure):
-    _fields_ = [("tol", c_double), ("restart", c_int), ("max_iters", c_int)]
+    _fields_ = [("tol", c_double), ("restart", c_int), ("max_iters", c_int), ("precond", c_int)]
 
 
 class GmresStats(ctypes.Structure):
@@ -125,9 +125,11 @@ def default_disc_opts():
     return o
 
 
-def default_gmres_opts(tol=None, restart=None, max_iters=None):
+def default_gmres_opts(tol=None, restart=None, max_iters=None, precond=None):
     o = GmresOpts()
     lib().bpqn_default_gmres_opts(ctypes.byref(o))
+    if precond is not None:
+        o.precond = precond
     if tol is not None:
         o.tol = tol
     if restart is not None:

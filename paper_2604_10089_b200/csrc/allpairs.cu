@@ -25,6 +25,8 @@
 //    6 FP64 instructions instead of the 9 of rsqrt() + powers.  rho = 0 (the target's
 //    own node) zeroes the seed with an integer select, so that pair contributes 0.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "bpqn_internal.h"
 
@@ -45,13 +47,13 @@ struct Rec<MODE_S> { static constexpr int n = 6; };    // y0 y1 y2 f0 f1 f2
 template <>
 struct Rec<MODE_D> { static constexpr int n = 10; };   // y0 y1 y2 n0 n1 n2 q0 q1 q2 pad
 template <>
-struct Rec<MODE_SD> { static constexpr int n = 12; };  // y0 y1 y2 n0 n1 n2 f0 f1 f2 q0 q1 q2
+struct Rec<MODE_SD> { static constexpr int n = 14; };  // y0 y1 y2 n0 n1 n2 f0 f1 f2 q0 q1 q2 pad pad
 
 __global__ void k1_pack(int mode, int N, int npad, const double* __restrict__ src, const double* __restrict__ sigS,
                         const double* __restrict__ sigD, double cS, double cD, double* __restrict__ out) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= npad) return;
-  const int rec = mode == MODE_S ? 6 : (mode == MODE_D ? 10 : 12);
+  const int rec = mode == MODE_S ? 6 : (mode == MODE_D ? 10 : 14);
   double* o = out + (size_t)rec * j;
   if (j >= N) {  // far away, zero strength
     o[0] = o[1] = o[2] = 1e30;
@@ -86,6 +88,7 @@ __global__ void k1_pack(int mode, int N, int npad, const double* __restrict__ sr
       o[9] = d * sigD[3 * (size_t)j];
       o[10] = d * sigD[3 * (size_t)j + 1];
       o[11] = d * sigD[3 * (size_t)j + 2];
+      o[12] = o[13] = 0.0;
     }
   }
 }
@@ -273,44 +276,336 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
   }
 }
 
+// ---------------------------------------------------------------- symmetric K1
+// Newton's third law: every unordered pair {i, j} of distinct blocks is evaluated
+// once and contributes to both u_i and u_j, sharing r, rho^2 and the rho^-k powers
+// (D mode: 35 FP64 instructions per pair = 17.5 per interaction, vs 24 above).
+//  * points are cut into blocks of KS_B = 32 R KS_W; a CTA holds one block as
+//    targets (R per lane, with their own n / f~ / q~ for the reverse direction);
+//  * work units (block b, 64-point source tile t) with t >= the block's first tile;
+//    tiles inside the block ("diagonal") run the one-directional loop, later tiles
+//    the symmetric one -- each unordered pair is covered exactly once;
+//  * symmetric loop per 32-point group: at step k lane l evaluates source
+//    (l + k) mod 32 (lane-distinct, conflict-free LDS.128 from the TMA ring) and
+//    carries that source's accumulator, which rotates one lane per step by
+//    __shfl_sync; after 32 steps lane l holds source l's sum.  The 8 warps' sums
+//    are reduced through shared memory and added with one fp64 atomic per value.
+// launch shapes (warps per CTA W, targets per lane R, min CTAs per SM) tried on B200
+struct SymCfg { int w, r, minb; };
+
+struct K1SymParams {
+  const double* pk;  // packed records [npad][REC] (targets and sources)
+  double* out;       // [N][3], zeroed, atomically accumulated
+  int N, nb, nt;     // blocks of KS_B points, tiles of K1_TS points
+  long long units;
+};
+
+template <int MODE>
+struct TgtN { static constexpr int n = MODE == MODE_S ? 6 : (MODE == MODE_D ? 9 : 12); };
+
+template <int MODE, int R, bool SYM>
+__device__ __forceinline__ void k1_group(const double* __restrict__ gr, const double (&tg)[R][TgtN<MODE>::n],
+                                         double (&acc)[R][3], int lane, double& as0, double& as1, double& as2) {
+  constexpr int REC = Rec<MODE>::n;
+#pragma unroll 2
+  for (int k = 0; k < 32; ++k) {
+    const int j = (lane + k) & 31;
+    const double2* rp = reinterpret_cast<const double2*>(gr + j * REC);
+    double sc[REC];
+#pragma unroll
+    for (int h = 0; h < REC / 2; ++h) {
+      const double2 v = rp[h];
+      sc[2 * h] = v.x;
+      sc[2 * h + 1] = v.y;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const double r0 = tg[r][0] - sc[0], r1 = tg[r][1] - sc[1], r2 = tg[r][2] - sc[2];
+      const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+      const double y = seed_or_zero(rr);
+      const double y2 = y * y;
+      const double e = fma(-rr, y2, 1.0);
+      if (MODE == MODE_D) {
+        const double c5 = fma(e, fma(e, 4.375, 2.5), 1.0);
+        const double y4 = y2 * y2;
+        const double s5 = (y * y4) * c5;
+        const double rn = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
+        const double rq = fma(r2, sc[8], fma(r1, sc[7], r0 * sc[6]));
+        const double tf = (rn * rq) * s5;
+        acc[r][0] = fma(r0, tf, acc[r][0]);
+        acc[r][1] = fma(r1, tf, acc[r][1]);
+        acc[r][2] = fma(r2, tf, acc[r][2]);
+        if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5
+          const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+          const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
+          const double tb = (rn2 * rq2) * s5;
+          as0 = fma(-r0, tb, as0);
+          as1 = fma(-r1, tb, as1);
+          as2 = fma(-r2, tb, as2);
+        }
+      } else {
+        const double s = fma(y * e, fma(e, 0.375, 0.5), y);
+        const double s2 = s * s;
+        const double s3 = s2 * s;
+        if (MODE == MODE_S) {
+          const double rf = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
+          const double tf = rf * s3;
+          acc[r][0] = fma(sc[3], s, fma(r0, tf, acc[r][0]));
+          acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
+          acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
+          if (SYM) {  // G(-r) = G(r)
+            const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+            const double tb = rf2 * s3;
+            as0 = fma(tg[r][3], s, fma(r0, tb, as0));
+            as1 = fma(tg[r][4], s, fma(r1, tb, as1));
+            as2 = fma(tg[r][5], s, fma(r2, tb, as2));
+          }
+        } else {
+          const double s5 = s3 * s2;
+          const double rn = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
+          const double rf = fma(r2, sc[8], fma(r1, sc[7], r0 * sc[6]));
+          const double rq = fma(r2, sc[11], fma(r1, sc[10], r0 * sc[9]));
+          const double tf = fma(rf, s3, (rn * rq) * s5);
+          acc[r][0] = fma(sc[6], s, fma(r0, tf, acc[r][0]));
+          acc[r][1] = fma(sc[7], s, fma(r1, tf, acc[r][1]));
+          acc[r][2] = fma(sc[8], s, fma(r2, tf, acc[r][2]));
+          if (SYM) {
+            const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+            const double rf2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
+            const double rq2 = fma(r2, tg[r][11], fma(r1, tg[r][10], r0 * tg[r][9]));
+            const double tb = fma(rf2, s3, -((rn2 * rq2) * s5));
+            as0 = fma(tg[r][6], s, fma(r0, tb, as0));
+            as1 = fma(tg[r][7], s, fma(r1, tb, as1));
+            as2 = fma(tg[r][8], s, fma(r2, tb, as2));
+          }
+        }
+      }
+    }
+    if (SYM) {  // the source accumulators travel with the sources: lane l takes lane l+1's
+      const int from = (lane + 1) & 31;
+      as0 = __shfl_sync(0xffffffffu, as0, from);
+      as1 = __shfl_sync(0xffffffffu, as1, from);
+      as2 = __shfl_sync(0xffffffffu, as2, from);
+    }
+  }
+}
+
+template <int MODE, int KS_W, int R, int MINB>
+__global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
+  constexpr int REC = Rec<MODE>::n;
+  constexpr int TN = TgtN<MODE>::n;  // per target: x and its own densities (reverse direction)
+  constexpr int KS_B = 32 * R * KS_W;
+  constexpr int TPB = KS_B / K1_TS;
+  constexpr int TILE_DBL = K1_TS * REC;
+  constexpr unsigned TILE_BYTES = TILE_DBL * 8;
+  constexpr int NS = K1_STAGES;
+  extern __shared__ __align__(128) double k1_dyn[];
+  double (*ring)[TILE_DBL] = reinterpret_cast<double (*)[TILE_DBL]>(k1_dyn);            // [NS][TILE_DBL]
+  double (*red)[KS_W][K1_TS * 3] =
+      reinterpret_cast<double (*)[KS_W][K1_TS * 3]>(k1_dyn + NS * TILE_DBL);             // [2][W][192]
+  __shared__ __align__(8) uint64_t full[NS];
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const long long u0 = P.units * blockIdx.x / gridDim.x;
+  const long long u1 = P.units * (blockIdx.x + 1) / gridDim.x;
+  if (u0 >= u1) return;
+  // unit u0 -> (block, tile); units run block-major, tiles from the block's first tile to the end
+  int b_cur = 0;
+  long long base = 0;
+  while (base + (P.nt - b_cur * TPB) <= u0) {
+    base += P.nt - b_cur * TPB;
+    ++b_cur;
+  }
+  int t_cur = b_cur * TPB + (int)(u0 - base);
+  int pb = b_cur, pt = t_cur;  // producer iterator (meaningful in thread 0 only)
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0) {
+    for (int s = 0; s < NS && u0 + s < u1; ++s) {
+      mbar_expect_tx(&full[s], TILE_BYTES);
+      bulk_g2s(ring[s], P.pk + (size_t)pt * TILE_DBL, TILE_BYTES, &full[s]);
+      if (++pt == P.nt) pt = ++pb * TPB;
+    }
+  }
+
+  double tg[R][TN], acc[R][3];
+  int loaded_b = -1, par = 0;
+  for (long long u = u0; u < u1; ++u) {
+    const int i = (int)(u - u0);
+    const int buf = i % NS;
+    const unsigned parity = (unsigned)(i / NS) & 1u;
+    if (b_cur != loaded_b) {
+      if (loaded_b >= 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int t = loaded_b * KS_B + warp * 32 * R + r * 32 + lane;
+          if (t < P.N) {
+            atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
+            atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
+            atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
+          }
+        }
+      }
+      loaded_b = b_cur;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int t = b_cur * KS_B + warp * 32 * R + r * 32 + lane;  // < npad
+        const double* rec = P.pk + (size_t)REC * t;
+#pragma unroll
+        for (int c = 0; c < TN; ++c) tg[r][c] = rec[c];
+        acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+      }
+    }
+    const bool diag = t_cur < (b_cur + 1) * TPB;
+    mbar_wait(&full[buf], parity);
+#pragma unroll 1
+    for (int grp = 0; grp < K1_TS / 32; ++grp) {
+      const double* gr = ring[buf] + grp * 32 * REC;
+      double as0 = 0.0, as1 = 0.0, as2 = 0.0;
+      if (diag) {
+        k1_group<MODE, R, false>(gr, tg, acc, lane, as0, as1, as2);
+      } else {
+        k1_group<MODE, R, true>(gr, tg, acc, lane, as0, as1, as2);
+        double* rw = red[par][warp] + (grp * 32 + lane) * 3;
+        rw[0] = as0;
+        rw[1] = as1;
+        rw[2] = as2;
+      }
+    }
+    __syncthreads();  // ring[buf] consumed by every warp; red[par] complete
+    if (!diag) {
+      if (tid < K1_TS * 3) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < KS_W; ++w) sum += red[par][w][tid];
+        if (t_cur * K1_TS + tid / 3 < P.N) atomicAdd(P.out + 3 * (size_t)t_cur * K1_TS + tid, sum);
+      }
+      par ^= 1;
+    }
+    if (tid == 0 && u + NS < u1) {
+      mbar_expect_tx(&full[buf], TILE_BYTES);
+      bulk_g2s(ring[buf], P.pk + (size_t)pt * TILE_DBL, TILE_BYTES, &full[buf]);
+      if (++pt == P.nt) pt = ++pb * TPB;
+    }
+    if (++t_cur == P.nt) t_cur = ++b_cur * TPB;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int t = loaded_b * KS_B + warp * 32 * R + r * 32 + lane;
+    if (t < P.N) {
+      atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
+      atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
+      atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
+    }
+  }
+}
+
 // Algorithmic flops per target-source pair of the fused formulation (DESIGN.md
 // "Roofline"): S 28, D 29, S+D 42 (the rsqrt counted as one operation).
 double allpairs_flops_per_pair(int mode) { return mode == MODE_S ? 28.0 : (mode == MODE_D ? 29.0 : 42.0); }
 
-template <int MODE>
-static int k1_grid(Geom& g) {
-  static int occ[3] = {0, 0, 0};
-  if (!occ[MODE]) {
-    int b = 0;
-    BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_allpairs<MODE>, K1_THREADS, 0));
-    occ[MODE] = std::max(1, b);
-  }
-  return occ[MODE] * g.sms;
+template <class K>
+static int k1_grid(Geom& g, K kern, int threads) {
+  int b = 0;
+  BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kern, threads, 0));
+  return std::max(1, b) * g.sms;
 }
 
-void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
+// K1 variant: symmetric (default) or one-directional (BPQN_K1=asym; A/B and self-check)
+static bool k1_symmetric() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BPQN_K1");
+    v = (e && std::string(e) == "asym") ? 0 : 1;
+  }
+  return v == 1;
+}
+
+template <int MODE, int W, int R, int MINB>
+static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
+  constexpr int KS_B = 32 * R * W;
+  K1SymParams P;
+  P.pk = g.packed.p;
+  P.out = out;
+  P.N = g.n;
+  P.nb = (g.n + KS_B - 1) / KS_B;
+  P.nt = P.nb * (KS_B / K1_TS);
+  P.units = 0;
+  for (int b = 0; b < P.nb; ++b) P.units += P.nt - b * (KS_B / K1_TS);
+  const int smem = (K1_STAGES * K1_TS * Rec<MODE>::n + 2 * W * K1_TS * 3) * 8;
+  static int grid = 0;
+  if (!grid) {
+    BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    int b = 0;
+    BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB>, 32 * W, smem));
+    grid = std::max(1, b) * g.sms;
+  }
+  const int gr = (int)std::min<long long>(grid, P.units);
+  k1_sym<MODE, W, R, MINB><<<gr, 32 * W, smem, st>>>(P);
+}
+
+// Launch shape per mode, measured on B200 at c4 (profiles/r01_k1_sym_shapes.md): D and S
+// are fastest with 12 warps x 3 targets/lane at 1 CTA/SM (168 regs), S+D with 8 x 3.
+// BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
+static int k1_cfg() {
+  static int v = -2;
+  if (v == -2) {
+    const char* e = getenv("BPQN_K1_CFG");
+    v = e ? atoi(e) : -1;
+  }
+  return v;
+}
+
+template <int MODE>
+static void launch_sym(Geom& g, double* out, cudaStream_t st) {
+  int c = k1_cfg();
+  if (c < 0) c = MODE == MODE_SD ? 3 : 1;
+  switch (c) {
+    case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
+    case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
+    case 3: launch_sym_cfg<MODE, 8, 3, 1>(g, out, st); break;
+    default: launch_sym_cfg<MODE, 8, 2, 2>(g, out, st); break;
+  }
+}
+
+template <int MODE>
+static void launch_asym(Geom& g, double* out, cudaStream_t st) {
   K1Params P;
   P.N = g.n;
   P.n_tb = (g.n + K1_TB - 1) / K1_TB;
   P.n_st = (g.n + K1_TS - 1) / K1_TS;
   P.units = (long long)P.n_tb * P.n_st;
-  const int npad = P.n_st * K1_TS;
-  g.packed.ensure((size_t)npad * 12);
-  k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
-                                             -3.0 / (4.0 * PI_A), g.packed.p);
-  BPQN_CHECK_LAUNCH();
   P.X = g.X.p;
   P.pk = g.packed.p;
   P.out = out;
+  static int grid = 0;
+  if (!grid) grid = k1_grid(g, k1_allpairs<MODE>, K1_THREADS);
+  const int gr = (int)std::min<long long>(grid, P.units);
+  k1_allpairs<MODE><<<gr, K1_THREADS, 0, st>>>(P);
+}
+
+void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
+  const bool sym = k1_symmetric();
+  constexpr int KS_B_MAX = 9216;  // multiple of every block size used (512, 768, 1024, 1152)
+  // packed records cover every target block / source tile of either variant
+  const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
+  g.packed.ensure((size_t)npad * 14);
+  k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
+                                             -3.0 / (4.0 * PI_A), g.packed.p);
+  BPQN_CHECK_LAUNCH();
   BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
-  int grid;
-  if (mode == MODE_D) grid = k1_grid<MODE_D>(g);
-  else if (mode == MODE_S) grid = k1_grid<MODE_S>(g);
-  else grid = k1_grid<MODE_SD>(g);
-  grid = (int)std::min<long long>(grid, P.units);
-  if (mode == MODE_D) k1_allpairs<MODE_D><<<grid, K1_THREADS, 0, st>>>(P);
-  else if (mode == MODE_S) k1_allpairs<MODE_S><<<grid, K1_THREADS, 0, st>>>(P);
-  else k1_allpairs<MODE_SD><<<grid, K1_THREADS, 0, st>>>(P);
+  if (sym) {
+    if (mode == MODE_D) launch_sym<MODE_D>(g, out, st);
+    else if (mode == MODE_S) launch_sym<MODE_S>(g, out, st);
+    else launch_sym<MODE_SD>(g, out, st);
+  } else {
+    if (mode == MODE_D) launch_asym<MODE_D>(g, out, st);
+    else if (mode == MODE_S) launch_asym<MODE_S>(g, out, st);
+    else launch_asym<MODE_SD>(g, out, st);
+  }
   BPQN_CHECK_LAUNCH();
   g.prof.allpairs_launches++;
   g.prof.launches += 2;

@@ -101,6 +101,7 @@ struct Geom {
   DBuf<double> E_S;   // S_self - naive same-sphere Stokeslet
   DBuf<double> E_L;   // D_self - naive same-sphere stresslet (layer operator)
   DBuf<double> E_A;   // E_L - I/2 + Pi_R (GMRES operator)
+  DBuf<double> Minv;  // inverse of the same-sphere block D_self - I/2 + Pi_R (block-Jacobi, K4)
 
   // near incidences (sorted by target); matrices [n_inc][3][3nq] per kernel kind
   long long n_inc = 0;
@@ -134,7 +135,8 @@ struct Geom {
 // ---------------------------------------------------------------- kernels / passes
 enum Mode { MODE_S = 0, MODE_D = 1, MODE_SD = 2 };
 
-void precompute(Geom& g, cudaStream_t st);  // self E matrices + near matrices
+void precompute(Geom& g, cudaStream_t st);
+void invert_in_place(double* A, int n, cudaStream_t st);  // Gauss-Jordan, partial pivoting  // self E matrices + near matrices
 
 // out = Layer(sigmaS, sigmaD) with the given self matrix (E), mode selects the kernels.
 // Es used for sigS, Ed for sigD (either may be null when the density is null).

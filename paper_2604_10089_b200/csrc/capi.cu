@@ -100,6 +100,7 @@ void bpqn_default_gmres_opts(bpqn_gmres_opts* o) {
   o->tol = 1e-12;
   o->restart = 50;
   o->max_iters = 1000;
+  o->precond = 1;
 }
 
 void bpqn_default_solve_opts(bpqn_solve_opts* o) {

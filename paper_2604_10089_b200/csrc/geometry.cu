@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
 // E_L likewise with Dring and naive_D; E_A = E_L - I/2 + Pi_R.
 __global__ void k_self_expand(int p, int nq, double a, double mu, const double* xi, const double* w,
                               const double* phi, const double* Sring, const double* Dring, double* ES,
-                              double* EL, double* EA, int want_s) {
+                              double* EL, double* EA, double* EB, int want_s) {
   size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)nq * nq) return;
   int i = (int)(idx / nq), j = (int)(idx % nq);
@@ -487,9 +487,101 @@ __global__ void k_self_expand(int p, int nq, double a, double mu, const double* 
           double pir = (u == v ? cu + co * ri_rj : 0.0) - co * rj[u] * ri[v];
           double half = (i == j && u == v) ? 0.5 : 0.0;
           EA[(3 * (size_t)i + u) * ld + 3 * j + v] = el - half + pir;
+          // the whole same-sphere block of A_op (D_self - I/2 + Pi_R), for the preconditioner
+          if (EB) EB[(3 * (size_t)i + u) * ld + 3 * j + v] = Rt[3 * u + v] - half + pir;
         }
     }
   }
+}
+
+// ------------------------------------------------------------------ block-Jacobi inverse
+// In-place Gauss-Jordan inversion with partial (row) pivoting of the n x n same-sphere
+// block of A_op (identical for every sphere): per pivot column one single-CTA kernel
+// (pivot search, row swap, row scaling, elimination factors) and one grid-wide rank-1
+// elimination; column swaps undo the pivoting at the end.  Preconditioner of K4.
+__global__ void k_gj_pivot(double* A, int n, int k, double* fcol, int* piv) {
+  __shared__ double bv[1024];
+  __shared__ int bi[1024];
+  double best = -1.0;
+  int bidx = k;
+  for (int i = k + threadIdx.x; i < n; i += blockDim.x) {
+    const double v = fabs(A[(size_t)i * n + k]);
+    if (v > best) {
+      best = v;
+      bidx = i;
+    }
+  }
+  bv[threadIdx.x] = best;
+  bi[threadIdx.x] = bidx;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      const double a = bv[threadIdx.x], b = bv[threadIdx.x + o];
+      const int ia = bi[threadIdx.x], ib = bi[threadIdx.x + o];
+      if (b > a || (b == a && ib < ia)) {
+        bv[threadIdx.x] = b;
+        bi[threadIdx.x] = ib;
+      }
+    }
+    __syncthreads();
+  }
+  const int p = bi[0];
+  if (threadIdx.x == 0) piv[k] = p;
+  if (p != k)
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      const double t = A[(size_t)k * n + j];
+      A[(size_t)k * n + j] = A[(size_t)p * n + j];
+      A[(size_t)p * n + j] = t;
+    }
+  __syncthreads();
+  const double d = 1.0 / A[(size_t)k * n + k];
+  __syncthreads();
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    const double v = (j == k) ? 1.0 : A[(size_t)k * n + j];
+    A[(size_t)k * n + j] = v * d;
+  }
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    fcol[i] = (i == k) ? 0.0 : A[(size_t)i * n + k];
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < n; i += blockDim.x)
+    if (i != k) A[(size_t)i * n + k] = 0.0;
+}
+
+__global__ void k_gj_elim(double* A, int n, int k, const double* fcol) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= n || i == k) return;
+  const double f = fcol[i];
+  if (f != 0.0) A[(size_t)i * n + j] = fma(-f, A[(size_t)k * n + j], A[(size_t)i * n + j]);
+}
+
+__global__ void k_gj_colswap(double* A, int n, const int* piv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  for (int k = n - 1; k >= 0; --k) {
+    const int p = piv[k];
+    if (p != k) {
+      const double t = A[(size_t)i * n + k];
+      A[(size_t)i * n + k] = A[(size_t)i * n + p];
+      A[(size_t)i * n + p] = t;
+    }
+  }
+}
+
+void invert_in_place(double* A, int n, cudaStream_t st) {
+  DBuf<double> fcol;
+  DBuf<int> piv;
+  fcol.alloc(n);
+  piv.alloc(n);
+  dim3 eg((n + 255) / 256, n);
+  for (int k = 0; k < n; ++k) {
+    k_gj_pivot<<<1, 1024, 0, st>>>(A, n, k, fcol.p, piv.p);
+    k_gj_elim<<<eg, 256, 0, st>>>(A, n, k, fcol.p);
+  }
+  k_gj_colswap<<<(n + 127) / 128, 128, 0, st>>>(A, n, piv.p);
+  BPQN_CHECK_LAUNCH();
+  BPQN_CUDA(cudaStreamSynchronize(st));
 }
 
 // ------------------------------------------------------------------ driver
@@ -554,11 +646,13 @@ void precompute(Geom& g, cudaStream_t st) {
   if (g.single_layer) g.E_S.alloc(ne);
   g.E_L.alloc(ne);
   g.E_A.alloc(ne);
+  g.Minv.alloc(ne);
   size_t nn = (size_t)nq * nq;
   k_self_expand<<<(unsigned)((nn + 255) / 256), 256, 0, st>>>(p, nq, g.a, g.mu, g.xi_d.p, g.w_d.p, dphi.p,
-                                                             Sring.p, Dring.p, g.E_S.p, g.E_L.p, g.E_A.p,
+                                                             Sring.p, Dring.p, g.E_S.p, g.E_L.p, g.E_A.p, g.Minv.p,
                                                              g.single_layer ? 1 : 0);
   BPQN_CHECK_LAUNCH();
+  invert_in_place(g.Minv.p, 3 * nq, st);
 
   // near incidences
   if (g.n_inc > 0) {

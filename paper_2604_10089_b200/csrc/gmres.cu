@@ -14,6 +14,7 @@
 namespace bpqn {
 
 constexpr int GT = 256;
+constexpr int GM_MAX_RESTART = 500;
 
 // partial dots red[i * nbx + bx] = sum_{e in slice bx} V_i[e] * w[e], i = blockIdx.y
 __global__ void k_mdot(const double* __restrict__ V, size_t ld, const double* __restrict__ w, size_t n,
@@ -56,8 +57,8 @@ __global__ void k_reduce_rows(const double* red, int nbx, double* out, int accum
 // w -= sum_{i<kv} V_i h_i ; red[bx] = partial |w|^2 (if red)
 __global__ void k_mupdate(const double* __restrict__ V, size_t ld, int kv, const double* __restrict__ h,
                           double* w, size_t n, double* red, int nbx) {
-  __shared__ double sh[64];
-  if (threadIdx.x < kv) sh[threadIdx.x] = h[threadIdx.x];
+  __shared__ double sh[GM_MAX_RESTART + 1];
+  for (int i = threadIdx.x; i < kv; i += blockDim.x) sh[i] = h[i];
   __syncthreads();
   double nrm = 0.0;
   for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n; e += (size_t)nbx * GT) {
@@ -154,8 +155,8 @@ __global__ void k_init_cycle(double* S, GmLayout L, double beta) {
 
 // x += V[0:kk] y  (y on device)
 __global__ void k_add_basis(const double* __restrict__ V, size_t ld, int kk, const double* y, double* x, size_t n) {
-  __shared__ double sy[64];
-  if (threadIdx.x < kk) sy[threadIdx.x] = y[threadIdx.x];
+  __shared__ double sy[GM_MAX_RESTART + 1];
+  for (int i = threadIdx.x; i < kk; i += blockDim.x) sy[i] = y[i];
   __syncthreads();
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     double acc = x[e];
@@ -194,7 +195,8 @@ static double read_scalar(Geom& g, const double* dev, cudaStream_t st) {
 int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, bpqn_gmres_stats& stt,
                 cudaStream_t st) {
   const size_t n = 3 * (size_t)g.n;
-  const int m = std::max(1, std::min(o.restart, 60));
+  const int m = std::max(1, std::min(o.restart, GM_MAX_RESTART));
+  const bool pre = o.precond != 0 && g.Minv.p != nullptr;  // block-Jacobi (K4)
   GmLayout L(m);
   g.V.ensure((size_t)(m + 1) * n);
   int nbx = nbx_for(n, g.sms);
@@ -253,7 +255,12 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
     for (int k = 0; k < m; ++k) {
       double* vk = g.V.p + (size_t)k * ld;
       double* w = g.V.p + (size_t)(k + 1) * ld;
-      apply_operator(g, nullptr, vk, nullptr, g.E_A.p, w, st);
+      if (pre) {  // right preconditioning: w = A_op M^-1 v_k
+        launch_self_gemm(g, g.Minv.p, vk, nullptr, nullptr, g.tmp2.p, 0, st);
+        apply_operator(g, nullptr, g.tmp2.p, nullptr, g.E_A.p, w, st);
+      } else {
+        apply_operator(g, nullptr, vk, nullptr, g.E_A.p, w, st);
+      }
       // CGS2
       k_mdot<<<dim3(nbx, k + 1), GT, 0, st>>>(g.V.p, ld, w, n, g.red.p, nbx);
       k_reduce_rows<<<k + 1, 256, 0, st>>>(g.red.p, nbx, S + L.h1, 0);
@@ -285,7 +292,13 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       }
     }
     k_backsolve<<<1, 32, 0, st>>>(S, L, kk);
-    k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, kk, S + L.y, x, n);
+    if (pre) {  // x += M^-1 (V y)
+      BPQN_CUDA(cudaMemsetAsync(g.tmp2.p, 0, n * sizeof(double), st));
+      k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, kk, S + L.y, g.tmp2.p, n);
+      launch_self_gemm(g, g.Minv.p, g.tmp2.p, nullptr, nullptr, x, 1, st);
+    } else {
+      k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, kk, S + L.y, x, n);
+    }
     BPQN_CHECK_LAUNCH();
     g.prof.launches += 2;
     if (done) break;

@@ -14,7 +14,34 @@ namespace bpqn {
 
 // ------------------------------------------------------------------ K2
 // One warp per (near target, component a): sum over the target's incidences of
-// dot(M[inc][a][:], sigma_m[:]) (length 3nq).  Deterministic, no atomics.
+// dot(M[inc][a][:], sigma_m[:]) (length 3nq, even).  The correction rows stream from
+// HBM exactly once per apply (16-byte streaming loads, 4 in flight per lane); the
+// densities are L2-resident.  Deterministic, no atomics.
+__device__ __forceinline__ double dot_row(const double* __restrict__ row, const double* __restrict__ sg, int len2,
+                                          int lane, double acc) {
+  const double2* r2 = reinterpret_cast<const double2*>(row);
+  const double2* s2 = reinterpret_cast<const double2*>(sg);
+  int c = lane;
+  for (; c + 96 < len2; c += 128) {
+    const double2 a0 = __ldcs(r2 + c), a1 = __ldcs(r2 + c + 32), a2 = __ldcs(r2 + c + 64), a3 = __ldcs(r2 + c + 96);
+    const double2 b0 = __ldg(s2 + c), b1 = __ldg(s2 + c + 32), b2 = __ldg(s2 + c + 64), b3 = __ldg(s2 + c + 96);
+    acc = fma(a0.x, b0.x, acc);
+    acc = fma(a0.y, b0.y, acc);
+    acc = fma(a1.x, b1.x, acc);
+    acc = fma(a1.y, b1.y, acc);
+    acc = fma(a2.x, b2.x, acc);
+    acc = fma(a2.y, b2.y, acc);
+    acc = fma(a3.x, b3.x, acc);
+    acc = fma(a3.y, b3.y, acc);
+  }
+  for (; c < len2; c += 32) {
+    const double2 a0 = __ldcs(r2 + c), b0 = __ldg(s2 + c);
+    acc = fma(a0.x, b0.x, acc);
+    acc = fma(a0.y, b0.y, acc);
+  }
+  return acc;
+}
+
 __global__ void k2_near(int n_targets, const int* nt_list, const int* nt_ptr, const int* inc_m, int nq,
                         const double* MS, const double* sigS, const double* MD, const double* sigD, double* out) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
@@ -23,20 +50,13 @@ __global__ void k2_near(int n_targets, const int* nt_list, const int* nt_ptr, co
   const int tix = warp / 3, a = warp - 3 * tix;
   const int i = nt_list[tix];
   const size_t len = 3 * (size_t)nq;
+  const int len2 = (int)(len / 2);
   double acc = 0.0;
   for (int k = nt_ptr[tix]; k < nt_ptr[tix + 1]; ++k) {
     const int m = inc_m[k];
     const size_t base = ((size_t)k * 3 + a) * len;
-    if (MD) {
-      const double* row = MD + base;
-      const double* sg = sigD + (size_t)m * len;
-      for (size_t c = lane; c < len; c += 32) acc = fma(__ldg(row + c), sg[c], acc);
-    }
-    if (MS) {
-      const double* row = MS + base;
-      const double* sg = sigS + (size_t)m * len;
-      for (size_t c = lane; c < len; c += 32) acc = fma(__ldg(row + c), sg[c], acc);
-    }
+    if (MD) acc = dot_row(MD + base, sigD + (size_t)m * len, len2, lane, acc);
+    if (MS) acc = dot_row(MS + base, sigS + (size_t)m * len, len2, lane, acc);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -59,9 +79,14 @@ void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, c
 }
 
 // ------------------------------------------------------------------ K3
-// C[M x Np] (column n = sphere n, contiguous M = 3nq) = E[M x M] * X[M x Np] (+ adds).
-// CTA tile 64 x 32, K step 16, 4 warps of 32 x 16 each, mma.sync m8n8k4 f64 (DMMA).
-constexpr int GBM = 64, GBN = 32, GBK = 16;
+// C[M x Np] (column n = sphere n, contiguous M = 3nq) = E[M x M] X[M x Np], E row-major,
+// the same for every sphere (translation invariance of the self rule).  FP64 tensor
+// cores via mma.sync m8n8k4 (DMMA; tcgen05 has no f64 kind).  CTA tile 64 x 72
+// (8 warps, each one 8-row strip x 9 n8 tiles), K in stages of 16 through a 3-deep
+// cp.async ring (zero-filled tails), split-K over gridDim.z with fp64 atomics into an
+// output that k3_prologue initialised with the fused additions (K1 + K2 results).
+constexpr int K3_BM = 64, K3_BN = 72, K3_BK = 16, K3_ST = 3, K3_LDA = K3_BK + 4;  // LDA 20: conflict-free fragments
+constexpr int K3_SMEM = K3_ST * (K3_BM + K3_BN) * K3_LDA * 8;
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -69,73 +94,105 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
                : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(128) k3_self_gemm(int M, int Nn, const double* __restrict__ E,
-                                                    const double* __restrict__ X, const double* add1,
-                                                    const double* add2, double* out, int accumulate) {
-  __shared__ double As[GBM][GBK + 1];
-  __shared__ double Bs[GBN][GBK + 1];
-  const int m0 = blockIdx.x * GBM, n0 = blockIdx.y * GBN;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 16;
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const int sz = valid ? 16 : 0;  // 0 -> zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
+}
+
+__global__ void k3_prologue(size_t n, const double* add1, const double* add2, double* out, int accumulate) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    double v = accumulate ? out[e] : 0.0;
+    if (add1) v += add1[e];
+    if (add2) v += add2[e];
+    out[e] = v;
+  }
+}
+
+__global__ void __launch_bounds__(256) k3_self_gemm(int M, int Nn, int kchunk, const double* __restrict__ E,
+                                                    const double* __restrict__ X, double* out) {
+  extern __shared__ __align__(16) double k3_dyn[];
+  double (*As)[K3_BM][K3_LDA] = reinterpret_cast<double (*)[K3_BM][K3_LDA]>(k3_dyn);
+  double (*Bs)[K3_BN][K3_LDA] = reinterpret_cast<double (*)[K3_BN][K3_LDA]>(k3_dyn + K3_ST * K3_BM * K3_LDA);
+  const int m0 = blockIdx.x * K3_BM, n0 = blockIdx.y * K3_BN;
+  const int kb = blockIdx.z * kchunk, ke = min(M, kb + kchunk);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int g = lane >> 2, t4 = lane & 3;
-  double acc[4][2][2];
+  double acc[9][2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-  for (int k0 = 0; k0 < M; k0 += GBK) {
-    __syncthreads();
-    for (int e = threadIdx.x; e < GBM * GBK; e += 128) {
-      int r = e / GBK, c = e - r * GBK;
-      int gr = m0 + r, gc = k0 + c;
-      As[r][c] = (gr < M && gc < M) ? E[(size_t)gr * M + gc] : 0.0;
+  for (int j = 0; j < 9; ++j) acc[j][0] = acc[j][1] = 0.0;
+  const int nst = (ke - kb + K3_BK - 1) / K3_BK;
+  auto load = [&](int s, int k0) {
+    // A: 64 rows x 16 doubles = 512 chunks of 16 B; B: 72 cols x 16 = 576 chunks
+    for (int c = tid; c < K3_BM * (K3_BK / 2) + K3_BN * (K3_BK / 2); c += 256) {
+      if (c < K3_BM * (K3_BK / 2)) {
+        const int r = c >> 3, kk = (c & 7) * 2;
+        const int gr = m0 + r, gk = k0 + kk;
+        const bool v = gr < M && gk < ke;
+        cp_async16(&As[s][r][kk], v ? E + (size_t)gr * M + gk : E, v);
+      } else {
+        const int c2 = c - K3_BM * (K3_BK / 2);
+        const int nn = c2 >> 3, kk = (c2 & 7) * 2;
+        const int gn = n0 + nn, gk = k0 + kk;
+        const bool v = gn < Nn && gk < ke;
+        cp_async16(&Bs[s][nn][kk], v ? X + (size_t)gn * M + gk : X, v);
+      }
     }
-    for (int e = threadIdx.x; e < GBN * GBK; e += 128) {
-      int nn = e / GBK, c = e - nn * GBK;
-      int gn = n0 + nn, gc = k0 + c;
-      Bs[nn][c] = (gn < Nn && gc < M) ? X[(size_t)gn * M + gc] : 0.0;
-    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll
+  for (int s = 0; s < K3_ST - 1; ++s) {
+    if (s < nst) load(s, kb + s * K3_BK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+  }
+  for (int st = 0; st < nst; ++st) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(K3_ST - 2) : "memory");
     __syncthreads();
+    const int nxt = st + K3_ST - 1;
+    if (nxt < nst) load(nxt % K3_ST, kb + nxt * K3_BK);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    const int s = st % K3_ST;
 #pragma unroll
-    for (int kk = 0; kk < GBK; kk += 4) {
-      double af[4], bf[2];
+    for (int kk = 0; kk < K3_BK; kk += 4) {
+      const double a = As[s][warp * 8 + g][kk + t4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[wm + 8 * i + g][kk + t4];
-#pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[wn + 8 * j + g][kk + t4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < 2; ++j) dmma884(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      for (int j = 0; j < 9; ++j) dmma884(acc[j][0], acc[j][1], a, Bs[s][j * 8 + g][kk + t4]);
     }
   }
-  // epilogue: C fragment row = g, cols = 2*t4 + {0,1}
+  // epilogue: fragment row g, cols 2 t4 + {0, 1} of each n8 tile
+  const int row = m0 + warp * 8 + g;
+  if (row < M) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j)
+    for (int j = 0; j < 9; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        int row = m0 + wm + 8 * i + g;
-        int col = n0 + wn + 8 * j + 2 * t4 + h;
-        if (row < M && col < Nn) {
-          size_t o = (size_t)col * M + row;
-          double v = acc[i][j][h];
-          if (add1) v += add1[o];
-          if (add2) v += add2[o];
-          if (accumulate) v += out[o];
-          out[o] = v;
-        }
+        const int col = n0 + j * 8 + 2 * t4 + h;
+        if (col < Nn) atomicAdd(out + (size_t)col * M + row, acc[j][h]);
       }
+  }
 }
 
 void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
                       double* out, int accumulate, cudaStream_t st) {
-  int M = 3 * g.nq;
-  dim3 grid((M + GBM - 1) / GBM, (g.np + GBN - 1) / GBN);
-  k3_self_gemm<<<grid, 128, 0, st>>>(M, g.np, E, X, add1, add2, out, accumulate);
+  const int M = 3 * g.nq;
+  const size_t n = (size_t)M * g.np;
+  k3_prologue<<<(unsigned)std::min<size_t>((n + 255) / 256, 4 * (size_t)g.sms), 256, 0, st>>>(n, add1, add2, out,
+                                                                                            accumulate);
+  const int mt = (M + K3_BM - 1) / K3_BM, nt = (g.np + K3_BN - 1) / K3_BN;
+  // split K so that the grid covers the GPU about twice
+  int ks = std::max(1, std::min((2 * g.sms + mt * nt - 1) / (mt * nt), (M + 8 * K3_BK - 1) / (8 * K3_BK)));
+  int kchunk = (M + ks - 1) / ks;
+  kchunk = ((kchunk + K3_BK - 1) / K3_BK) * K3_BK;
+  ks = (M + kchunk - 1) / kchunk;
+  dim3 grid(mt, nt, ks);
+  static bool attr = false;
+  if (!attr) {
+    BPQN_CUDA(cudaFuncSetAttribute(k3_self_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, K3_SMEM));
+    attr = true;
+  }
+  k3_self_gemm<<<grid, 256, K3_SMEM, st>>>(M, g.np, kchunk, E, X, out);
   BPQN_CHECK_LAUNCH();
-  g.prof.launches++;
+  g.prof.launches += 2;
 }
 
 // ------------------------------------------------------------------ operator

@@ -18,6 +18,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--mode", default="d")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--save", default="")
 a = ap.parse_args()
 cfg = make_config(a.config)
 g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
@@ -33,3 +34,5 @@ pr = bp.profile_get(g)
 print("N", g.N, "mode", a.mode, "k1 ms/launch %.3f" % (pr["ms_allpairs"] / a.reps),
       "TFLOP/s %.2f" % (pr["allpairs_gflop"] / pr["ms_allpairs"]), "k2 %.3f k3 %.3f" % (pr["ms_near"] / a.reps,
                                                                                      pr["ms_self"] / a.reps))
+if a.save:
+    np.save(a.save, u.cpu().numpy())
