@@ -147,6 +147,7 @@ def oracle_mvp_sample(cfg, n_targets, k_g):
     N = X.shape[0]
     rng = np.random.default_rng(7)
     q = rng.standard_normal((N, 3))
+    n_targets = n_targets or N                    # default: one whole coarse pass (~10 s on 16 cores)
     idx = np.sort(rng.choice(N, size=n_targets, replace=False))
     tsph = idx // grid["xi"].shape[0]            # far_sum skips each target's own sphere
     excl_ptr = np.zeros(n_targets + 1, dtype=np.int64)
@@ -182,7 +183,7 @@ def run_reference(args, ws, rank):
         return
     cfg = make_config(args.config)
     k_g, src = oracle_kg(args.config)
-    n_t = args.cpu_sample_targets or 256
+    n_t = args.cpu_sample_targets or 0
     times = []
     for _ in range(args.warmup):
         oracle_mvp_sample(cfg, n_t, k_g)
@@ -190,6 +191,7 @@ def run_reference(args, ws, rank):
         ms, dt, N, passes = oracle_mvp_sample(cfg, n_t, k_g)
         times.append(ms)
     v = float(np.mean(times))
+    n_t = n_t or N
     sample = ("oracle plain-C fp64 coarse stresslet pass for %d of %d targets x all sources, scaled by N/%d x "
               "(k_g+1 = %d) passes (k_g from the oracle's c%s fixture); near/self parts not included" %
               (n_t, N, n_t, passes, src))
@@ -322,10 +324,11 @@ def run_ours(args, ws, rank, local):
 
     if rank == 0 and ws == 1:
         k_g_or, src = oracle_kg(args.config)
-        n_t = args.cpu_sample_targets or 512
+        n_t = args.cpu_sample_targets or 0
         ms_cpu, dt, N, passes = oracle_mvp_sample(cfg, n_t, int(round(k_g)))
+        n_t = n_t or N
         line["cpu_baseline"] = {"value": ms_cpu, "unit": "ms", "cores": cores_used(), "kind": "oracle",
-                                "sample": "oracle plain-C coarse stresslet pass over %d of %d targets (%.1f s), "
+                                "sample": "oracle plain-C coarse stresslet pass over %d of %d targets (%.2f s), "
                                           "scaled by N/%d x %d operator passes; near/self parts excluded"
                                           % (n_t, N, dt, n_t, passes)}
     if rank == 0:

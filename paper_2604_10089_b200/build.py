@@ -30,6 +30,8 @@ def build(force=False, verbose=False):
     for s in SOURCES:
         o = os.path.join(objdir, s + ".o")
         cmd = [NVCC] + FLAGS + ["-c", os.path.join(CSRC, s), "-o", o]
+        if s.endswith(".cpp"):
+            cmd += ["-Xcompiler", "-fopenmp", "-Xcompiler", "-march=x86-64-v3"]
         if s.endswith(".cu") and verbose:
             cmd += ["-Xptxas", "-v"]
         procs.append((s, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -44,7 +46,7 @@ def build(force=False, verbose=False):
     if failed:
         raise RuntimeError("nvcc failed")
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs +
-                          ["-lcudart"])
+                          ["-lcudart", "-lgomp"])
     return LIB
 
 

@@ -6,9 +6,8 @@
 // P:802-810), cached low-fidelity secant (App. D.2).  Readings R11
 // (x~ = x - tau H g), R15 (prox residual with the +[a; a~] term), R16-R19, R22.
 //
-// Runs on the host: Nc <= 540 and rank r <= ~60 make every step O(Nc r^2) ~ tens of
-// microseconds, against an MVP of milliseconds to seconds; one Nc-vector crosses
-// PCIe per MVP.  C^{-1} = (D + UU^T)^{-1} is applied by the Woodbury identity.
+// Runs on the host (OpenMP for the O(Nc r^2) and O(r^3) prox pieces): one Nc-vector
+// crosses PCIe per MVP.  C^{-1} = (D + UU^T)^{-1} is applied by the Woodbury identity.
 #include <algorithm>
 #include <cmath>
 #include <functional>
@@ -118,8 +117,99 @@ bool Bfgs::update(const Vec& s, const Vec& y, const Vec* Bs_in, double curv) {
   return true;
 }
 
+// ------------------------------------------------------------------ dense kernels (host)
+// Row-major small dense linear algebra for the prox; OpenMP over rows once the
+// problem is big enough to pay (Bi-PQN seeds the subproblem memory with every
+// earlier secant pair, so r reaches a few hundred, "full memory").
+static bool par(long long work) { return work > 200000; }
+
+// C[m x p] = A[m x k] B[p x k]^T (+ C if acc)
+static void gemm_nt(const double* A, const double* B, double* C, int m, int p, int k, bool acc) {
+#pragma omp parallel for schedule(static) if (par((long long)m * p * k))
+  for (int i = 0; i < m; ++i) {
+    const double* a = A + (size_t)i * k;
+    for (int j = 0; j < p; ++j) {
+      const double* bb = B + (size_t)j * k;
+      double s = 0.0;
+#pragma omp simd reduction(+ : s)
+      for (int e = 0; e < k; ++e) s += a[e] * bb[e];
+      C[(size_t)i * p + j] = acc ? C[(size_t)i * p + j] + s : s;
+    }
+  }
+}
+
+// in-place Cholesky K = L L^T (lower), false if not positive definite
+static bool cholesky(std::vector<double>& K, int n) {
+  for (int j = 0; j < n; ++j) {
+    double d = K[(size_t)j * n + j];
+    for (int k = 0; k < j; ++k) d -= K[(size_t)j * n + k] * K[(size_t)j * n + k];
+    if (!(d > 0.0)) return false;
+    d = std::sqrt(d);
+    K[(size_t)j * n + j] = d;
+#pragma omp parallel for schedule(static) if (par((long long)(n - j) * j))
+    for (int i = j + 1; i < n; ++i) {
+      double s = K[(size_t)i * n + j];
+      for (int k = 0; k < j; ++k) s -= K[(size_t)i * n + k] * K[(size_t)j * n + k];
+      K[(size_t)i * n + j] = s / d;
+    }
+  }
+  return true;
+}
+
+// X[n x m] (row-major, columns are right-hand sides) <- K^{-1} X with K = L L^T
+static void chol_solve(const std::vector<double>& L, int n, double* X, int m) {
+#pragma omp parallel for schedule(static) if (par((long long)n * n * m))
+  for (int c = 0; c < m; ++c) {
+    for (int i = 0; i < n; ++i) {
+      double s = X[(size_t)i * m + c];
+      for (int k = 0; k < i; ++k) s -= L[(size_t)i * n + k] * X[(size_t)k * m + c];
+      X[(size_t)i * m + c] = s / L[(size_t)i * n + i];
+    }
+    for (int i = n - 1; i >= 0; --i) {
+      double s = X[(size_t)i * m + c];
+      for (int k = i + 1; k < n; ++k) s -= L[(size_t)k * n + i] * X[(size_t)k * m + c];
+      X[(size_t)i * m + c] = s / L[(size_t)i * n + i];
+    }
+  }
+}
+
+// LU with partial pivoting, one right-hand side; trailing update threaded by rows
+static bool lu_solve_par(std::vector<double>& A, int n, Vec& b) {
+  for (int k = 0; k < n; ++k) {
+    int pm = k;
+    for (int i = k + 1; i < n; ++i)
+      if (std::fabs(A[(size_t)i * n + k]) > std::fabs(A[(size_t)pm * n + k])) pm = i;
+    if (A[(size_t)pm * n + k] == 0.0) return false;
+    if (pm != k) {
+      for (int j = 0; j < n; ++j) std::swap(A[(size_t)k * n + j], A[(size_t)pm * n + j]);
+      std::swap(b[k], b[pm]);
+    }
+    const double piv = A[(size_t)k * n + k];
+    const double* rk = &A[(size_t)k * n];
+#pragma omp parallel for schedule(static) if (par((long long)(n - k) * (n - k)))
+    for (int i = k + 1; i < n; ++i) {
+      double* ri = &A[(size_t)i * n];
+      const double f = ri[k] / piv;
+      if (f == 0.0) continue;
+#pragma omp simd
+      for (int j = k; j < n; ++j) ri[j] -= f * rk[j];
+      b[i] -= f * b[k];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < n; ++j) s -= A[(size_t)i * n + j] * b[j];
+    b[i] = s / A[(size_t)i * n + i];
+  }
+  return true;
+}
+
 // ------------------------------------------------------------------ weighted prox
-// prox^B_{x>=0}(x~), B = I + UU^T - VV^T (D = I in both solvers, R19)
+// prox^B_{x>=0}(x~), B = I + UU^T - VV^T (D = I in both solvers, R19), by the dual
+// root of Prop. 1 with Alg. 4's semi-smooth Newton on the
+// residual with the "+[alpha; alpha~]" term restored (R15).  C^{-1} V by Woodbury
+// with one Cholesky factor of I + U^T U; the Jacobian blocks of P:709-712 as
+// products over the active / inactive coordinates.
 Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters) {
   const int n = (int)xt.size();
   const int r = (int)q.U.size();
@@ -134,43 +224,59 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     for (double v : xt) mx = std::max(mx, std::fabs(v));
     tol = 1e-12 * mx;
   }
-  // Woodbury: C^{-1} V = V - U (I + U^T U)^{-1} U^T V
-  std::vector<double> K(r * r);
-  for (int i = 0; i < r; ++i)
-    for (int j = 0; j < r; ++j) K[i * r + j] = dot(q.U[i], q.U[j]) + (i == j ? 1.0 : 0.0);
-  std::vector<Vec> CV(r, Vec(n));
+  std::vector<double> Um((size_t)r * n), Vm((size_t)r * n), CV((size_t)r * n);
   for (int c = 0; c < r; ++c) {
-    Vec rhs(r);
-    for (int i = 0; i < r; ++i) rhs[i] = dot(q.U[i], q.V[c]);
-    if (!lu_solve(K, r, rhs)) throw std::runtime_error("singular Woodbury core");
-    for (int e = 0; e < n; ++e) {
-      double s = q.V[c][e];
-      for (int i = 0; i < r; ++i) s -= q.U[i][e] * rhs[i];
-      CV[c][e] = s;
+    std::copy(q.U[c].begin(), q.U[c].end(), Um.begin() + (size_t)c * n);
+    std::copy(q.V[c].begin(), q.V[c].end(), Vm.begin() + (size_t)c * n);
+  }
+  // C^{-1} V = V - U (I + U^T U)^{-1} U^T V   (rows: CV_c = V_c - sum_i X[i][c] U_i)
+  std::vector<double> K((size_t)r * r), X((size_t)r * r);
+  gemm_nt(Um.data(), Um.data(), K.data(), r, r, n, false);
+  for (int i = 0; i < r; ++i) K[(size_t)i * r + i] += 1.0;
+  if (!cholesky(K, r)) throw std::runtime_error("Woodbury core not positive definite");
+  gemm_nt(Um.data(), Vm.data(), X.data(), r, r, n, false);  // X[i][c] = U_i . V_c
+  chol_solve(K, r, X.data(), r);
+#pragma omp parallel for schedule(static) if (par((long long)r * r * n))
+  for (int c = 0; c < r; ++c) {
+    double* o = &CV[(size_t)c * n];
+    std::copy(&Vm[(size_t)c * n], &Vm[(size_t)c * n] + n, o);
+    for (int i = 0; i < r; ++i) {
+      const double f = X[(size_t)i * r + c];
+      const double* u = &Um[(size_t)i * n];
+#pragma omp simd
+      for (int e = 0; e < n; ++e) o[e] -= f * u[e];
     }
   }
   const int d = 2 * r;
   Vec al(d, 0.0);  // [alpha; alpha~]
   auto residual = [&](const Vec& a, Vec& L, Vec& z, std::vector<char>& act) {
-    Vec y = xt;
-    for (int c = 0; c < r; ++c)
-      for (int e = 0; e < n; ++e) y[e] += CV[c][e] * a[r + c];
+    Vec y = xt, v(n);
+    for (int c = 0; c < r; ++c) {
+      const double* cv = &CV[(size_t)c * n];
+      const double ac = a[r + c];
+      for (int e = 0; e < n; ++e) y[e] += cv[e] * ac;
+    }
+    v = y;
+    for (int c = 0; c < r; ++c) {
+      const double* u = &Um[(size_t)c * n];
+      const double ac = a[c];
+      for (int e = 0; e < n; ++e) v[e] -= u[e] * ac;
+    }
     z.assign(n, 0.0);
     act.assign(n, 0);
-    for (int e = 0; e < n; ++e) {
-      double v = y[e];
-      for (int c = 0; c < r; ++c) v -= q.U[c][e] * a[c];
-      if (v > 0) {
-        z[e] = v;
+    for (int e = 0; e < n; ++e)
+      if (v[e] > 0) {
+        z[e] = v[e];
         act[e] = 1;
       }
-    }
     L.assign(d, 0.0);
     for (int c = 0; c < r; ++c) {
+      const double* u = &Um[(size_t)c * n];
+      const double* vv = &Vm[(size_t)c * n];
       double s1 = 0, s2 = 0;
       for (int e = 0; e < n; ++e) {
-        s1 += q.U[c][e] * (y[e] - z[e]);
-        s2 += q.V[c][e] * (xt[e] - z[e]);
+        s1 += u[e] * (y[e] - z[e]);
+        s2 += vv[e] * (xt[e] - z[e]);
       }
       L[c] = a[c] + s1;
       L[r + c] = a[r + c] + s2;
@@ -186,34 +292,50 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
   residual(al, L, z, act);
   double nr = infn(L);
   int j = 0;
+  std::vector<double> Ua, Va, CVa, Ui, CVi, blk((size_t)r * r);
   for (j = 0; j < jmax && nr > tol; ++j) {
-    // J = [[U^T Lam U, U^T (I-Lam) CV], [V^T Lam U, -V^T Lam CV]] + I
-    std::vector<double> J(d * d, 0.0);
-    for (int a = 0; a < r; ++a)
-      for (int b = 0; b < r; ++b) {
-        double uu = 0, ucv = 0, vu = 0, vcv = 0;
-        for (int e = 0; e < n; ++e) {
-          if (act[e]) {
-            uu += q.U[a][e] * q.U[b][e];
-            vu += q.V[a][e] * q.U[b][e];
-            vcv += q.V[a][e] * CV[b][e];
-          } else {
-            ucv += q.U[a][e] * CV[b][e];
-          }
-        }
-        J[a * d + b] = uu;
-        J[a * d + r + b] = ucv;
-        J[(r + a) * d + b] = vu;
-        J[(r + a) * d + r + b] = -vcv;
+    // J = [[U^T Lam U, U^T (I-Lam) CV], [V^T Lam U, -V^T Lam CV]] + I   (P:709-712)
+    std::vector<int> ia, ii;
+    for (int e = 0; e < n; ++e) (act[e] ? ia : ii).push_back(e);
+    const int na = (int)ia.size(), ni = (int)ii.size();
+    Ua.assign((size_t)r * na, 0.0);
+    Va.assign((size_t)r * na, 0.0);
+    CVa.assign((size_t)r * na, 0.0);
+    Ui.assign((size_t)r * ni, 0.0);
+    CVi.assign((size_t)r * ni, 0.0);
+    for (int c = 0; c < r; ++c) {
+      for (int t = 0; t < na; ++t) {
+        Ua[(size_t)c * na + t] = Um[(size_t)c * n + ia[t]];
+        Va[(size_t)c * na + t] = Vm[(size_t)c * n + ia[t]];
+        CVa[(size_t)c * na + t] = CV[(size_t)c * n + ia[t]];
       }
-    for (int i = 0; i < d; ++i) J[i * d + i] += 1.0;
+      for (int t = 0; t < ni; ++t) {
+        Ui[(size_t)c * ni + t] = Um[(size_t)c * n + ii[t]];
+        CVi[(size_t)c * ni + t] = CV[(size_t)c * n + ii[t]];
+      }
+    }
+    std::vector<double> J((size_t)d * d, 0.0);
+    auto put = [&](int r0, int c0, double sgn) {
+      for (int a = 0; a < r; ++a)
+        for (int b = 0; b < r; ++b) J[(size_t)(r0 + a) * d + c0 + b] = sgn * blk[(size_t)a * r + b];
+    };
+    gemm_nt(Ua.data(), Ua.data(), blk.data(), r, r, na, false);
+    put(0, 0, 1.0);
+    gemm_nt(Ui.data(), CVi.data(), blk.data(), r, r, ni, false);
+    put(0, r, 1.0);
+    gemm_nt(Va.data(), Ua.data(), blk.data(), r, r, na, false);
+    put(r, 0, 1.0);
+    gemm_nt(Va.data(), CVa.data(), blk.data(), r, r, na, false);
+    put(r, r, -1.0);
+    for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1.0;
     Vec step = L;
-    if (!lu_solve(J, d, step)) {
+    std::vector<double> Jc = J;
+    if (!lu_solve_par(Jc, d, step)) {
       double jn = 0;
       for (double v : J) jn = std::max(jn, std::fabs(v));
-      for (int i = 0; i < d; ++i) J[i * d + i] += 1e-10 * jn * d;
+      for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1e-10 * jn * d;
       step = L;
-      if (!lu_solve(J, d, step)) break;
+      if (!lu_solve_par(J, d, step)) break;
     }
     double t = 1.0;
     bool ok = false;
