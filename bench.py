@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--gmres-restart", type=int, default=50)
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
+    ap.add_argument("--recycle", type=int, default=1)   # GMRES recycling inside the LCP solve (NEXT-3)
+    ap.add_argument("--solvers", default="bi")          # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--c5-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-targets", type=int, default=0)
     return ap.parse_args()
@@ -315,7 +317,9 @@ def run_ours(args, ws, rank, local):
         "e2e": {"value": e2e_v, "unit": "ms", "h2d_bytes_per_step": 8 * nc, "d2h_bytes_per_step": 8 * nc},
     }
     if not args.no_solve:
-        line["lcp_solve"] = run_solve(args, cfg, g, pairs, nrm, gaps, dev)
+        for k, meth in enumerate(args.solvers.split(",")):
+            key = "lcp_solve" if k == 0 else "lcp_solve_" + meth
+            line[key] = run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth)
     del g
     torch.cuda.empty_cache()
 
@@ -335,16 +339,16 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
-def run_solve(args, cfg, g, pairs, nrm, gaps, dev):
+def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
     """One full LCP solve at the bench config: b from the Janus-slip non-collisional
     mobility solve, then Bi-PQN (Alg. 3) with the low fidelity at p_lo
     (or Mono-PQN when the config has none), paper-mode tolerances."""
     import torch
     import paper_2604_10089_b200 as bp
-    gmo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart)
+    gmo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart, recycle=int(args.recycle))
     t0 = time.time()
     lo = None
-    if cfg.get("p_lo"):
+    if meth == "bi" and cfg.get("p_lo"):
         lo = bp.Geometry(cfg["centers"], cfg["p_lo"], cfg["radius"], cfg["mu"])
         bp.set_contacts(lo, pairs, nrm, gaps)
     torch.cuda.synchronize()
@@ -356,16 +360,19 @@ def run_solve(args, cfg, g, pairs, nrm, gaps, dev):
     e1.record()
     torch.cuda.synchronize()
     ms_b = e0.elapsed_time(e1)
-    o = bp.default_solve_opts(method=1 if lo is not None else 0, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8)
+    o = bp.default_solve_opts(method=1 if lo is not None else (2 if meth == "bb" else 0), eps_kkt_abs=1e-8,
+                              eps_kkt_rel=1e-8, k_max=500)
     o.gm_hi = gmo
-    o.gm_lo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart)
+    o.gm_lo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart, recycle=int(args.recycle))
     lam = torch.zeros(g.nc, dtype=torch.float64, device=dev)
     t0 = time.perf_counter()
     lam, rep, rc = bp.solve_lcp(g, lo, b, lam, opts=o)
     torch.cuda.synchronize()
     ms_solve = (time.perf_counter() - t0) * 1e3
     r = rep.as_dict()
-    out = {"method": "Bi-PQN" if lo is not None else "Mono-PQN", "p_hi": cfg["p"], "p_lo": cfg.get("p_lo"),
+    out = {"method": {"bi": "Bi-PQN", "mono": "Mono-PQN", "bb": "BB-PGD"}[meth] if (lo is not None or meth != "bi")
+           else "Mono-PQN", "p_hi": cfg["p"], "p_lo": cfg.get("p_lo") if lo is not None else None,
+           "gmres_recycling": bool(args.recycle),
            "ms_b": ms_b, "gmres_iters_b": st_b.iters, "ms_solve": ms_solve, "ms_total": ms_b + ms_solve,
            "rc": rc, "lo_geometry_init_s": round(t_lo_init, 3),
            "negative_b_fraction": float((b < 0).double().mean().item()),

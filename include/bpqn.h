@@ -66,17 +66,24 @@ typedef struct {
   int restart;
   int max_iters;
   int precond;
+  int recycle;        /* 1: start from the least-squares combination of this handle's earlier
+                         solutions and keep this solve's (rhs, solution) pair (Krylov
+                         recycling across the MVPs of one LCP solve).
+                         The store holds up to 256 orthonormalised pairs; it is emptied by
+                         bpqn_gmres_recycle_reset and at the start of bpqn_solve_lcp.  0: off. */
 } bpqn_gmres_opts;
 
 typedef struct {
-  int iters;          /* total GMRES iterations (operator applications in the Krylov loop) */
+  int iters;          /* GMRES (Arnoldi) iterations */
   int restarts;
-  double rel_resid;   /* final relative residual estimate */
+  double rel_resid;   /* final relative residual estimate ||b - A x|| / ||b|| */
   double ms;          /* device time of the whole call (CUDA events) */
+  int applies;        /* operator applications (iterations + restart / initial-guess residuals) */
 } bpqn_gmres_stats;
 
 typedef struct {
-  int method;                 /* 0 = Mono-PQN (Alg. 1), 1 = Bi-PQN (Alg. 3) */
+  int method;                 /* 0 = Mono-PQN (Alg. 1), 1 = Bi-PQN (Alg. 3),
+                                 2 = BB-PGD, the paper's baseline (eq. spectralStepSize) */
   int k_max;                  /* outer iteration cap (default 200) */
   double eps_kkt_abs;         /* ||min(x, Ax+b)||_2 stop, default 1e-10 */
   double eps_kkt_rel;         /* relative KKT stop; <= 0 disables (default 0) */
@@ -153,8 +160,8 @@ int bpqn_lcp_mvp(bpqn_geom_t g, const double* lambda_dev, double* w_dev, const b
 int bpqn_lcp_b(bpqn_geom_t g, const double* fnc_dev, const double* slip_dev, double dt, double* b_dev,
                const bpqn_gmres_opts* gm, bpqn_gmres_stats* st, void* stream);
 
-/* LCP solve 0 <= A x + b  _|_  x >= 0, A = D^T M D by Mono-PQN
- * (lo == NULL or o->method == 0) or Bi-PQN (lo = coarser-p handle over the same
+/* LCP solve 0 <= A x + b  _|_  x >= 0, A = D^T M D by BB-PGD (o->method == 2),
+ * Mono-PQN (lo == NULL or o->method == 0) or Bi-PQN (lo = coarser-p handle over the same
  * spheres with the same contact set).  b_dev [Nc]; lambda_dev [Nc]: in = x_init
  * (>= 0), out = solution.  rep may be NULL. */
 int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* lambda_dev,
@@ -164,6 +171,9 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
  * A_host, Ahat_host [n][n] row-major (Ahat NULL -> Mono-PQN), b_host, x_host [n]. */
 int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, const double* b_host,
                          double* x_host, const bpqn_solve_opts* o, bpqn_report* rep);
+
+/* Empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
+int bpqn_gmres_recycle_reset(bpqn_geom_t g);
 
 /* Thread-local message for the last non-zero return. */
 const char* bpqn_last_error(void);

@@ -15,6 +15,10 @@ Follows PAPER.md in the paper's order and notation, with the readings of SURVEY
 * the gradient cache A x_{k+1} = A x_k + eta A p_k (Remark P:390-392), refreshed
   every 20 iterations (R18);
 * KKT errors eq. (kkt-error) P:531-533 in the Euclidean norm (R12);
+* BB-PGD: projected gradient with the spectral step eq.
+  (spectralStepSize); first step tau = 1 and a non-positive BB denominator reuses
+  the previous tau (R31); one MVP per iteration
+  on the new iterate (A x_{k+1} directly, no cache drift);
 * Alg. 3 Bi-PQN with the subproblem eq. (pqnSubproblem) P:468-470,
   secant re-use P:475-487, cached low-fidelity secant A^ s = eta(A^ x^ - A^ x)
   (App. D.2), sub-solver settings R22.
@@ -254,6 +258,47 @@ def mono_pqn(mvp, b, x0, eps_abs=1e-10, eps_rel=0.0, k_max=200, tau=1.0, refresh
     rep = Report(iterations=it, mvps=mvps, termination=term, kkt_abs=trace[-1],
                  kkt_trace=trace, x_trace=xs, objective=float(0.5 * np.dot(x, g - b) + np.dot(x, b)))
     return x, g, aux_x, pairs, rep
+
+
+def bb_step(s, As, tau_prev):
+    """eq. (spectralStepSize): tau_bb = ||s||^2 / s^T A s; a non-positive denominator
+    reuses the previous tau."""
+    den = float(np.dot(s, As))
+    return float(np.dot(s, s)) / den if den > 0.0 else tau_prev
+
+
+def bb_pgd(mvp, b, x0, eps_abs=1e-10, eps_rel=0.0, k_max=500):
+    """BB-PGD: x_{k+1} = (x_k - tau_k (A x_k + b))_+ with tau_0 = 1, tau_k = tau_bb
+    of the last step.  ``mvp(v) -> A v``.  Returns (x, g, report)."""
+    x = np.maximum(np.array(x0, dtype=np.float64), 0.0)
+    g = mvp(x) + b
+    mvps = 1
+    tau = 1.0
+    prev = None
+    trace = []
+    it = 0
+    term = TERM_MAX_ITER
+    for k in range(k_max):
+        e_abs, e_rel = kkt_errors(x, g, prev)
+        prev = e_abs
+        trace.append(e_abs)
+        if e_abs <= eps_abs:
+            term = TERM_KKT_ABS
+            break
+        if eps_rel > 0 and e_rel <= eps_rel:
+            term = TERM_KKT_REL
+            break
+        x_new = np.maximum(x - tau * g, 0.0)
+        g_new = mvp(x_new) + b
+        mvps += 1
+        s, As = x_new - x, g_new - g
+        tau = bb_step(s, As, tau)
+        x, g = x_new, g_new
+        it += 1
+    else:
+        trace.append(kkt_errors(x, g, prev)[0])
+    rep = Report(iterations=it, mvps=mvps, termination=term, kkt_abs=trace[-1], kkt_trace=trace)
+    return x, g, rep
 
 
 def bi_pqn(mvp_hi, mvp_lo, b, x_init, eps_abs=1e-10, eps_rel=0.0, k_max=100,

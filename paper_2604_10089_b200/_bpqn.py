@@ -21,11 +21,13 @@ class DiscOpts(ctypes.Structure):
 
 
 class GmresOpts(ctypes.Structure):
-    _fields_ = [("tol", c_double), ("restart", c_int), ("max_iters", c_int), ("precond", c_int)]
+    _fields_ = [("tol", c_double), ("restart", c_int), ("max_iters", c_int), ("precond", c_int),
+                ("recycle", c_int)]
 
 
 class GmresStats(ctypes.Structure):
-    _fields_ = [("iters", c_int), ("restarts", c_int), ("rel_resid", c_double), ("ms", c_double)]
+    _fields_ = [("iters", c_int), ("restarts", c_int), ("rel_resid", c_double), ("ms", c_double),
+                ("applies", c_int)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -62,6 +64,7 @@ SYMBOLS = {
     "bpqn_solve_lcp": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(SolveOpts), P(Report), c_void_p]),
     "bpqn_solve_lcp_dense": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, P(SolveOpts), P(Report)]),
     "bpqn_last_error": (ctypes.c_char_p, []),
+    "bpqn_gmres_recycle_reset": (c_int, [c_void_p]),
     "bpqn_profile_get": (c_int, [c_void_p, P(c_double), P(c_double), P(c_double), P(c_double), P(c_longlong),
                                  P(c_longlong)]),
     "bpqn_profile_reset": (c_int, [c_void_p, c_int]),
@@ -125,9 +128,11 @@ def default_disc_opts():
     return o
 
 
-def default_gmres_opts(tol=None, restart=None, max_iters=None, precond=None):
+def default_gmres_opts(tol=None, restart=None, max_iters=None, precond=None, recycle=None):
     o = GmresOpts()
     lib().bpqn_default_gmres_opts(ctypes.byref(o))
+    if recycle is not None:
+        o.recycle = recycle
     if precond is not None:
         o.precond = precond
     if tol is not None:
@@ -276,6 +281,10 @@ def solve_lcp_dense(A, b, x0=None, Ahat=None, opts=None):
     if rc not in (0, 4, 5):
         _check(rc)
     return x, rep, rc
+
+
+def gmres_recycle_reset(g):
+    _check(lib().bpqn_gmres_recycle_reset(g.h))
 
 
 def profile_reset(g, events=True):

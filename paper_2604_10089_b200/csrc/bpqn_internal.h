@@ -125,6 +125,9 @@ struct Geom {
   DBuf<double> red;      // reduction scratch
   DBuf<double> scal;     // device scalars
   DBuf<double> ft, uo;   // [np][6]
+  // GMRES recycling store (gmres.cu): W orthonormal past rhs, Z = A_op^-1 W
+  DBuf<double> rec_W, rec_Z;
+  int rec_k = 0, rec_cap = 0;
   double* host_scal = nullptr;  // pinned
   int gm_restart = 0;
 

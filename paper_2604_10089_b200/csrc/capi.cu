@@ -101,6 +101,7 @@ void bpqn_default_gmres_opts(bpqn_gmres_opts* o) {
   o->restart = 50;
   o->max_iters = 1000;
   o->precond = 1;
+  o->recycle = 0;
 }
 
 void bpqn_default_solve_opts(bpqn_solve_opts* o) {
@@ -118,6 +119,7 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o) {
   o->curv_skip = 1e-12;
   bpqn_default_gmres_opts(&o->gm_hi);
   bpqn_default_gmres_opts(&o->gm_lo);
+  o->gm_hi.recycle = o->gm_lo.recycle = 1;
   o->cost_ratio = 0.0;
 }
 
@@ -410,6 +412,8 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     BPQN_CUDA(cudaMemcpyAsync(x0.data(), lambda_dev, 8 * nc, cudaMemcpyDeviceToHost, s));
     BPQN_CUDA(cudaStreamSynchronize(s));
     for (double v : x0) BPQN_REQUIRE(v >= 0, "x_init must be >= 0");
+    if (o.gm_hi.recycle) hi->rec_k = 0;
+    if (bi && o.gm_lo.recycle) lo->rec_k = 0;
     DBuf<double> dv, dw;
     dv.alloc(nc);
     dw.alloc(nc);
@@ -451,7 +455,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       kkt = r.kkt;
       kkt_rel = r.kkt_rel;
     } else {
-      MonoResult r = mono_pqn(fhi, b, x0, q, nullptr, nullptr, nullptr);
+      MonoResult r = o.method == 2 ? bb_pgd(fhi, b, x0, q) : mono_pqn(fhi, b, x0, q, nullptr, nullptr, nullptr);
       x = r.x;
       iters = r.iterations;
       term = r.termination;
@@ -529,7 +533,7 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
         rep->termination = term;
       }
     } else {
-      MonoResult r = mono_pqn(dense(A), b, x0, q, nullptr, nullptr, nullptr);
+      MonoResult r = o.method == 2 ? bb_pgd(dense(A), b, x0, q) : mono_pqn(dense(A), b, x0, q, nullptr, nullptr, nullptr);
       std::copy(r.x.begin(), r.x.end(), x_host);
       term = r.termination;
       if (rep) {
@@ -542,6 +546,14 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
     }
     if (term == 3) return BPQN_ERR_STALLED;
     if (term == 2) return BPQN_ERR_NOCONV;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_gmres_recycle_reset(bpqn_geom_t g) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    g->rec_k = 0;
     return BPQN_OK;
   });
 }

@@ -215,6 +215,31 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   stt.iters = 0;
   stt.restarts = 0;
   stt.rel_resid = 0.0;
+  stt.applies = 0;
+  // Recycling: W orthonormal past right-hand sides, Z with
+  // A_op Z = W (to the past solves' tolerance).  Initial guess x0 = Z W^T b.
+  const bool rec = o.recycle != 0 && beta_b > 0.0 && std::isfinite(beta_b);
+  if (rec && g.rec_cap == 0) {  // lazily: up to 256 pairs within ~4 GB
+    g.rec_cap = (int)std::max<size_t>(1, std::min<size_t>(256, (size_t)4e9 / (2 * n * sizeof(double))));
+    g.rec_W.alloc((size_t)g.rec_cap * n);
+    g.rec_Z.alloc((size_t)g.rec_cap * n);
+    g.rec_k = 0;
+  }
+  const int kr = rec ? g.rec_k : 0;
+  double* Sc = nullptr;
+  if (rec) {
+    g.red.ensure((size_t)(std::max(m, g.rec_cap) + 2) * nbx + 16);
+    g.scal.ensure(L.total + 2 * (size_t)(g.rec_cap + 1));
+    S = g.scal.p;
+    Sc = S + L.total;
+  }
+  if (kr > 0) {
+    k_mdot<<<dim3(nbx, kr), GT, 0, st>>>(g.rec_W.p, n, b, n, g.red.p, nbx);
+    k_reduce_rows<<<kr, 256, 0, st>>>(g.red.p, nbx, Sc, 0);
+    k_add_basis<<<std::min<int>((int)((n + 255) / 256), g.sms * 8), 256, 0, st>>>(g.rec_Z.p, n, kr, Sc, x, n);
+    BPQN_CHECK_LAUNCH();
+    g.prof.launches += 3;
+  }
   int status = BPQN_OK;
   if (!(beta_b > 0.0)) {
     BPQN_CUDA(cudaEventRecord(e1, st));
@@ -228,7 +253,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   }
   const int blocks_vec = std::min<int>((int)((n + 255) / 256), g.sms * 8);
   double* r = g.tmp.p;
-  bool first = true;
+  bool first = kr == 0;
   double resid = 1.0;
   for (;;) {
     double beta;
@@ -238,12 +263,19 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       k_scale<<<blocks_vec, 256, 0, st>>>(g.V.p, b, n, S + 3, 1);  // V0 = b / beta
       first = false;
     } else {
-      // r = b - A x
+      // r = b - A x (restart, or the recycled initial guess)
       apply_operator(g, nullptr, x, nullptr, g.E_A.p, g.tmp2.p, st);
+      stt.applies++;
       k_sub<<<blocks_vec, 256, 0, st>>>(r, b, g.tmp2.p, n);
       norm2(g, r, n, S + 2, st);
       beta = std::sqrt(read_scalar(g, S + 2, st));
       if (!(beta > 0.0)) break;
+      resid = beta / beta_b;
+      if (!std::isfinite(resid)) {
+        status = BPQN_ERR_NAN;
+        break;
+      }
+      if (resid <= o.tol) break;
       k_set<<<1, 1, 0, st>>>(S + 3, beta);
       k_scale<<<blocks_vec, 256, 0, st>>>(g.V.p, r, n, S + 3, 1);
       stt.restarts++;
@@ -261,6 +293,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       } else {
         apply_operator(g, nullptr, vk, nullptr, g.E_A.p, w, st);
       }
+      stt.applies++;
       // CGS2
       k_mdot<<<dim3(nbx, k + 1), GT, 0, st>>>(g.V.p, ld, w, n, g.red.p, nbx);
       k_reduce_rows<<<k + 1, 256, 0, st>>>(g.red.p, nbx, S + L.h1, 0);
@@ -304,6 +337,31 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
     if (done) break;
   }
   stt.rel_resid = resid;
+  if (rec && status == BPQN_OK && g.rec_k < g.rec_cap) {
+    // append (b, x): CGS2 of b against W with the same coefficients applied to x vs Z
+    const size_t ld2 = n;
+    double* wn = g.rec_W.p + (size_t)g.rec_k * ld2;
+    double* zn = g.rec_Z.p + (size_t)g.rec_k * ld2;
+    BPQN_CUDA(cudaMemcpyAsync(wn, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    BPQN_CUDA(cudaMemcpyAsync(zn, x, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    const int k0 = g.rec_k;
+    for (int pass = 0; pass < 2 && k0 > 0; ++pass) {
+      k_mdot<<<dim3(nbx, k0), GT, 0, st>>>(g.rec_W.p, ld2, wn, n, g.red.p, nbx);
+      k_reduce_rows<<<k0, 256, 0, st>>>(g.red.p, nbx, Sc, 0);
+      k_mupdate<<<nbx, GT, 0, st>>>(g.rec_W.p, ld2, k0, Sc, wn, n, nullptr, nbx);
+      k_mupdate<<<nbx, GT, 0, st>>>(g.rec_Z.p, ld2, k0, Sc, zn, n, nullptr, nbx);
+      g.prof.launches += 4;
+    }
+    norm2(g, wn, n, S + 2, st);
+    const double nw = std::sqrt(read_scalar(g, S + 2, st));
+    if (nw > 1e-8 * beta_b) {  // a new direction: normalise and keep
+      k_set<<<1, 1, 0, st>>>(S + 3, nw);
+      k_scale<<<blocks_vec, 256, 0, st>>>(wn, wn, n, S + 3, 1);
+      k_scale<<<blocks_vec, 256, 0, st>>>(zn, zn, n, S + 3, 1);
+      BPQN_CHECK_LAUNCH();
+      g.rec_k++;
+    }
+  }
   BPQN_CUDA(cudaEventRecord(e1, st));
   BPQN_CUDA(cudaEventSynchronize(e1));
   float ms = 0;

@@ -385,6 +385,59 @@ double optimal_eta(const Vec& x, const Vec& p, const Vec& g, const Vec& Ap, std:
 }
 
 // ------------------------------------------------------------------ Alg. 1
+// ------------------------------------------------------------------ BB-PGD
+// The paper's baseline: x_{k+1} = (x_k - tau_k (A x_k + b))_+ with the
+// spectral step tau_bb = |s|^2 / s^T A s of eq. (spectralStepSize), over-relaxation 1
+// (Table 1).  tau_0 = 1; a non-positive denominator keeps the previous tau (SPEC
+// S:363-365; R31).  One MVP per iteration, on the new iterate.
+MonoResult bb_pgd(const MvpFn& mvp, const Vec& b, const Vec& x0, const PqnOpts& o) {
+  const size_t n = b.size();
+  MonoResult R;
+  R.x.resize(n);
+  for (size_t i = 0; i < n; ++i) R.x[i] = std::max(x0[i], 0.0);
+  Vec Ax;
+  mvp(R.x, Ax, nullptr);
+  R.mvps = 1;
+  R.g.resize(n);
+  for (size_t i = 0; i < n; ++i) R.g[i] = Ax[i] + b[i];
+  double tau = 1.0, prev = -1.0;
+  R.termination = 2;
+  for (int k = 0; k < o.k_max; ++k) {
+    const double e = kkt_abs(R.x, R.g);
+    const double den = prev < 0 ? 0.0 : std::max(e, prev);
+    const double erel = prev < 0 ? std::numeric_limits<double>::infinity() : (den > 0 ? std::fabs(e - prev) / den : 0.0);
+    prev = e;
+    R.kkt = e;
+    R.kkt_rel = erel;
+    if (e <= o.eps_abs) {
+      R.termination = 0;
+      break;
+    }
+    if (o.eps_rel > 0 && erel <= o.eps_rel) {
+      R.termination = 1;
+      break;
+    }
+    Vec xn(n), gn(n);
+    for (size_t i = 0; i < n; ++i) xn[i] = std::max(R.x[i] - tau * R.g[i], 0.0);
+    mvp(xn, Ax, nullptr);
+    R.mvps++;
+    double ss = 0.0, sAs = 0.0;
+    for (size_t i = 0; i < n; ++i) {
+      gn[i] = Ax[i] + b[i];
+      const double si = xn[i] - R.x[i];
+      ss += si * si;
+      sAs += si * (gn[i] - R.g[i]);
+    }
+    if (sAs > 0.0) tau = ss / sAs;
+    R.x.swap(xn);
+    R.g.swap(gn);
+    R.iterations++;
+    if (!std::isfinite(tau)) throw std::runtime_error("BB-PGD: non-finite step");
+  }
+  if (R.termination == 2) R.kkt = kkt_abs(R.x, R.g);
+  return R;
+}
+
 MonoResult mono_pqn(const MvpFn& mvp, const Vec& b, const Vec& x0, const PqnOpts& o, const Vec* g0,
                     const Vec* aux0, const std::vector<std::pair<Vec, Vec>>* seed) {
   const size_t n = b.size();

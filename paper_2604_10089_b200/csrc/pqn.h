@@ -49,6 +49,7 @@ double optimal_eta(const std::vector<double>& x, const std::vector<double>& p, c
 MonoResult mono_pqn(const MvpFn& mvp, const std::vector<double>& b, const std::vector<double>& x0, const PqnOpts& o,
                     const std::vector<double>* g0, const std::vector<double>* aux0,
                     const std::vector<std::pair<std::vector<double>, std::vector<double>>>* seed);
+MonoResult bb_pgd(const MvpFn& mvp, const std::vector<double>& b, const std::vector<double>& x0, const PqnOpts& o);
 BiResult bi_pqn(const MvpFn& hi, const MvpFn& lo, const std::vector<double>& b, const std::vector<double>& x_init,
                 const PqnOpts& o);
 

@@ -136,3 +136,21 @@ def test_dense_pqn_vs_brute_force(lib, seed, method):
     np.testing.assert_allclose(x, ref, atol=1e-9)
     if method == 1:
         assert rep.hi_mvps == rep.iterations + 1 + rep.iterations // 20  # P:574 + refresh every 20 (R18)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_dense_bb_pgd_vs_brute_force(lib, seed):
+    """BB-PGD (method 2) behind the C ABI: SPEC S:366-367 and brute-force LCPs."""
+    import paper_2604_10089_b200 as bp
+    o = bp.default_solve_opts(method=2, eps_kkt_abs=1e-12, k_max=5000)
+    x, rep, rc = bp.solve_lcp_dense(np.eye(2), np.array([-1.0, -1.0]), opts=o)
+    assert rc == 0 and rep.iterations == 1 and np.allclose(x, [1.0, 1.0])
+    rng = np.random.default_rng(50 + seed)
+    n = 8
+    M = rng.standard_normal((n, n))
+    A = M @ M.T / n + 0.5 * np.eye(n)
+    b = rng.standard_normal(n)
+    x, rep, rc = bp.solve_lcp_dense(A, b, opts=o)
+    assert rc == 0
+    np.testing.assert_allclose(x, _brute(A, b), atol=1e-10)
+    assert rep.hi_mvps == rep.iterations + 1

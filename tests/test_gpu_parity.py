@@ -314,3 +314,46 @@ def test_solve_lcp_bi_c3(bp):
     assert rc == 0
     assert rel(lam.cpu().numpy(), z["lam_bi"]) <= TOL_LAM
     assert rep.kkt_abs <= TOL_KKT
+
+
+# ------------------------------------------------------------------ GMRES recycling (NEXT-3)
+def test_gmres_recycling_same_result_fewer_iterations(bp):
+    """Recycled initial guesses change the iteration count, not the MVP (to tolerance):
+    w(l3) for l3 = l1 + 0.5 l2 after solving l1 and l2 equals the cold solve, and a
+    repeated right-hand side converges in at most a couple of Arnoldi iterations."""
+    z = fixture(2)
+    from synth import lambda_test
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    l1, l2 = lambda_test(2, g.nc, 0), lambda_test(2, g.nc, 1)
+    l3 = l1 + 0.5 * l2
+    cold = bp.default_gmres_opts(tol=1e-12)
+    w3, st_cold = bp.lcp_mvp(g, T(l3), gmres=cold)
+    warm = bp.default_gmres_opts(tol=1e-12, recycle=1)
+    bp.gmres_recycle_reset(g)
+    bp.lcp_mvp(g, T(l1), gmres=warm)
+    bp.lcp_mvp(g, T(l2), gmres=warm)
+    w3r, st_warm = bp.lcp_mvp(g, T(l3), gmres=warm)
+    assert rel(w3r.cpu().numpy(), w3.cpu().numpy()) <= TOL_VEL
+    assert st_warm.iters < st_cold.iters
+    w1r, st1 = bp.lcp_mvp(g, T(l1), gmres=warm)
+    assert st1.iters <= 2 and rel(w1r.cpu().numpy(), z["w_test"][0]) <= TOL_VEL
+    bp.gmres_recycle_reset(g)
+    _, st_reset = bp.lcp_mvp(g, T(l3), gmres=warm)
+    assert abs(st_reset.iters - st_cold.iters) <= 1   # fp64 atomics: summation order may differ
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_solve_lcp_bb_pgd(bp, c):
+    """BB-PGD (method 2) on the device MVP reaches the unique LCP solution (R30)."""
+    z = fixture(c)
+    ref = z["lam_brute"] if c == 1 else z["lam_mono"]
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    o = bp.default_solve_opts(method=2, eps_kkt_abs=1e-10, k_max=2000)
+    o.gm_hi.tol = 1e-12
+    lam, rep, rc = bp.solve_lcp(g, None, T(z["b"]), T(np.zeros(g.nc)), opts=o)
+    assert rc == 0
+    assert rel(lam.cpu().numpy(), ref) <= TOL_LAM
+    assert rep.kkt_abs <= TOL_KKT
+    assert rep.hi_mvps == rep.iterations + 1

@@ -202,3 +202,47 @@ def test_lcp_solvers_vs_brute_force(seed):
     assert r2["termination"] == pqn.TERM_KKT_ABS
     assert np.abs(x2 - ref).max() < 1e-9
     assert r2["hi_mvps"] == r2["iterations"] + 1
+
+
+# ------------------------------------------------------------------ BB-PGD (NEXT-1)
+def test_bb_step_examples():
+    """A = I -> 1; A = diag(2,1), s = (1,0) -> 0.5; random SPD -> in [1/l_max, 1/l_min]."""
+    from oracle.pqn import bb_step
+    s = np.array([0.3, -1.2])
+    assert bb_step(s, s, 7.0) == pytest.approx(1.0, abs=1e-15)
+    assert bb_step(np.array([1.0, 0.0]), np.array([2.0, 0.0]), 7.0) == pytest.approx(0.5, abs=1e-15)
+    assert bb_step(np.array([1.0, -1.0]), np.array([-1.0, 1.0]), 7.0) == 7.0   # non-positive denominator
+    rng = np.random.default_rng(4)
+    M = rng.standard_normal((6, 6))
+    A = M @ M.T + 0.1 * np.eye(6)
+    ev = np.linalg.eigvalsh(A)
+    for _ in range(20):
+        s = rng.standard_normal(6)
+        t = bb_step(s, A @ s, 0.0)
+        assert 1 / ev[-1] - 1e-12 <= t <= 1 / ev[0] + 1e-12
+
+
+def test_bb_pgd_examples():
+    """A = I, b = (-1,-1), x0 = 0 -> (1,1) in one step; A = diag(1,10), b = (-1,-10) -> (1,1)."""
+    from oracle.pqn import bb_pgd
+    x, g, rep = bb_pgd(lambda v: v, np.array([-1.0, -1.0]), np.zeros(2))
+    assert np.allclose(x, [1.0, 1.0], atol=1e-15) and rep["iterations"] == 1 and rep["mvps"] == 2
+    A = np.diag([1.0, 10.0])
+    x, g, rep = bb_pgd(lambda v: A @ v, np.array([-1.0, -10.0]), np.zeros(2), eps_abs=1e-8)
+    assert np.allclose(x, [1.0, 1.0], atol=1e-8) and rep["kkt_abs"] <= 1e-8
+    assert rep["mvps"] == rep["iterations"] + 1
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_bb_pgd_vs_brute_force(seed):
+    from oracle.lcp import brute_force_lcp
+    from oracle.pqn import bb_pgd
+    rng = np.random.default_rng(50 + seed)
+    n = 8
+    M = rng.standard_normal((n, n))
+    A = M @ M.T / n + 0.5 * np.eye(n)
+    b = rng.standard_normal(n)
+    x, g, rep = bb_pgd(lambda v: A @ v, b, np.zeros(n), eps_abs=1e-12, k_max=5000)
+    ref, cnt = brute_force_lcp(A, b)
+    assert cnt == 1 and rep["termination"] == 0
+    np.testing.assert_allclose(x, ref, atol=1e-10)
