@@ -167,6 +167,39 @@ int bpqn_lcp_b(bpqn_geom_t g, const double* fnc_dev, const double* slip_dev, dou
 int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* lambda_dev,
                    const bpqn_solve_opts* o, bpqn_report* rep, void* stream);
 
+/* Report of one DVI time step (bpqn_dvi_step). */
+typedef struct {
+  int n_contacts;           /* candidate contacts (gap < delta) at the start of the step */
+  int active_contacts;      /* lambda_l > 0 */
+  int solve_rc;             /* bpqn_solve_lcp return code (0 when there were no contacts) */
+  double min_gap_before, min_gap_after;
+  double ms_total;          /* host wall time of the step */
+  bpqn_report lcp;          /* LCP solver report (zeros when there were no contacts) */
+  bpqn_gmres_stats gm_nc, gm_c;   /* non-collisional and collisional mobility solves */
+} bpqn_step_report;
+
+/* One forward-Euler step of the collision-resolving DVI (eq. dvi; SURVEY
+ * NEXT-2) on the spheres of `hi` (and its low-fidelity twin `lo`, or NULL):
+ *   contacts (gap < delta) at the current centres;
+ *   U_nc = M_slip(F_nc, 0; u_s) with the Janus slip of the current axes (R13, B = slip_B);
+ *   b = Phi/dt + D^T U_nc;  lambda from bpqn_solve_lcp(hi, lo, b, 0, o);
+ *   U = U_nc + M D lambda;  c <- c + dt U,  a <- normalise(a + dt Omega x a)
+ *   (orientation reading R32; quaternions are out of scope);
+ * then both handles are moved to the new centres (bpqn_geometry_update).
+ * centers_host, axes_host [Np][3] in/out; fnc_host [Np][3]; uo_host [Np][6] out (U, Omega) or
+ * NULL.  Returns the solver's code; BPQN_ERR_INVALID if the step makes spheres overlap (the
+ * handles then keep the old centres; reduce dt). */
+int bpqn_dvi_step(bpqn_geom_t hi, bpqn_geom_t lo, double* centers_host, double* axes_host, const double* fnc_host,
+                  double slip_B, double dt, double delta, const bpqn_solve_opts* o, double* uo_host,
+                  bpqn_step_report* rep, void* stream);
+
+/* Move a geometry handle to new centres (same Np, p, a, mu): nodes, near incidences and
+ * correction rows are rebuilt; the grid, SH analysis, self operators and the block-Jacobi
+ * inverse are kept.  The contact set and the GMRES recycling store are cleared.
+ * BPQN_ERR_INVALID if two spheres overlap (the handle is then unusable until updated
+ * with valid centres). */
+int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream);
+
 /* Same solvers on explicit dense operators (test-only; SPEC.md worked examples):
  * A_host, Ahat_host [n][n] row-major (Ahat NULL -> Mono-PQN), b_host, x_host [n]. */
 int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, const double* b_host,

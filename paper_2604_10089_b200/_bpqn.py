@@ -47,6 +47,12 @@ class Report(ctypes.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class StepReport(ctypes.Structure):
+    _fields_ = [("n_contacts", c_int), ("active_contacts", c_int), ("solve_rc", c_int),
+                ("min_gap_before", c_double), ("min_gap_after", c_double), ("ms_total", c_double),
+                ("lcp", Report), ("gm_nc", GmresStats), ("gm_c", GmresStats)]
+
+
 SYMBOLS = {
     "bpqn_default_disc_opts": (None, [P(DiscOpts)]),
     "bpqn_default_gmres_opts": (None, [P(GmresOpts)]),
@@ -65,6 +71,9 @@ SYMBOLS = {
     "bpqn_solve_lcp_dense": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, P(SolveOpts), P(Report)]),
     "bpqn_last_error": (ctypes.c_char_p, []),
     "bpqn_gmres_recycle_reset": (c_int, [c_void_p]),
+    "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
+    "bpqn_dvi_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
+                              P(SolveOpts), c_void_p, P(StepReport), c_void_p]),
     "bpqn_profile_get": (c_int, [c_void_p, P(c_double), P(c_double), P(c_double), P(c_double), P(c_longlong),
                                  P(c_longlong)]),
     "bpqn_profile_reset": (c_int, [c_void_p, c_int]),
@@ -281,6 +290,35 @@ def solve_lcp_dense(A, b, x0=None, Ahat=None, opts=None):
     if rc not in (0, 4, 5):
         _check(rc)
     return x, rep, rc
+
+
+def geometry_update(g, centers, stream=None):
+    """Move the handle to new centres (same spheres, p); clears its contact set."""
+    import numpy as np
+    c, cp = _hptr(np.asarray(centers, dtype=np.float64).reshape(-1, 3))
+    _check(lib().bpqn_geometry_update(g.h, cp, _stream(stream)))
+    g.nc = 0
+
+
+def dvi_step(hi, lo, centers, axes, fnc, slip_B=1.0, dt=1.0, delta=0.1, opts=None, stream=None):
+    """One DVI time step (bpqn_dvi_step).  centers / axes (numpy [Np,3]) are updated in
+    place; returns ((U, Omega) [Np,6], StepReport, rc)."""
+    import numpy as np
+    assert centers.dtype == np.float64 and centers.flags.c_contiguous
+    assert axes.dtype == np.float64 and axes.flags.c_contiguous
+    f, fp = _hptr(np.asarray(fnc, dtype=np.float64).reshape(-1, 3))
+    uo = np.zeros((hi.np, 6))
+    rep = StepReport()
+    rc = lib().bpqn_dvi_step(hi.h, lo.h if lo is not None else None, centers.ctypes.data_as(c_void_p),
+                             axes.ctypes.data_as(c_void_p), fp, slip_B, dt, delta,
+                             ctypes.byref(opts) if opts is not None else None, uo.ctypes.data_as(c_void_p),
+                             ctypes.byref(rep), _stream(stream))
+    if rc not in (0, 4, 5):
+        _check(rc)
+    hi.nc = 0
+    if lo is not None:
+        lo.nc = 0
+    return uo, rep, rc
 
 
 def gmres_recycle_reset(g):

@@ -138,7 +138,7 @@ struct Geom {
 // ---------------------------------------------------------------- kernels / passes
 enum Mode { MODE_S = 0, MODE_D = 1, MODE_SD = 2 };
 
-void precompute(Geom& g, cudaStream_t st);
+void precompute(Geom& g, cudaStream_t st, bool with_self);
 void invert_in_place(double* A, int n, cudaStream_t st);  // Gauss-Jordan, partial pivoting  // self E matrices + near matrices
 
 // out = Layer(sigmaS, sigmaD) with the given self matrix (E), mode selects the kernels.

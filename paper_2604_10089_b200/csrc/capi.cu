@@ -1,6 +1,7 @@
 // C ABI of libbpqn (declarations and contracts in include/bpqn.h).
 #include <algorithm>
 #include <chrono>
+#include <limits>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -52,6 +53,71 @@ static bpqn_gmres_opts gm_or_default(const bpqn_gmres_opts* gm) {
   if (o.max_iters <= 0) o.max_iters = 1000;
   if (!(o.tol > 0)) o.tol = 1e-12;
   return o;
+}
+
+// Nodes, source records and near incidences for a set of centres (init and update):
+// validates that no two spheres overlap; incidences (target i, sphere m) with
+// |x_i - c_m| - a < d_near (R8), sorted by (i, m).
+static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
+  Geom* g = &G;
+  const double radius = g->a;
+  const int n_spheres = g->np;
+  g->centers.assign(centers_host, centers_host + 3 * (size_t)n_spheres);
+  for (int i = 0; i < n_spheres; ++i)
+    for (int j = i + 1; j < n_spheres; ++j) {
+      double dx = g->centers[3 * j] - g->centers[3 * i], dy = g->centers[3 * j + 1] - g->centers[3 * i + 1],
+             dz = g->centers[3 * j + 2] - g->centers[3 * i + 2];
+      double d = std::sqrt(dx * dx + dy * dy + dz * dz);
+      BPQN_REQUIRE(d - 2 * radius > 0, "spheres " + std::to_string(i) + " and " + std::to_string(j) + " overlap");
+    }
+  const int nq = g->nq, N = g->n;
+  std::vector<double> X(3 * (size_t)N), src(8 * (size_t)N);
+  for (int m = 0; m < g->np; ++m)
+    for (int k = 0; k < nq; ++k) {
+      size_t i = (size_t)m * nq + k;
+      for (int c = 0; c < 3; ++c) {
+        X[3 * i + c] = g->centers[3 * m + c] + radius * g->grid.xi[3 * k + c];
+        src[8 * i + c] = X[3 * i + c];
+        src[8 * i + 4 + c] = g->grid.xi[3 * k + c];
+      }
+      src[8 * i + 3] = g->grid.w[k];
+      src[8 * i + 7] = 0.0;
+    }
+  upload(g->X, X, st);
+  upload(g->src, src, st);
+  upload(g->centers_d, g->centers, st);
+  std::vector<std::pair<int, int>> inc;
+  for (int n = 0; n < g->np; ++n)
+    for (int m = 0; m < g->np; ++m) {
+      if (m == n) continue;
+      double dx = g->centers[3 * m] - g->centers[3 * n], dy = g->centers[3 * m + 1] - g->centers[3 * n + 1],
+             dz = g->centers[3 * m + 2] - g->centers[3 * n + 2];
+      if (std::sqrt(dx * dx + dy * dy + dz * dz) - 2 * radius >= g->d_near) continue;
+      for (int k = 0; k < nq; ++k) {
+        size_t i = (size_t)n * nq + k;
+        double rx = X[3 * i] - g->centers[3 * m], ry = X[3 * i + 1] - g->centers[3 * m + 1],
+               rz = X[3 * i + 2] - g->centers[3 * m + 2];
+        if (std::sqrt(rx * rx + ry * ry + rz * rz) - radius < g->d_near) inc.emplace_back((int)i, m);
+      }
+    }
+  std::sort(inc.begin(), inc.end());
+  g->n_inc = (long long)inc.size();
+  std::vector<int> it(inc.size()), im(inc.size()), ntl, ntp;
+  for (size_t k = 0; k < inc.size(); ++k) {
+    it[k] = inc[k].first;
+    im[k] = inc[k].second;
+    if (k == 0 || inc[k].first != inc[k - 1].first) {
+      ntl.push_back(inc[k].first);
+      ntp.push_back((int)k);
+    }
+  }
+  ntp.push_back((int)inc.size());
+  g->n_near_targets = (int)ntl.size();
+  upload_i(g->inc_t, it, st);
+  upload_i(g->inc_m, im, st);
+  upload_i(g->nt_list, ntl, st);
+  upload_i(g->nt_ptr, ntp, st);
+  BPQN_CUDA(cudaStreamSynchronize(st));  // host staging vectors go out of scope
 }
 
 // (U, Omega) = M_slip(ft; slip) -> uo (device); returns GMRES status
@@ -152,69 +218,14 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       g->n2 = o.near_n2 > 0 ? o.near_n2 : p + 8;
       g->nphi = o.near_nphi > 0 ? o.near_nphi : 4 * p;
       g->single_layer = o.build_single_layer != 0;
-      g->centers.assign(centers_host, centers_host + 3 * (size_t)n_spheres);
-      for (int i = 0; i < n_spheres; ++i)
-        for (int j = i + 1; j < n_spheres; ++j) {
-          double dx = g->centers[3 * j] - g->centers[3 * i], dy = g->centers[3 * j + 1] - g->centers[3 * i + 1],
-                 dz = g->centers[3 * j + 2] - g->centers[3 * i + 2];
-          double d = std::sqrt(dx * dx + dy * dy + dz * dz);
-          BPQN_REQUIRE(d - 2 * radius > 0, "spheres " + std::to_string(i) + " and " + std::to_string(j) + " overlap");
-        }
       build_grid(p, radius, g->grid);
       g->nq = g->grid.nq;
       g->n = g->np * g->nq;
       g->nb = sh_count(p);
-      const int nq = g->nq, N = g->n;
-      std::vector<double> X(3 * (size_t)N), src(8 * (size_t)N);
-      for (int m = 0; m < g->np; ++m)
-        for (int k = 0; k < nq; ++k) {
-          size_t i = (size_t)m * nq + k;
-          for (int c = 0; c < 3; ++c) {
-            X[3 * i + c] = g->centers[3 * m + c] + radius * g->grid.xi[3 * k + c];
-            src[8 * i + c] = X[3 * i + c];
-            src[8 * i + 4 + c] = g->grid.xi[3 * k + c];
-          }
-          src[8 * i + 3] = g->grid.w[k];
-          src[8 * i + 7] = 0.0;
-        }
-      upload(g->X, X, st);
-      upload(g->src, src, st);
-      upload(g->centers_d, g->centers, st);
       upload(g->xi_d, g->grid.xi, st);
       upload(g->w_d, g->grid.w, st);
-      // near incidences (target i, sphere m): |x_i - c_m| - a < d_near (R8), sorted by (i, m)
-      std::vector<std::pair<int, int>> inc;
-      for (int n = 0; n < g->np; ++n)
-        for (int m = 0; m < g->np; ++m) {
-          if (m == n) continue;
-          double dx = g->centers[3 * m] - g->centers[3 * n], dy = g->centers[3 * m + 1] - g->centers[3 * n + 1],
-                 dz = g->centers[3 * m + 2] - g->centers[3 * n + 2];
-          if (std::sqrt(dx * dx + dy * dy + dz * dz) - 2 * radius >= g->d_near) continue;
-          for (int k = 0; k < nq; ++k) {
-            size_t i = (size_t)n * nq + k;
-            double rx = X[3 * i] - g->centers[3 * m], ry = X[3 * i + 1] - g->centers[3 * m + 1],
-                   rz = X[3 * i + 2] - g->centers[3 * m + 2];
-            if (std::sqrt(rx * rx + ry * ry + rz * rz) - radius < g->d_near) inc.emplace_back((int)i, m);
-          }
-        }
-      std::sort(inc.begin(), inc.end());
-      g->n_inc = (long long)inc.size();
-      std::vector<int> it(inc.size()), im(inc.size()), ntl, ntp;
-      for (size_t k = 0; k < inc.size(); ++k) {
-        it[k] = inc[k].first;
-        im[k] = inc[k].second;
-        if (k == 0 || inc[k].first != inc[k - 1].first) {
-          ntl.push_back(inc[k].first);
-          ntp.push_back((int)k);
-        }
-      }
-      ntp.push_back((int)inc.size());
-      g->n_near_targets = (int)ntl.size();
-      upload_i(g->inc_t, it, st);
-      upload_i(g->inc_m, im, st);
-      upload_i(g->nt_list, ntl, st);
-      upload_i(g->nt_ptr, ntp, st);
-      size_t n3 = 3 * (size_t)N;
+      set_centers(*g, centers_host, st);
+      size_t n3 = 3 * (size_t)g->n;
       g->far.alloc(n3);
       g->nearout.alloc(n3);
       g->rhs.alloc(n3);
@@ -224,7 +235,7 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       g->ft.alloc(6 * (size_t)g->np);
       g->uo.alloc(6 * (size_t)g->np);
       BPQN_CUDA(cudaMallocHost(&g->host_scal, 64 * sizeof(double)));
-      precompute(*g, st);
+      precompute(*g, st, true);
     } catch (...) {
       delete g;
       throw;
@@ -237,6 +248,18 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
 int bpqn_geometry_destroy(bpqn_geom_t g) {
   return guarded([&]() -> int {
     delete g;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && centers_host, "null pointer");
+    cudaStream_t st = S(stream);
+    set_centers(*g, centers_host, st);
+    precompute(*g, st, false);  // near rows only; grid, SH analysis, self operators and inverse kept
+    g->nc = 0;
+    g->rec_k = 0;
     return BPQN_OK;
   });
 }
@@ -497,6 +520,130 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       return BPQN_ERR_NOCONV;
     }
     return BPQN_OK;
+  });
+}
+
+static double min_gap(const std::vector<double>& c, int np, double a) {
+  double m = std::numeric_limits<double>::infinity();
+  for (int i = 0; i < np; ++i)
+    for (int j = i + 1; j < np; ++j) {
+      const double dx = c[3 * j] - c[3 * i], dy = c[3 * j + 1] - c[3 * i + 1], dz = c[3 * j + 2] - c[3 * i + 2];
+      m = std::min(m, std::sqrt(dx * dx + dy * dy + dz * dz) - 2 * a);
+    }
+  return m;
+}
+
+int bpqn_dvi_step(bpqn_geom_t hi, bpqn_geom_t lo, double* centers_host, double* axes_host, const double* fnc_host,
+                  double slip_B, double dt, double delta, const bpqn_solve_opts* opts, double* uo_host,
+                  bpqn_step_report* rep, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(hi && centers_host && axes_host && fnc_host, "null pointer");
+    BPQN_REQUIRE(dt > 0, "dt must be > 0");
+    BPQN_REQUIRE(!lo || (lo->np == hi->np && lo->a == hi->a), "lo must cover the same spheres");
+    auto t0 = std::chrono::steady_clock::now();
+    cudaStream_t s = S(stream);
+    Geom& g = *hi;
+    const int np = g.np;
+    bpqn_step_report R{};
+    R.min_gap_before = min_gap(g.centers, np, g.a);
+    bpqn_solve_opts o;
+    bpqn_default_solve_opts(&o);
+    if (opts) o = *opts;
+    // contacts at the current configuration (K5), shared with the low fidelity
+    const int cap = std::max(1, np * (np - 1) / 2);
+    g.pairs.ensure(2 * (size_t)cap);
+    g.normals.ensure(3 * (size_t)cap);
+    g.gaps.ensure((size_t)cap);
+    g.nc = detect_contacts(g, delta, cap, g.pairs.p, g.normals.p, g.gaps.p, s);
+    const int nc = g.nc;
+    R.n_contacts = nc;
+    if (lo) {
+      lo->pairs.ensure(2 * (size_t)cap);
+      lo->normals.ensure(3 * (size_t)cap);
+      lo->gaps.ensure((size_t)cap);
+      if (nc > 0) {
+        BPQN_CUDA(cudaMemcpyAsync(lo->pairs.p, g.pairs.p, 2 * sizeof(int) * nc, cudaMemcpyDeviceToDevice, s));
+        BPQN_CUDA(cudaMemcpyAsync(lo->normals.p, g.normals.p, 3 * sizeof(double) * nc, cudaMemcpyDeviceToDevice, s));
+        BPQN_CUDA(cudaMemcpyAsync(lo->gaps.p, g.gaps.p, sizeof(double) * nc, cudaMemcpyDeviceToDevice, s));
+      }
+      lo->nc = nc;
+    }
+    // non-collisional mobility with the Janus slip of the current axes
+    DBuf<double> ax, slip, ft, uo_nc, uo_c, bvec, lam;
+    ax.alloc(3 * (size_t)np);
+    slip.alloc(3 * (size_t)g.n);
+    ft.alloc(6 * (size_t)np);
+    uo_nc.alloc(6 * (size_t)np);
+    uo_c.alloc(6 * (size_t)np);
+    BPQN_CUDA(cudaMemcpyAsync(ax.p, axes_host, 3 * sizeof(double) * np, cudaMemcpyHostToDevice, s));
+    launch_slip(g, ax.p, slip_B, slip.p, s);
+    std::vector<double> fth(6 * (size_t)np, 0.0);
+    for (int m = 0; m < np; ++m)
+      for (int c = 0; c < 3; ++c) fth[6 * m + c] = fnc_host[3 * m + c];
+    BPQN_CUDA(cudaMemcpyAsync(ft.p, fth.data(), 6 * sizeof(double) * np, cudaMemcpyHostToDevice, s));
+    bpqn_gmres_opts gm = gm_or_default(&o.gm_hi);
+    int rc = mobility(g, ft.p, slip.p, uo_nc.p, gm, R.gm_nc, s);
+    if (rc) return rc;
+    std::vector<double> U(6 * (size_t)np);
+    BPQN_CUDA(cudaMemcpyAsync(U.data(), uo_nc.p, 6 * sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+    BPQN_CUDA(cudaStreamSynchronize(s));
+    if (nc > 0) {
+      // b = Phi/dt + D^T U_nc ; LCP ; U_c = M D lambda
+      bvec.alloc(nc);
+      lam.alloc(nc);
+      launch_dt_gather(g, uo_nc.p, bvec.p, 1.0, nullptr, s);
+      launch_axpby(bvec.p, 1.0 / dt, g.gaps.p, 1.0, nc, s);
+      BPQN_CUDA(cudaMemsetAsync(lam.p, 0, sizeof(double) * nc, s));
+      R.solve_rc = bpqn_solve_lcp(hi, lo, bvec.p, lam.p, &o, &R.lcp, stream);
+      if (R.solve_rc != BPQN_OK && R.solve_rc != BPQN_ERR_NOCONV && R.solve_rc != BPQN_ERR_STALLED)
+        return R.solve_rc;
+      launch_d_scatter(g, lam.p, ft.p, s);
+      rc = mobility(g, ft.p, nullptr, uo_c.p, gm, R.gm_c, s);
+      if (rc) return rc;
+      std::vector<double> Uc(6 * (size_t)np), lh(nc);
+      BPQN_CUDA(cudaMemcpyAsync(Uc.data(), uo_c.p, 6 * sizeof(double) * np, cudaMemcpyDeviceToHost, s));
+      BPQN_CUDA(cudaMemcpyAsync(lh.data(), lam.p, sizeof(double) * nc, cudaMemcpyDeviceToHost, s));
+      BPQN_CUDA(cudaStreamSynchronize(s));
+      for (size_t i = 0; i < U.size(); ++i) U[i] += Uc[i];
+      for (double v : lh) R.active_contacts += v > 0.0;
+    }
+    // forward Euler on centres and Janus axes
+    std::vector<double> cn(3 * (size_t)np), an(3 * (size_t)np);
+    for (int m = 0; m < np; ++m) {
+      const double* u = &U[6 * m];
+      const double* a = &axes_host[3 * m];
+      double w[3] = {u[4] * a[2] - u[5] * a[1], u[5] * a[0] - u[3] * a[2], u[3] * a[1] - u[4] * a[0]};
+      double nrm = 0;
+      for (int c = 0; c < 3; ++c) {
+        cn[3 * m + c] = centers_host[3 * m + c] + dt * u[c];
+        an[3 * m + c] = a[c] + dt * w[c];
+        nrm += an[3 * m + c] * an[3 * m + c];
+      }
+      nrm = std::sqrt(nrm);
+      for (int c = 0; c < 3; ++c) an[3 * m + c] /= nrm;
+    }
+    R.min_gap_after = min_gap(cn, np, g.a);
+    if (!(R.min_gap_after > 0)) {
+      if (rep) *rep = R;
+      throw Error{BPQN_ERR_INVALID, "the step makes spheres overlap (min gap " + std::to_string(R.min_gap_after) +
+                                        "); reduce dt"};
+    }
+    set_centers(g, cn.data(), s);
+    precompute(g, s, false);
+    g.nc = 0;
+    g.rec_k = 0;
+    if (lo) {
+      set_centers(*lo, cn.data(), s);
+      precompute(*lo, s, false);
+      lo->nc = 0;
+      lo->rec_k = 0;
+    }
+    std::copy(cn.begin(), cn.end(), centers_host);
+    std::copy(an.begin(), an.end(), axes_host);
+    if (uo_host) std::copy(U.begin(), U.end(), uo_host);
+    R.ms_total = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (rep) *rep = R;
+    return R.solve_rc;
   });
 }
 

@@ -585,7 +585,7 @@ void invert_in_place(double* A, int n, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ driver
-void precompute(Geom& g, cudaStream_t st) {
+void precompute(Geom& g, cudaStream_t st, bool with_self) {
   const int p = g.p, nq = g.nq, nb = g.nb;
   BPQN_REQUIRE(3 * ((nb + 1) / 2) <= QT * 4, "p too large for k_quad_rows tiles (p <= 26)");
   BPQN_REQUIRE(g.nphi <= 256 && 2 * g.p_s <= 256 && g.n1 + g.n2 <= 128 && g.p_s + 1 <= 128,
@@ -600,6 +600,7 @@ void precompute(Geom& g, cudaStream_t st) {
   ShTables T{d_ra.p, d_rb.p, d_cm.p};
 
   // analysis matrix
+  if (with_self) {
   std::vector<double> wunit(nq);
   for (int i = 0; i < nq; ++i) wunit[i] = g.grid.w[i] / (g.a * g.a);
   DBuf<double> d_wunit, Yn;
@@ -609,6 +610,8 @@ void precompute(Geom& g, cudaStream_t st) {
   g.analysis.alloc((size_t)nb * nq);
   k_analysis<<<(nq + 127) / 128, 128, 0, st>>>(p, nq, g.xi_d.p, d_wunit.p, T, Yn.p, g.analysis.p, nb);
   BPQN_CHECK_LAUNCH();
+  BPQN_CUDA(cudaStreamSynchronize(st));  // d_wunit / Yn are released at the end of this scope
+  }
 
   // GL tables
   std::vector<double> t_s, w_s, t1, w1, t2, w2;
@@ -635,7 +638,8 @@ void precompute(Geom& g, cudaStream_t st) {
   size_t smem = (128 + 128 + 128 + 256 + 256 + QPC * 12 + (size_t)QPC * nb + 12 * (size_t)nb) * sizeof(double);
   BPQN_CUDA(cudaFuncSetAttribute(k_quad_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
 
-  // self rings
+  // self rings (depend on p, a, mu only: kept by bpqn_geometry_update)
+  if (with_self) {
   DBuf<double> Sring, Dring;
   Sring.alloc((size_t)(p + 1) * 9 * nq);
   Dring.alloc((size_t)(p + 1) * 9 * nq);
@@ -653,8 +657,11 @@ void precompute(Geom& g, cudaStream_t st) {
                                                              g.single_layer ? 1 : 0);
   BPQN_CHECK_LAUNCH();
   invert_in_place(g.Minv.p, 3 * nq, st);
+  }
 
   // near incidences
+  g.M_D.release();
+  g.M_S.release();
   if (g.n_inc > 0) {
     size_t per = (size_t)9 * nq;
     g.M_D.alloc((size_t)g.n_inc * per);

@@ -357,3 +357,33 @@ def test_solve_lcp_bb_pgd(bp, c):
     assert rel(lam.cpu().numpy(), ref) <= TOL_LAM
     assert rep.kkt_abs <= TOL_KKT
     assert rep.hi_mvps == rep.iterations + 1
+
+
+# ------------------------------------------------------------------ DVI time step (NEXT-2)
+def test_dvi_steps_vs_oracle(bp):
+    """Two forward-Euler DVI steps through bpqn_dvi_step -- contacts, Janus-slip
+    mobility, LCP, M D lambda, Euler update and bpqn_geometry_update -- against oracle/dvi.py."""
+    from oracle import dvi
+    C0 = np.array([[0.0, 0.0, 0.0], [2.03, 0.05, 0.0], [4.07, -0.05, 0.04]])
+    ax0 = np.array([[0.0, 0.6, 0.8], [1.0, 0.0, 0.0], [0.0, -0.8, 0.6]])
+    F = np.array([[3.0, 0.0, 0.0], [0.0, 0.0, 0.0], [-3.0, 0.0, 0.0]])
+    p, dt = 6, 0.2
+    hi = bp.Geometry(C0, p)
+    o = bp.default_solve_opts(method=0, eps_kkt_abs=1e-12)
+    o.gm_hi.tol = 1e-12
+    C, ax = C0.copy(), ax0.copy()
+    Co, axo = C0.copy(), ax0.copy()
+    active = 0
+    for step in range(2):
+        uo, rep, rc = bp.dvi_step(hi, None, C, ax, F, slip_B=1.0, dt=dt, delta=0.1, opts=o)
+        assert rc == 0
+        Cn, an, Uo, lam, pairs = dvi.dvi_step(Co, axo, F, p=p, dt=dt, slip_B=1.0)
+        assert rep.n_contacts == len(pairs)
+        assert rep.active_contacts == int((lam > 0).sum())
+        assert rel(uo, Uo) <= 1e-7
+        assert rel(C - Co, Cn - Co) <= 1e-7
+        np.testing.assert_allclose(ax, an, atol=1e-9)
+        Co, axo = Cn, an
+        active += rep.active_contacts
+    assert active > 0                      # the LCP branch is exercised (step 2 has a live contact)
+    assert rep.min_gap_after > 0
