@@ -303,11 +303,11 @@ struct K1SymParams {
 template <int MODE>
 struct TgtN { static constexpr int n = MODE == MODE_S ? 6 : (MODE == MODE_D ? 9 : 12); };
 
-template <int MODE, int R, bool SYM>
+template <int MODE, int R, bool SYM, int UNR>
 __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const double (&tg)[R][TgtN<MODE>::n],
                                          double (&acc)[R][3], int lane, double& as0, double& as1, double& as2) {
   constexpr int REC = Rec<MODE>::n;
-#pragma unroll 2
+#pragma unroll UNR
   for (int k = 0; k < 32; ++k) {
     const int j = (lane + k) & 31;
     const double2* rp = reinterpret_cast<const double2*>(gr + j * REC);
@@ -390,7 +390,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
   }
 }
 
-template <int MODE, int KS_W, int R, int MINB>
+template <int MODE, int KS_W, int R, int MINB, int UNR>
 __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   constexpr int REC = Rec<MODE>::n;
   constexpr int TN = TgtN<MODE>::n;  // per target: x and its own densities (reverse direction)
@@ -466,9 +466,9 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       const double* gr = ring[buf] + grp * 32 * REC;
       double as0 = 0.0, as1 = 0.0, as2 = 0.0;
       if (diag) {
-        k1_group<MODE, R, false>(gr, tg, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, false, UNR>(gr, tg, acc, lane, as0, as1, as2);
       } else {
-        k1_group<MODE, R, true>(gr, tg, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, true, UNR>(gr, tg, acc, lane, as0, as1, as2);
         double* rw = red[par][warp] + (grp * 32 + lane) * 3;
         rw[0] = as0;
         rw[1] = as1;
@@ -524,7 +524,7 @@ static bool k1_symmetric() {
   return v == 1;
 }
 
-template <int MODE, int W, int R, int MINB>
+template <int MODE, int W, int R, int MINB, int UNR = 2>
 static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   constexpr int KS_B = 32 * R * W;
   K1SymParams P;
@@ -538,17 +538,17 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   const int smem = (K1_STAGES * K1_TS * Rec<MODE>::n + 2 * W * K1_TS * 3) * 8;
   static int grid = 0;
   if (!grid) {
-    BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int b = 0;
-    BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB>, 32 * W, smem));
+    BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB, UNR>, 32 * W, smem));
     grid = std::max(1, b) * g.sms;
   }
   const int gr = (int)std::min<long long>(grid, P.units);
-  k1_sym<MODE, W, R, MINB><<<gr, 32 * W, smem, st>>>(P);
+  k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
 }
 
 // Launch shape per mode, measured on B200 at c4 (profiles/r01_k1_sym_shapes.md): D and S
-// are fastest with 12 warps x 3 targets/lane at 1 CTA/SM (168 regs), S+D with 8 x 3.
+// are fastest with 8 warps x 4 targets/lane at 1 CTA/SM (198 regs), S+D with 8 x 3.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -562,11 +562,16 @@ static int k1_cfg() {
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
   int c = k1_cfg();
-  if (c < 0) c = MODE == MODE_SD ? 3 : 1;
+  if (c < 0) c = MODE == MODE_SD ? 3 : 4;
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
     case 3: launch_sym_cfg<MODE, 8, 3, 1>(g, out, st); break;
+    case 4: launch_sym_cfg<MODE, 8, 4, 1>(g, out, st); break;
+    case 5: launch_sym_cfg<MODE, 12, 3, 1, 1>(g, out, st); break;
+    case 6: launch_sym_cfg<MODE, 4, 3, 3>(g, out, st); break;
+    case 7: launch_sym_cfg<MODE, 6, 3, 2>(g, out, st); break;
+    case 8: launch_sym_cfg<MODE, 12, 3, 1, 4>(g, out, st); break;
     default: launch_sym_cfg<MODE, 8, 2, 2>(g, out, st); break;
   }
 }
@@ -589,7 +594,7 @@ static void launch_asym(Geom& g, double* out, cudaStream_t st) {
 
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   const bool sym = k1_symmetric();
-  constexpr int KS_B_MAX = 9216;  // multiple of every block size used (512, 768, 1024, 1152)
+  constexpr int KS_B_MAX = 9216;  // multiple of every block size used (384 ... 1152)
   // packed records cover every target block / source tile of either variant
   const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
   g.packed.ensure((size_t)npad * 14);
