@@ -290,34 +290,80 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
 //    carries that source's accumulator, which rotates one lane per step by
 //    __shfl_sync; after 32 steps lane l holds source l's sum.  The 8 warps' sums
 //    are reduced through shared memory and added with one fp64 atomic per value.
-// launch shapes (warps per CTA W, targets per lane R, min CTAs per SM) tried on B200
-struct SymCfg { int w, r, minb; };
-
+//  * sources are points of spheres of radius a, so r.n_y = (h_m(x) - rho^2) / (2a) with
+//    h_m(x) = |x - c_m|^2 - a^2 per (target, source sphere): the forward r.n costs one FMA
+//    and the records carry no normals.  A 64-point tile spans at most two spheres
+//    (Nq >= 64 is checked), so each target keeps h for both (recomputed per tile).
 struct K1SymParams {
-  const double* pk;  // packed records [npad][REC] (targets and sources)
-  double* out;       // [N][3], zeroed, atomically accumulated
-  int N, nb, nt;     // blocks of KS_B points, tiles of K1_TS points
+  const double* pk;       // packed records [npad][RecS] (targets and sources)
+  const double* centers;  // [Np][3]
+  double* out;            // [N][3], zeroed, atomically accumulated
+  int N, nb, nt, nq, np;  // blocks of KS_B points, tiles of K1_TS points, nodes per sphere, spheres
+  double a;
   long long units;
 };
 
+// compact records of the symmetric kernel: S {y, f~}, D {y, q~}, S+D {y, f~, q~, pad}
+template <int MODE>
+struct RecS { static constexpr int n = MODE == MODE_S ? 6 : (MODE == MODE_D ? 6 : 10); };
+// per-target registers: x, own density (and own normal for the reverse stresslet)
 template <int MODE>
 struct TgtN { static constexpr int n = MODE == MODE_S ? 6 : (MODE == MODE_D ? 9 : 12); };
 
+__global__ void k1_pack_sym(int mode, int N, int npad, const double* __restrict__ src,
+                            const double* __restrict__ sigS, const double* __restrict__ sigD, double cS, double cD,
+                            double* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= npad) return;
+  const int rec = mode == MODE_SD ? 10 : 6;
+  double* o = out + (size_t)rec * j;
+  if (j >= N) {  // far away, zero strength
+    o[0] = o[1] = o[2] = 1e30;
+    for (int k = 3; k < rec; ++k) o[k] = 0.0;
+    return;
+  }
+  const double* g = src + 8 * (size_t)j;  // {y, w, n, 0}
+  const double w = g[3];
+  o[0] = g[0];
+  o[1] = g[1];
+  o[2] = g[2];
+  if (mode != MODE_D) {
+    const double c = cS * w;
+    o[3] = c * sigS[3 * (size_t)j];
+    o[4] = c * sigS[3 * (size_t)j + 1];
+    o[5] = c * sigS[3 * (size_t)j + 2];
+  }
+  if (mode != MODE_S) {
+    const double d = cD * w;
+    const int b = mode == MODE_D ? 3 : 6;
+    o[b] = d * sigD[3 * (size_t)j];
+    o[b + 1] = d * sigD[3 * (size_t)j + 1];
+    o[b + 2] = d * sigD[3 * (size_t)j + 2];
+  }
+  if (mode == MODE_SD) o[9] = 0.0;
+}
+
+// One 32-source group.  tg[r] = {x(3), [n(3)], [f~(3)], [q~(3)]} (see TgtN / k1_sym);
+// h[r][0|1] = (|x - c_m|^2 - a^2)/(2a) for the group's first / second source sphere,
+// sources with in-tile index >= jb belong to the second.
 template <int MODE, int R, bool SYM, int UNR>
 __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const double (&tg)[R][TgtN<MODE>::n],
-                                         double (&acc)[R][3], int lane, double& as0, double& as1, double& as2) {
-  constexpr int REC = Rec<MODE>::n;
+                                         const double (&h)[R][2], int jl0, int jb, double inv2a, double (&acc)[R][3],
+                                         int lane, double& as0, double& as1, double& as2) {
+  constexpr int REC = RecS<MODE>::n;
+  constexpr int QO = MODE == MODE_D ? 3 : 6;  // offset of q~ in a source record
 #pragma unroll UNR
   for (int k = 0; k < 32; ++k) {
     const int j = (lane + k) & 31;
     const double2* rp = reinterpret_cast<const double2*>(gr + j * REC);
     double sc[REC];
 #pragma unroll
-    for (int h = 0; h < REC / 2; ++h) {
-      const double2 v = rp[h];
-      sc[2 * h] = v.x;
-      sc[2 * h + 1] = v.y;
+    for (int hh = 0; hh < REC / 2; ++hh) {
+      const double2 v = rp[hh];
+      sc[2 * hh] = v.x;
+      sc[2 * hh + 1] = v.y;
     }
+    const bool second = jl0 + j >= jb;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       const double r0 = tg[r][0] - sc[0], r1 = tg[r][1] - sc[1], r2 = tg[r][2] - sc[2];
@@ -325,50 +371,54 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
       const double y = seed_or_zero(rr);
       const double y2 = y * y;
       const double e = fma(-rr, y2, 1.0);
-      if (MODE == MODE_D) {
-        const double c5 = fma(e, fma(e, 4.375, 2.5), 1.0);
-        const double y4 = y2 * y2;
-        const double s5 = (y * y4) * c5;
-        const double rn = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
-        const double rq = fma(r2, sc[8], fma(r1, sc[7], r0 * sc[6]));
-        const double tf = (rn * rq) * s5;
-        acc[r][0] = fma(r0, tf, acc[r][0]);
-        acc[r][1] = fma(r1, tf, acc[r][1]);
-        acc[r][2] = fma(r2, tf, acc[r][2]);
-        if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5
-          const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
-          const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
-          const double tb = (rn2 * rq2) * s5;
-          as0 = fma(-r0, tb, as0);
-          as1 = fma(-r1, tb, as1);
-          as2 = fma(-r2, tb, as2);
+      if (MODE == MODE_S) {
+        const double s = fma(y * e, fma(e, 0.375, 0.5), y);
+        const double s3 = (s * s) * s;
+        const double rf = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
+        const double tf = rf * s3;
+        acc[r][0] = fma(sc[3], s, fma(r0, tf, acc[r][0]));
+        acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
+        acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
+        if (SYM) {  // G(-r) = G(r)
+          const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+          const double tb = rf2 * s3;
+          as0 = fma(tg[r][3], s, fma(r0, tb, as0));
+          as1 = fma(tg[r][4], s, fma(r1, tb, as1));
+          as2 = fma(tg[r][5], s, fma(r2, tb, as2));
         }
       } else {
-        const double s = fma(y * e, fma(e, 0.375, 0.5), y);
-        const double s2 = s * s;
-        const double s3 = s2 * s;
-        if (MODE == MODE_S) {
+        const double hm = second ? h[r][1] : h[r][0];
+        const double rn = fma(rr, -inv2a, hm);  // r . n_y on the source sphere
+        const double rq = fma(r2, sc[QO + 2], fma(r1, sc[QO + 1], r0 * sc[QO]));
+        double s, s3, s5;
+        if (MODE == MODE_D) {
+          s5 = (y * (y2 * y2)) * fma(e, fma(e, 4.375, 2.5), 1.0);
+          s = s3 = 0.0;
+        } else {
+          s = fma(y * e, fma(e, 0.375, 0.5), y);
+          const double s2 = s * s;
+          s3 = s2 * s;
+          s5 = s3 * s2;
+        }
+        if (MODE == MODE_D) {
+          const double tf = (rn * rq) * s5;
+          acc[r][0] = fma(r0, tf, acc[r][0]);
+          acc[r][1] = fma(r1, tf, acc[r][1]);
+          acc[r][2] = fma(r2, tf, acc[r][2]);
+          if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5
+            const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+            const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
+            const double tb = (rn2 * rq2) * s5;
+            as0 = fma(-r0, tb, as0);
+            as1 = fma(-r1, tb, as1);
+            as2 = fma(-r2, tb, as2);
+          }
+        } else {
           const double rf = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
-          const double tf = rf * s3;
+          const double tf = fma(rf, s3, (rn * rq) * s5);
           acc[r][0] = fma(sc[3], s, fma(r0, tf, acc[r][0]));
           acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
           acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
-          if (SYM) {  // G(-r) = G(r)
-            const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
-            const double tb = rf2 * s3;
-            as0 = fma(tg[r][3], s, fma(r0, tb, as0));
-            as1 = fma(tg[r][4], s, fma(r1, tb, as1));
-            as2 = fma(tg[r][5], s, fma(r2, tb, as2));
-          }
-        } else {
-          const double s5 = s3 * s2;
-          const double rn = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
-          const double rf = fma(r2, sc[8], fma(r1, sc[7], r0 * sc[6]));
-          const double rq = fma(r2, sc[11], fma(r1, sc[10], r0 * sc[9]));
-          const double tf = fma(rf, s3, (rn * rq) * s5);
-          acc[r][0] = fma(sc[6], s, fma(r0, tf, acc[r][0]));
-          acc[r][1] = fma(sc[7], s, fma(r1, tf, acc[r][1]));
-          acc[r][2] = fma(sc[8], s, fma(r2, tf, acc[r][2]));
           if (SYM) {
             const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
             const double rf2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
@@ -392,8 +442,8 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
 
 template <int MODE, int KS_W, int R, int MINB, int UNR>
 __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
-  constexpr int REC = Rec<MODE>::n;
-  constexpr int TN = TgtN<MODE>::n;  // per target: x and its own densities (reverse direction)
+  constexpr int REC = RecS<MODE>::n;
+  constexpr int TN = TgtN<MODE>::n;
   constexpr int KS_B = 32 * R * KS_W;
   constexpr int TPB = KS_B / K1_TS;
   constexpr int TILE_DBL = K1_TS * REC;
@@ -403,12 +453,15 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   double (*ring)[TILE_DBL] = reinterpret_cast<double (*)[TILE_DBL]>(k1_dyn);            // [NS][TILE_DBL]
   double (*red)[KS_W][K1_TS * 3] =
       reinterpret_cast<double (*)[KS_W][K1_TS * 3]>(k1_dyn + NS * TILE_DBL);             // [2][W][192]
+  double* cs = k1_dyn + NS * TILE_DBL + 2 * KS_W * K1_TS * 3;                             // centres [Np][3]
   __shared__ __align__(8) uint64_t full[NS];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const long long u0 = P.units * blockIdx.x / gridDim.x;
   const long long u1 = P.units * (blockIdx.x + 1) / gridDim.x;
   if (u0 >= u1) return;
+  if (MODE != MODE_S)
+    for (int e = tid; e < 3 * P.np; e += blockDim.x) cs[e] = P.centers[e];
   // unit u0 -> (block, tile); units run block-major, tiles from the block's first tile to the end
   int b_cur = 0;
   long long base = 0;
@@ -430,9 +483,10 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       if (++pt == P.nt) pt = ++pb * TPB;
     }
   }
+  const double a = P.a, inv2a = 0.5 / P.a, inva = 1.0 / P.a;
 
-  double tg[R][TN], acc[R][3];
-  int loaded_b = -1, par = 0;
+  double tg[R][TN], acc[R][3], hs[R][2];
+  int loaded_b = -1, par = 0, h_m0 = -1, h_b = -1;
   for (long long u = u0; u < u1; ++u) {
     const int i = (int)(u - u0);
     const int buf = i % NS;
@@ -454,9 +508,40 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       for (int r = 0; r < R; ++r) {
         const int t = b_cur * KS_B + warp * 32 * R + r * 32 + lane;  // < npad
         const double* rec = P.pk + (size_t)REC * t;
+        tg[r][0] = rec[0];
+        tg[r][1] = rec[1];
+        tg[r][2] = rec[2];
+        if (MODE == MODE_S) {
+          tg[r][3] = rec[3];
+          tg[r][4] = rec[4];
+          tg[r][5] = rec[5];
+        } else {
+          // own outward normal n = (x - c_m)/a (zero for padding targets)
+          const int m = t < P.N ? t / P.nq : -1;
 #pragma unroll
-        for (int c = 0; c < TN; ++c) tg[r][c] = rec[c];
+          for (int c = 0; c < 3; ++c) tg[r][3 + c] = m >= 0 ? (rec[c] - cs[3 * m + c]) * inva : 0.0;
+#pragma unroll
+          for (int c = 3; c < REC - (MODE == MODE_SD ? 1 : 0); ++c) tg[r][3 + c] = rec[c];
+        }
         acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
+      }
+    }
+    // source spheres of this tile: first m0, second from in-tile index jb on
+    const int s0 = t_cur * K1_TS;
+    const int m0 = min(s0 / P.nq, P.np - 1);
+    const int m1 = min(m0 + 1, P.np - 1);
+    const int jb = (m0 + 1) * P.nq - s0;
+    if (MODE != MODE_S && (m0 != h_m0 || b_cur != h_b)) {  // h per (target, source sphere)
+      h_m0 = m0;
+      h_b = b_cur;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double* c = cs + 3 * (q ? m1 : m0);
+          const double d0 = tg[r][0] - c[0], d1 = tg[r][1] - c[1], d2 = tg[r][2] - c[2];
+          hs[r][q] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+        }
       }
     }
     const bool diag = t_cur < (b_cur + 1) * TPB;
@@ -466,9 +551,9 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       const double* gr = ring[buf] + grp * 32 * REC;
       double as0 = 0.0, as1 = 0.0, as2 = 0.0;
       if (diag) {
-        k1_group<MODE, R, false, UNR>(gr, tg, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, false, UNR>(gr, tg, hs, grp * 32, jb, inv2a, acc, lane, as0, as1, as2);
       } else {
-        k1_group<MODE, R, true, UNR>(gr, tg, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, acc, lane, as0, as1, as2);
         double* rw = red[par][warp] + (grp * 32 + lane) * 3;
         rw[0] = as0;
         rw[1] = as1;
@@ -529,26 +614,32 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   constexpr int KS_B = 32 * R * W;
   K1SymParams P;
   P.pk = g.packed.p;
+  P.centers = g.centers_d.p;
   P.out = out;
   P.N = g.n;
+  P.nq = g.nq;
+  P.np = g.np;
+  P.a = g.a;
   P.nb = (g.n + KS_B - 1) / KS_B;
   P.nt = P.nb * (KS_B / K1_TS);
   P.units = 0;
   for (int b = 0; b < P.nb; ++b) P.units += P.nt - b * (KS_B / K1_TS);
-  const int smem = (K1_STAGES * K1_TS * Rec<MODE>::n + 2 * W * K1_TS * 3) * 8;
-  static int grid = 0;
-  if (!grid) {
+  const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 + (MODE == MODE_S ? 0 : 3 * g.np)) * 8;
+  BPQN_REQUIRE(g.np <= 4096, "symmetric K1 stages the sphere centres in shared memory (Np <= 4096)");
+  static int grid = 0, grid_smem = -1;  // per instantiation; smem grows with Np
+  if (smem != grid_smem) {
     BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     int b = 0;
     BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB, UNR>, 32 * W, smem));
     grid = std::max(1, b) * g.sms;
+    grid_smem = smem;
   }
   const int gr = (int)std::min<long long>(grid, P.units);
   k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
 }
 
-// Launch shape per mode, measured on B200 at c4 (profiles/r01_k1_sym_shapes.md): D and S
-// are fastest with 8 warps x 4 targets/lane at 1 CTA/SM (198 regs), S+D with 8 x 3.
+// Launch shape per mode, measured on B200 at c4 (profiles/r01_k1_sym_shapes.md): D with 8
+// warps x 4 targets/lane at 1 CTA/SM, S with 12 x 3, S+D with 8 x 3.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -562,7 +653,7 @@ static int k1_cfg() {
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
   int c = k1_cfg();
-  if (c < 0) c = MODE == MODE_SD ? 3 : 4;
+  if (c < 0) c = MODE == MODE_SD ? 3 : (MODE == MODE_D ? (g.n >= 60000 ? 4 : 3) : 1);
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
@@ -598,11 +689,17 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   // packed records cover every target block / source tile of either variant
   const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
   g.packed.ensure((size_t)npad * 14);
-  k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
-                                             -3.0 / (4.0 * PI_A), g.packed.p);
+  // the symmetric kernel's tile may span at most two spheres
+  const bool use_sym = sym && g.nq >= K1_TS;
+  if (use_sym)
+    k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
+                                                   1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);
+  else
+    k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
+                                               -3.0 / (4.0 * PI_A), g.packed.p);
   BPQN_CHECK_LAUNCH();
   BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
-  if (sym) {
+  if (use_sym) {
     if (mode == MODE_D) launch_sym<MODE_D>(g, out, st);
     else if (mode == MODE_S) launch_sym<MODE_S>(g, out, st);
     else launch_sym<MODE_SD>(g, out, st);
