@@ -43,7 +43,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--gmres-tol", type=float, default=1e-8)   # paper's hi-fidelity eps_gmres (R9)
-    ap.add_argument("--gmres-restart", type=int, default=50)
+    ap.add_argument("--gmres-restart", type=int, default=100)
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--recycle", type=int, default=1)   # GMRES recycling inside the LCP solve (NEXT-3)

@@ -56,7 +56,7 @@ typedef struct {
   int build_single_layer; /* 1 (default): also precompute S-kernel near/self data */
 } bpqn_disc_opts;
 
-/* GMRES options (R9).  NULL -> tol 1e-12 (relative residual), restart 50 (<= 500),
+/* GMRES options (R9).  NULL -> tol 1e-12 (relative residual), restart 100 (<= 500),
  * max 1000, precond 1.  precond = 1: right block-Jacobi preconditioning by the exact
  * inverse of the same-sphere block (D_self - I/2 + Pi_R, identical for every sphere);
  * right preconditioning leaves the residual -- hence the stopping test -- that of

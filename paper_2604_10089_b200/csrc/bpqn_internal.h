@@ -73,7 +73,7 @@ int sh_count(int p);  // dim V_p = p^2 + 2p
 // 4 events (no host sync); bpqn_profile_get synchronises once and sums them.
 struct Profile {
   bool events = false;
-  std::vector<cudaEvent_t> pool;  // groups of 4: before K1, after K1, after K2, after K3
+  std::vector<cudaEvent_t> pool;  // groups of 5 per operator application (layer.cu)
   size_t used = 0;
   double ms_allpairs = 0, ms_near = 0, ms_self = 0;
   double allpairs_flop = 0;       // algorithmic flops of the timed K1 launches
@@ -132,6 +132,9 @@ struct Geom {
   int gm_restart = 0;
 
   Profile prof;
+  cudaStream_t side = nullptr;            // K2 overlapped with K1 (layer.cu)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  bool overlap_k2 = false;
   ~Geom();
 };
 

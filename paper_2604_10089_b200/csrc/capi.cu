@@ -19,6 +19,9 @@ Geom::~Geom() {
   if (host_scal) cudaFreeHost(host_scal);
   for (auto& e : prof.pool)
     if (e) cudaEventDestroy(e);
+  if (ev_fork) cudaEventDestroy(ev_fork);
+  if (ev_join) cudaEventDestroy(ev_join);
+  if (side) cudaStreamDestroy(side);
 }
 
 template <class F>
@@ -49,7 +52,7 @@ static bpqn_gmres_opts gm_or_default(const bpqn_gmres_opts* gm) {
   bpqn_gmres_opts o;
   bpqn_default_gmres_opts(&o);
   if (gm) o = *gm;
-  if (o.restart <= 0) o.restart = 50;
+  if (o.restart <= 0) o.restart = 100;
   if (o.max_iters <= 0) o.max_iters = 1000;
   if (!(o.tol > 0)) o.tol = 1e-12;
   return o;
@@ -164,7 +167,7 @@ void bpqn_default_disc_opts(bpqn_disc_opts* o) {
 void bpqn_default_gmres_opts(bpqn_gmres_opts* o) {
   if (!o) return;
   o->tol = 1e-12;
-  o->restart = 50;
+  o->restart = 100;
   o->max_iters = 1000;
   o->precond = 1;
   o->recycle = 0;
@@ -218,6 +221,8 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       g->n2 = o.near_n2 > 0 ? o.near_n2 : p + 8;
       g->nphi = o.near_nphi > 0 ? o.near_nphi : 4 * p;
       g->single_layer = o.build_single_layer != 0;
+      const char* ov = getenv("BPQN_OVERLAP_K2");
+      g->overlap_k2 = ov && ov[0] == '1';
       build_grid(p, radius, g->grid);
       g->nq = g->grid.nq;
       g->n = g->np * g->nq;

@@ -202,24 +202,43 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
                     double* out, cudaStream_t st) {
   int mode = (sigS && sigD) ? MODE_SD : (sigS ? MODE_S : MODE_D);
   Profile& P = g.prof;
+  // Optionally (BPQN_OVERLAP_K2=1) K2 (HBM bound) runs on a side stream concurrently
+  // with K1 (FP64 bound).  Measured on B200 at c4: no gain -- K1 slows by K2's whole
+  // duration -- so K2 runs in order by default.
+  if (!g.side) {
+    BPQN_CUDA(cudaStreamCreateWithFlags(&g.side, cudaStreamNonBlocking));
+    BPQN_CUDA(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
+    BPQN_CUDA(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
+  }
+  const bool overlap = g.overlap_k2;
+  cudaStream_t sk2 = overlap ? g.side : st;
   cudaEvent_t* ev = nullptr;
   if (P.events) {
-    while (P.pool.size() < P.used + 4) {
+    while (P.pool.size() < P.used + 5) {
       cudaEvent_t e;
       BPQN_CUDA(cudaEventCreate(&e));
       P.pool.push_back(e);
     }
     ev = P.pool.data() + P.used;
-    P.used += 4;
-    BPQN_CUDA(cudaEventRecord(ev[0], st));
+    P.used += 5;
   }
+  if (overlap) {
+    BPQN_CUDA(cudaEventRecord(g.ev_fork, st));
+    BPQN_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
+  }
+  if (ev) BPQN_CUDA(cudaEventRecord(ev[2], sk2));
+  launch_near(g, sigS, sigD, g.nearout.p, sk2);
+  if (ev) BPQN_CUDA(cudaEventRecord(ev[3], sk2));
+  if (ev) BPQN_CUDA(cudaEventRecord(ev[0], st));
   launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
   if (ev) {
     BPQN_CUDA(cudaEventRecord(ev[1], st));
     P.allpairs_flop += (double)g.n * (double)g.n * allpairs_flops_per_pair(mode);
   }
-  launch_near(g, sigS, sigD, g.nearout.p, st);
-  if (ev) BPQN_CUDA(cudaEventRecord(ev[2], st));
+  if (overlap) {
+    BPQN_CUDA(cudaEventRecord(g.ev_join, g.side));
+    BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
+  }
   if (sigS && sigD) {
     launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st);
     launch_self_gemm(g, Ed, sigD, nullptr, nullptr, out, 1, st);
@@ -228,19 +247,22 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   } else {
     launch_self_gemm(g, Ed, sigD, g.far.p, g.nearout.p, out, 0, st);
   }
-  if (ev) BPQN_CUDA(cudaEventRecord(ev[3], st));
+  if (ev) BPQN_CUDA(cudaEventRecord(ev[4], st));
 }
 
 // Sum the recorded operator timings (one host sync) and recycle the events.
+// Per application: [2]/[3] around K2 (side stream when overlapped), [0]/[1] around K1,
+// [4] main after K3.  ms_self = [1] -> [4] (K3, plus any
+// wait for an overlapped K2 that outlasted K1).
 void profile_collect(Geom& g) {
   Profile& P = g.prof;
   if (P.used == 0) return;
   BPQN_CUDA(cudaEventSynchronize(P.pool[P.used - 1]));
-  for (size_t k = 0; k < P.used; k += 4) {
+  for (size_t k = 0; k < P.used; k += 5) {
     float a = 0, b = 0, c = 0;
     BPQN_CUDA(cudaEventElapsedTime(&a, P.pool[k], P.pool[k + 1]));
-    BPQN_CUDA(cudaEventElapsedTime(&b, P.pool[k + 1], P.pool[k + 2]));
-    BPQN_CUDA(cudaEventElapsedTime(&c, P.pool[k + 2], P.pool[k + 3]));
+    BPQN_CUDA(cudaEventElapsedTime(&b, P.pool[k + 2], P.pool[k + 3]));
+    BPQN_CUDA(cudaEventElapsedTime(&c, P.pool[k + 1], P.pool[k + 4]));
     P.ms_allpairs += a;
     P.ms_near += b;
     P.ms_self += c;
