@@ -306,9 +306,10 @@ struct K1SymParams {
 // compact records of the symmetric kernel: S {y, f~}, D {y, q~}, S+D {y, f~, q~, pad}
 template <int MODE>
 struct RecS { static constexpr int n = MODE == MODE_S ? 6 : (MODE == MODE_D ? 6 : 10); };
-// per-target registers: x, own density (and own normal for the reverse stresslet)
+// per-target registers: x and its own density (the record without padding); the reverse
+// stresslet's r.n_t comes from the sphere identity via H (see k1_sym)
 template <int MODE>
-struct TgtN { static constexpr int n = MODE == MODE_S ? 6 : (MODE == MODE_D ? 9 : 12); };
+struct TgtN { static constexpr int n = MODE == MODE_SD ? 9 : 6; };
 
 __global__ void k1_pack_sym(int mode, int N, int npad, const double* __restrict__ src,
                             const double* __restrict__ sigS, const double* __restrict__ sigD, double cS, double cD,
@@ -343,12 +344,14 @@ __global__ void k1_pack_sym(int mode, int N, int npad, const double* __restrict_
   if (mode == MODE_SD) o[9] = 0.0;
 }
 
-// One 32-source group.  tg[r] = {x(3), [n(3)], [f~(3)], [q~(3)]} (see TgtN / k1_sym);
+// One 32-source group.  tg[r] = {x(3), [f~(3)], [q~(3)]} (see TgtN / k1_sym);
 // h[r][0|1] = (|x - c_m|^2 - a^2)/(2a) for the group's first / second source sphere,
-// sources with in-tile index >= jb belong to the second.
+// sources with in-tile index >= jb belong to the second; Hg[slot * K1_TS + j] =
+// (|y_j - c_t|^2 - a^2)/(2a) for the block's target spheres (reverse r.n_t).
 template <int MODE, int R, bool SYM, int UNR>
 __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const double (&tg)[R][TgtN<MODE>::n],
-                                         const double (&h)[R][2], int jl0, int jb, double inv2a, double (&acc)[R][3],
+                                         const double (&h)[R][2], int jl0, int jb, double inv2a,
+                                         const double* __restrict__ Hg, const int (&slot)[R], double (&acc)[R][3],
                                          int lane, double& as0, double& as1, double& as2) {
   constexpr int REC = RecS<MODE>::n;
   constexpr int QO = MODE == MODE_D ? 3 : 6;  // offset of q~ in a source record
@@ -405,9 +408,9 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           acc[r][0] = fma(r0, tf, acc[r][0]);
           acc[r][1] = fma(r1, tf, acc[r][1]);
           acc[r][2] = fma(r2, tf, acc[r][2]);
-          if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5
-            const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
-            const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
+          if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5, r.n_i = (rho^2 - H)/(2a)
+            const double rn2 = fma(rr, inv2a, -Hg[slot[r] * K1_TS + jl0 + j]);
+            const double rq2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
             const double tb = (rn2 * rq2) * s5;
             as0 = fma(-r0, tb, as0);
             as1 = fma(-r1, tb, as1);
@@ -420,13 +423,13 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
           acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
           if (SYM) {
-            const double rn2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
-            const double rf2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
-            const double rq2 = fma(r2, tg[r][11], fma(r1, tg[r][10], r0 * tg[r][9]));
+            const double rn2 = fma(rr, inv2a, -Hg[slot[r] * K1_TS + jl0 + j]);
+            const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+            const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
             const double tb = fma(rf2, s3, -((rn2 * rq2) * s5));
-            as0 = fma(tg[r][6], s, fma(r0, tb, as0));
-            as1 = fma(tg[r][7], s, fma(r1, tb, as1));
-            as2 = fma(tg[r][8], s, fma(r2, tb, as2));
+            as0 = fma(tg[r][3], s, fma(r0, tb, as0));
+            as1 = fma(tg[r][4], s, fma(r1, tb, as1));
+            as2 = fma(tg[r][5], s, fma(r2, tb, as2));
           }
         }
       }
@@ -454,6 +457,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   double (*red)[KS_W][K1_TS * 3] =
       reinterpret_cast<double (*)[KS_W][K1_TS * 3]>(k1_dyn + NS * TILE_DBL);             // [2][W][192]
   double* cs = k1_dyn + NS * TILE_DBL + 2 * KS_W * K1_TS * 3;                             // centres [Np][3]
+  double* Hs = cs + (MODE == MODE_S ? 0 : 3 * P.np);                                      // [slots][K1_TS]
   __shared__ __align__(8) uint64_t full[NS];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -483,10 +487,11 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       if (++pt == P.nt) pt = ++pb * TPB;
     }
   }
-  const double a = P.a, inv2a = 0.5 / P.a, inva = 1.0 / P.a;
+  const double a = P.a, inv2a = 0.5 / P.a;
 
   double tg[R][TN], acc[R][3], hs[R][2];
-  int loaded_b = -1, par = 0, h_m0 = -1, h_b = -1;
+  int slot[R];
+  int loaded_b = -1, par = 0, h_m0 = -1, h_b = -1, fs = 0, nslot = 0;
   for (long long u = u0; u < u1; ++u) {
     const int i = (int)(u - u0);
     const int buf = i % NS;
@@ -504,25 +509,15 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
         }
       }
       loaded_b = b_cur;
+      fs = min(b_cur * KS_B / P.nq, P.np - 1);  // target spheres of the block: fs .. fs + nslot - 1
+      nslot = min((b_cur * KS_B + KS_B - 1) / P.nq, P.np - 1) - fs + 1;
 #pragma unroll
       for (int r = 0; r < R; ++r) {
         const int t = b_cur * KS_B + warp * 32 * R + r * 32 + lane;  // < npad
         const double* rec = P.pk + (size_t)REC * t;
-        tg[r][0] = rec[0];
-        tg[r][1] = rec[1];
-        tg[r][2] = rec[2];
-        if (MODE == MODE_S) {
-          tg[r][3] = rec[3];
-          tg[r][4] = rec[4];
-          tg[r][5] = rec[5];
-        } else {
-          // own outward normal n = (x - c_m)/a (zero for padding targets)
-          const int m = t < P.N ? t / P.nq : -1;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) tg[r][3 + c] = m >= 0 ? (rec[c] - cs[3 * m + c]) * inva : 0.0;
-#pragma unroll
-          for (int c = 3; c < REC - (MODE == MODE_SD ? 1 : 0); ++c) tg[r][3 + c] = rec[c];
-        }
+        for (int c = 0; c < TN; ++c) tg[r][c] = rec[c];
+        slot[r] = min(t / P.nq, P.np - 1) - fs;
         acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
       }
     }
@@ -546,14 +541,24 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     }
     const bool diag = t_cur < (b_cur + 1) * TPB;
     mbar_wait(&full[buf], parity);
+    if (MODE != MODE_S && !diag) {  // H[slot][j] = (|y_j - c_slot|^2 - a^2)/(2a) for this tile
+      for (int e = tid; e < nslot * K1_TS; e += blockDim.x) {
+        const int sl = e / K1_TS, j = e - sl * K1_TS;
+        const double* y = ring[buf] + j * REC;
+        const double* c = cs + 3 * (fs + sl);
+        const double d0 = y[0] - c[0], d1 = y[1] - c[1], d2 = y[2] - c[2];
+        Hs[e] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+      }
+      __syncthreads();
+    }
 #pragma unroll 1
     for (int grp = 0; grp < K1_TS / 32; ++grp) {
       const double* gr = ring[buf] + grp * 32 * REC;
       double as0 = 0.0, as1 = 0.0, as2 = 0.0;
       if (diag) {
-        k1_group<MODE, R, false, UNR>(gr, tg, hs, grp * 32, jb, inv2a, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, false, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
       } else {
-        k1_group<MODE, R, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
         double* rw = red[par][warp] + (grp * 32 + lane) * 3;
         rw[0] = as0;
         rw[1] = as1;
@@ -624,7 +629,9 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   P.nt = P.nb * (KS_B / K1_TS);
   P.units = 0;
   for (int b = 0; b < P.nb; ++b) P.units += P.nt - b * (KS_B / K1_TS);
-  const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 + (MODE == MODE_S ? 0 : 3 * g.np)) * 8;
+  const int nslot_max = KS_B / g.nq + 2;
+  const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
+                    (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * K1_TS)) * 8;
   BPQN_REQUIRE(g.np <= 4096, "symmetric K1 stages the sphere centres in shared memory (Np <= 4096)");
   static int grid = 0, grid_smem = -1;  // per instantiation; smem grows with Np
   if (smem != grid_smem) {
