@@ -670,6 +670,9 @@ static void launch_sym(Geom& g, double* out, cudaStream_t st) {
     case 6: launch_sym_cfg<MODE, 4, 3, 3>(g, out, st); break;
     case 7: launch_sym_cfg<MODE, 6, 3, 2>(g, out, st); break;
     case 8: launch_sym_cfg<MODE, 12, 3, 1, 4>(g, out, st); break;
+    case 9: launch_sym_cfg<MODE, 8, 3, 2>(g, out, st); break;
+    case 10: launch_sym_cfg<MODE, 8, 4, 1, 1>(g, out, st); break;
+    case 11: launch_sym_cfg<MODE, 4, 4, 2>(g, out, st); break;
     default: launch_sym_cfg<MODE, 8, 2, 2>(g, out, st); break;
   }
 }
