@@ -19,9 +19,10 @@ ap.add_argument("--config", type=int, default=4)
 ap.add_argument("--mode", default="d")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--save", default="")
+ap.add_argument("--p", type=int, default=0)
 a = ap.parse_args()
 cfg = make_config(a.config)
-g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+g = bp.Geometry(cfg["centers"], a.p or cfg["p"], cfg["radius"], cfg["mu"])
 f, q = layer_densities(a.config, g.N)
 f = torch.tensor(f, device="cuda") if "s" in a.mode else None
 q = torch.tensor(q, device="cuda") if "d" in a.mode else None
