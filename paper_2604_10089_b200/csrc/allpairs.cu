@@ -632,7 +632,6 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   const int nslot_max = KS_B / g.nq + 2;
   const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
                     (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * K1_TS)) * 8;
-  BPQN_REQUIRE(g.np <= 4096, "symmetric K1 stages the sphere centres in shared memory (Np <= 4096)");
   static int grid = 0, grid_smem = -1;  // per instantiation; smem grows with Np
   if (smem != grid_smem) {
     BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -699,8 +698,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   // packed records cover every target block / source tile of either variant
   const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
   g.packed.ensure((size_t)npad * 14);
-  // the symmetric kernel's tile may span at most two spheres
-  const bool use_sym = sym && g.nq >= K1_TS;
+  const bool use_sym = sym && g.nq >= K1_TS && g.np <= 4096;  // tile spans <= 2 spheres; centres fit smem
   if (use_sym)
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
                                                    1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);
