@@ -9,6 +9,9 @@
 // Runs on the host (OpenMP for the O(Nc r^2) and O(r^3) prox pieces): one Nc-vector
 // crosses PCIe per MVP.  C^{-1} = (D + UU^T)^{-1} is applied by the Woodbury identity.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <functional>
 #include <limits>
@@ -210,9 +213,26 @@ static bool lu_solve_par(std::vector<double>& A, int n, Vec& b) {
 // residual with the "+[alpha; alpha~]" term restored (R15).  C^{-1} V by Woodbury
 // with one Cholesky factor of I + U^T U; the Jacobian blocks of P:709-712 as
 // products over the active / inactive coordinates.
+struct ProxTimers {
+  double setup = 0, jac = 0, lu = 0, resid = 0;
+  long calls = 0, newton = 0, rsum = 0;
+  ~ProxTimers() {
+    if (getenv("BPQN_PQN_PROFILE"))
+      fprintf(stderr, "prox: calls %ld newton %ld avg r %.1f | setup %.3fs jac %.3fs lu %.3fs resid %.3fs\n", calls,
+              newton, calls ? (double)rsum / calls : 0.0, setup, jac, lu, resid);
+  }
+};
+static ProxTimers g_pt;
+static double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters) {
   const int n = (int)xt.size();
   const int r = (int)q.U.size();
+  g_pt.calls++;
+  g_pt.rsum += r;
+  double t_0 = now_s();
   if (r == 0) {
     Vec z(n);
     for (int i = 0; i < n; ++i) z[i] = std::max(xt[i], 0.0);
@@ -248,6 +268,7 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     }
   }
   const int d = 2 * r;
+  g_pt.setup += now_s() - t_0;
   Vec al(d, 0.0);  // [alpha; alpha~]
   auto residual = [&](const Vec& a, Vec& L, Vec& z, std::vector<char>& act) {
     Vec y = xt, v(n);
@@ -294,6 +315,8 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
   int j = 0;
   std::vector<double> Ua, Va, CVa, Ui, CVi, blk((size_t)r * r);
   for (j = 0; j < jmax && nr > tol; ++j) {
+    g_pt.newton++;
+    double t_1 = now_s();
     // J = [[U^T Lam U, U^T (I-Lam) CV], [V^T Lam U, -V^T Lam CV]] + I
     std::vector<int> ia, ii;
     for (int e = 0; e < n; ++e) (act[e] ? ia : ii).push_back(e);
@@ -328,9 +351,14 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     gemm_nt(Va.data(), CVa.data(), blk.data(), r, r, na, false);
     put(r, r, -1.0);
     for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1.0;
+    double t_2 = now_s();
+    g_pt.jac += t_2 - t_1;
     Vec step = L;
     std::vector<double> Jc = J;
-    if (!lu_solve_par(Jc, d, step)) {
+    const bool lu_ok = lu_solve_par(Jc, d, step);
+    g_pt.lu += now_s() - t_2;
+    t_2 = now_s();
+    if (!lu_ok) {
       double jn = 0;
       for (double v : J) jn = std::max(jn, std::fabs(v));
       for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1e-10 * jn * d;
@@ -354,6 +382,7 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     }
     if (!ok) break;
     double smax = t * infn(step);
+    g_pt.resid += now_s() - t_2;
     al = a2;
     L = L2;
     z = z2;
