@@ -387,3 +387,17 @@ def test_dvi_steps_vs_oracle(bp):
         active += rep.active_contacts
     assert active > 0                      # the LCP branch is exercised (step 2 has a live contact)
     assert rep.min_gap_after > 0
+
+
+def test_gmres_not_converged_reported(bp):
+    """max_iters reached before the tolerance -> BPQN_ERR_NOCONV (4), with the iterate and the
+    achieved residual still returned through the stats (bpqn.h conventions)."""
+    z = fixture(1)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    from synth import lambda_test
+    with pytest.raises(bp.BpqnError) as e:
+        bp.lcp_mvp(g, T(lambda_test(1, g.nc, 0)), gmres=bp.default_gmres_opts(tol=1e-14, max_iters=5))
+    assert e.value.code == 4
+    _, st = bp.mobility_apply(g, T(z["FT_test"]), gmres=bp.default_gmres_opts(tol=1e-6))
+    assert 1 <= st.iters < 60 and st.rel_resid <= 1e-6 and st.applies >= st.iters
