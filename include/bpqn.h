@@ -205,6 +205,19 @@ int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream
 int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, const double* b_host,
                          double* x_host, const bpqn_solve_opts* o, bpqn_report* rep);
 
+/* Multi-GPU (one process per GPU): shard the target side of the layer
+ * operator.  Rank r of `world` owns spheres [Np r/world, Np (r+1)/world); every operator
+ * application computes only the owned rows (K1 targets x all sources, K2 and K3 for the
+ * owned spheres), copies them into send_dev (rows = ceil(Np/world) * Nq nodes, [rows][3],
+ * zero-padded) and calls allgather(user) once the handle's stream has been synchronised;
+ * the callback must fill recv_dev ([world][rows][3], rank-major -- e.g. NCCL
+ * all_gather_into_tensor) and return 0.  Everything else (GMRES, contacts, D, PQN) runs
+ * replicated on full vectors, deterministically, so all ranks take the same decisions.
+ * send_dev / recv_dev / user stay owned by the caller and must outlive the sharding.
+ * world = 1 restores the single-GPU operator (symmetric K1). */
+int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, double* recv_dev,
+                        int (*allgather)(void* user), void* user);
+
 /* Empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
 int bpqn_gmres_recycle_reset(bpqn_geom_t g);
 

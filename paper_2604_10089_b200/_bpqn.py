@@ -53,6 +53,8 @@ class StepReport(ctypes.Structure):
                 ("lcp", Report), ("gm_nc", GmresStats), ("gm_c", GmresStats)]
 
 
+ALLGATHER_FN = ctypes.CFUNCTYPE(c_int, c_void_p)
+
 SYMBOLS = {
     "bpqn_default_disc_opts": (None, [P(DiscOpts)]),
     "bpqn_default_gmres_opts": (None, [P(GmresOpts)]),
@@ -71,6 +73,7 @@ SYMBOLS = {
     "bpqn_solve_lcp_dense": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, P(SolveOpts), P(Report)]),
     "bpqn_last_error": (ctypes.c_char_p, []),
     "bpqn_gmres_recycle_reset": (c_int, [c_void_p]),
+    "bpqn_geometry_shard": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
     "bpqn_dvi_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                               P(SolveOpts), c_void_p, P(StepReport), c_void_p]),
@@ -319,6 +322,48 @@ def dvi_step(hi, lo, centers, axes, fnc, slip_B=1.0, dt=1.0, delta=0.1, opts=Non
     if lo is not None:
         lo.nc = 0
     return uo, rep, rc
+
+
+def _torch_allgather(send, recv):
+    """all-gather of equal-size device buffers with torch.distributed (NCCL directly; other
+    backends, e.g. gloo in tests, through host copies)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.all_gather_into_tensor(recv, send)
+    else:
+        parts = [torch.empty(send.numel(), dtype=send.dtype) for _ in range(dist.get_world_size())]
+        dist.all_gather(parts, send.cpu())
+        recv.copy_(torch.cat(parts).to(recv.device))
+    torch.cuda.current_stream().synchronize()
+
+
+def geometry_shard(g, rank, world, allgather=None):
+    """Shard the layer operator's target side over `world` ranks (bpqn_geometry_shard);
+    `allgather(send, recv)` performs the collective on the two CUDA tensors (default:
+    torch.distributed).  world = 1 restores the single-GPU operator."""
+    import torch
+    if world == 1:
+        _check(lib().bpqn_geometry_shard(g.h, 0, 1, None, None, ALLGATHER_FN(0), None))
+        g._shard = None
+        return
+    rows = -(-g.np // world) * g.nq
+    send = torch.zeros(3 * rows, dtype=torch.float64, device="cuda")
+    recv = torch.zeros(world * 3 * rows, dtype=torch.float64, device="cuda")
+    fn = allgather or _torch_allgather
+
+    def cb(_user):
+        try:
+            fn(send, recv)
+            return 0
+        except Exception:  # reported as BPQN_ERR_CUDA by the library
+            import traceback
+            traceback.print_exc()
+            return 1
+
+    cfun = ALLGATHER_FN(cb)
+    g._shard = (send, recv, cfun)  # keep alive as long as the sharding
+    _check(lib().bpqn_geometry_shard(g.h, rank, world, _ptr(send), _ptr(recv), cfun, None))
 
 
 def gmres_recycle_reset(g):

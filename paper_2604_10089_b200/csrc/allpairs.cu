@@ -137,10 +137,10 @@ __device__ __forceinline__ double seed_or_zero(double rr) {
 }
 
 struct K1Params {
-  const double* X;     // [N][3] targets
+  const double* X;     // [N][3] node positions (targets t0 .. t0 + nt - 1)
   const double* pk;    // packed sources [npad][REC]
-  double* out;         // [N][3], zeroed, atomically accumulated
-  int N, n_tb, n_st;
+  double* out;         // [N][3], zeroed, atomically accumulated (target rows only)
+  int t0, nt, n_tb, n_st;
   long long units;     // n_tb * n_st
 };
 
@@ -183,8 +183,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
       if (cur_tb >= 0) {
 #pragma unroll
         for (int r = 0; r < K1_R; ++r) {
-          const int t = cur_tb * K1_TB + r * K1_THREADS + tid;
-          if (t < P.N) {
+          const int tl = cur_tb * K1_TB + r * K1_THREADS + tid;
+          const int t = P.t0 + tl;
+          if (tl < P.nt) {
             atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
             atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
             atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
@@ -194,8 +195,8 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
       cur_tb = tb;
 #pragma unroll
       for (int r = 0; r < K1_R; ++r) {
-        int t = tb * K1_TB + r * K1_THREADS + tid;
-        t = t < P.N ? t : P.N - 1;
+        int tl = tb * K1_TB + r * K1_THREADS + tid;
+        const int t = P.t0 + (tl < P.nt ? tl : P.nt - 1);
         x[r][0] = P.X[3 * (size_t)t];
         x[r][1] = P.X[3 * (size_t)t + 1];
         x[r][2] = P.X[3 * (size_t)t + 2];
@@ -267,8 +268,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
   }
 #pragma unroll
   for (int r = 0; r < K1_R; ++r) {
-    const int t = cur_tb * K1_TB + r * K1_THREADS + tid;
-    if (t < P.N) {
+    const int tl = cur_tb * K1_TB + r * K1_THREADS + tid;
+    const int t = P.t0 + tl;
+    if (tl < P.nt) {
       atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
       atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
       atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
@@ -677,10 +679,11 @@ static void launch_sym(Geom& g, double* out, cudaStream_t st) {
 }
 
 template <int MODE>
-static void launch_asym(Geom& g, double* out, cudaStream_t st) {
+static void launch_asym(Geom& g, double* out, cudaStream_t st, int t0, int t1) {
   K1Params P;
-  P.N = g.n;
-  P.n_tb = (g.n + K1_TB - 1) / K1_TB;
+  P.t0 = t0;
+  P.nt = t1 - t0;
+  P.n_tb = (P.nt + K1_TB - 1) / K1_TB;
   P.n_st = (g.n + K1_TS - 1) / K1_TS;
   P.units = (long long)P.n_tb * P.n_st;
   P.X = g.X.p;
@@ -698,7 +701,8 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   // packed records cover every target block / source tile of either variant
   const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
   g.packed.ensure((size_t)npad * 14);
-  const bool use_sym = sym && g.nq >= K1_TS && g.np <= 4096;  // tile spans <= 2 spheres; centres fit smem
+  // symmetric kernel: tile spans <= 2 spheres, centres fit smem, all targets on this GPU
+  const bool use_sym = sym && g.nq >= K1_TS && g.np <= 4096 && g.shard_world == 1;
   if (use_sym)
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
                                                    1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);
@@ -712,9 +716,11 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
     else if (mode == MODE_S) launch_sym<MODE_S>(g, out, st);
     else launch_sym<MODE_SD>(g, out, st);
   } else {
-    if (mode == MODE_D) launch_asym<MODE_D>(g, out, st);
-    else if (mode == MODE_S) launch_asym<MODE_S>(g, out, st);
-    else launch_asym<MODE_SD>(g, out, st);
+    // sharded (bpqn_geometry_shard): this rank's target rows against all sources
+    const int t0 = g.shard_world > 1 ? g.sh_t0 : 0, t1 = g.shard_world > 1 ? g.sh_t1 : g.n;
+    if (mode == MODE_D) launch_asym<MODE_D>(g, out, st, t0, t1);
+    else if (mode == MODE_S) launch_asym<MODE_S>(g, out, st, t0, t1);
+    else launch_asym<MODE_SD>(g, out, st, t0, t1);
   }
   BPQN_CHECK_LAUNCH();
   g.prof.allpairs_launches++;

@@ -135,6 +135,16 @@ struct Geom {
   cudaStream_t side = nullptr;            // K2 overlapped with K1 (layer.cu)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool overlap_k2 = false;
+  // target-side sharding over ranks (bpqn_geometry_shard, NEXT-4): this rank owns spheres
+  // [sh_s0, sh_s1) = nodes [sh_t0, sh_t1) and near-target list entries [sh_k0, sh_k1);
+  // after each operator application the owned rows go through sh_fn (an all-gather of
+  // sh_rows * 3 doubles per rank from sh_send into sh_recv, user-owned device buffers).
+  int shard_rank = 0, shard_world = 1;
+  int sh_s0 = 0, sh_s1 = 0, sh_t0 = 0, sh_t1 = 0, sh_k0 = 0, sh_k1 = 0, sh_rows = 0;
+  double *sh_send = nullptr, *sh_recv = nullptr;
+  int (*sh_fn)(void* user) = nullptr;
+  void* sh_user = nullptr;
+  std::vector<int> nt_list_h;  // host copy of the near-target list (shard ranges)
   ~Geom();
 };
 
@@ -154,7 +164,7 @@ void profile_collect(Geom& g);
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st);
 void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st);
 void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
-                      double* out, int accumulate, cudaStream_t st);
+                      double* out, int accumulate, cudaStream_t st, int s0 = 0, int s1 = -1);
 
 // GMRES on A_op q = rhs (A_op = E_A + coarse + near); returns stats.
 int gmres_solve(Geom& g, const double* rhs, double* x, const bpqn_gmres_opts& o, bpqn_gmres_stats& st,

@@ -58,6 +58,18 @@ static bpqn_gmres_opts gm_or_default(const bpqn_gmres_opts* gm) {
   return o;
 }
 
+// Owned spheres / nodes / near-target entries of this rank (bpqn_geometry_shard).
+static void shard_ranges(Geom& g) {
+  if (g.shard_world <= 1) return;
+  g.sh_s0 = (int)((long long)g.np * g.shard_rank / g.shard_world);
+  g.sh_s1 = (int)((long long)g.np * (g.shard_rank + 1) / g.shard_world);
+  g.sh_t0 = g.sh_s0 * g.nq;
+  g.sh_t1 = g.sh_s1 * g.nq;
+  g.sh_rows = (int)((g.np + g.shard_world - 1) / g.shard_world) * g.nq;
+  g.sh_k0 = (int)(std::lower_bound(g.nt_list_h.begin(), g.nt_list_h.end(), g.sh_t0) - g.nt_list_h.begin());
+  g.sh_k1 = (int)(std::lower_bound(g.nt_list_h.begin(), g.nt_list_h.end(), g.sh_t1) - g.nt_list_h.begin());
+}
+
 // Nodes, source records and near incidences for a set of centres (init and update):
 // validates that no two spheres overlap; incidences (target i, sphere m) with
 // |x_i - c_m| - a < d_near (R8), sorted by (i, m).
@@ -116,6 +128,8 @@ static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
   }
   ntp.push_back((int)inc.size());
   g->n_near_targets = (int)ntl.size();
+  g->nt_list_h = ntl;
+  shard_ranges(*g);
   upload_i(g->inc_t, it, st);
   upload_i(g->inc_m, im, st);
   upload_i(g->nt_list, ntl, st);
@@ -265,6 +279,29 @@ int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream
     precompute(*g, st, false);  // near rows only; grid, SH analysis, self operators and inverse kept
     g->nc = 0;
     g->rec_k = 0;
+    return BPQN_OK;
+  });
+}
+
+int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, double* recv_dev,
+                        int (*allgather)(void* user), void* user) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    BPQN_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+    if (world == 1) {
+      g->shard_world = 1;
+      g->shard_rank = 0;
+      return BPQN_OK;
+    }
+    BPQN_REQUIRE(world <= g->np, "more ranks than spheres");
+    BPQN_REQUIRE(send_dev && recv_dev && allgather, "null buffer or callback");
+    g->shard_rank = rank;
+    g->shard_world = world;
+    g->sh_send = send_dev;
+    g->sh_recv = recv_dev;
+    g->sh_fn = allgather;
+    g->sh_user = user;
+    shard_ranges(*g);
     return BPQN_OK;
   });
 }

@@ -69,10 +69,13 @@ void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, c
   if (g.n_near_targets == 0) return;
   const double* MS = (sigS && g.M_S.p) ? g.M_S.p : nullptr;
   const double* MD = sigD ? g.M_D.p : nullptr;
-  int warps = 3 * g.n_near_targets;
+  // sharded: only this rank's near targets (the list is sorted by target node)
+  const int k0 = g.shard_world > 1 ? g.sh_k0 : 0, k1 = g.shard_world > 1 ? g.sh_k1 : g.n_near_targets;
+  if (k1 <= k0) return;
+  int warps = 3 * (k1 - k0);
   int threads = 256;
   int blocks = (warps * 32 + threads - 1) / threads;
-  k2_near<<<blocks, threads, 0, st>>>(g.n_near_targets, g.nt_list.p, g.nt_ptr.p, g.inc_m.p, g.nq, MS, sigS, MD,
+  k2_near<<<blocks, threads, 0, st>>>(k1 - k0, g.nt_list.p + k0, g.nt_ptr.p + k0, g.inc_m.p, g.nq, MS, sigS, MD,
                                       sigD, out);
   BPQN_CHECK_LAUNCH();
   g.prof.launches++;
@@ -173,14 +176,24 @@ __global__ void __launch_bounds__(256) k3_self_gemm(int M, int Nn, int kchunk, c
 }
 
 void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
-                      double* out, int accumulate, cudaStream_t st) {
-  const int M = 3 * g.nq;
-  const size_t n = (size_t)M * g.np;
+                      double* out, int accumulate, cudaStream_t st, int s0, int s1) {
+  // spheres [s0, s1) only (sharded operator); columns are contiguous per sphere
+  if (s1 < 0) s1 = g.np;
+  const int M = 3 * g.nq, ncol = s1 - s0;
+  if (ncol <= 0) return;
+  const size_t off = (size_t)M * s0;
+  X += off;
+  out += off;
+  if (add1) add1 += off;
+  if (add2) add2 += off;
+  const size_t n = (size_t)M * ncol;
   k3_prologue<<<(unsigned)std::min<size_t>((n + 255) / 256, 4 * (size_t)g.sms), 256, 0, st>>>(n, add1, add2, out,
                                                                                             accumulate);
-  const int mt = (M + K3_BM - 1) / K3_BM, nt = (g.np + K3_BN - 1) / K3_BN;
-  // split K so that the grid covers the GPU about twice
+  const int mt = (M + K3_BM - 1) / K3_BM, nt = (ncol + K3_BN - 1) / K3_BN;
+  // split K so that the grid covers the GPU about twice; no split (a single writer per
+  // output, bit-reproducible) when sharded, so that every rank's replicated GMRES agrees
   int ks = std::max(1, std::min((2 * g.sms + mt * nt - 1) / (mt * nt), (M + 8 * K3_BK - 1) / (8 * K3_BK)));
+  if (g.shard_world > 1) ks = 1;
   int kchunk = (M + ks - 1) / ks;
   kchunk = ((kchunk + K3_BK - 1) / K3_BK) * K3_BK;
   ks = (M + kchunk - 1) / kchunk;
@@ -190,7 +203,35 @@ void launch_self_gemm(Geom& g, const double* E, const double* X, const double* a
     BPQN_CUDA(cudaFuncSetAttribute(k3_self_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, K3_SMEM));
     attr = true;
   }
-  k3_self_gemm<<<grid, 256, K3_SMEM, st>>>(M, g.np, kchunk, E, X, out);
+  k3_self_gemm<<<grid, 256, K3_SMEM, st>>>(M, ncol, kchunk, E, X, out);
+  BPQN_CHECK_LAUNCH();
+  g.prof.launches += 2;
+}
+
+// Sharded operator (bpqn_geometry_shard): gather every rank's owned rows into `out`.
+__global__ void k_shard_pack(const double* __restrict__ out, int t0, int nrow, double* __restrict__ send, int rows) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 3 * rows) return;
+  send[e] = e < 3 * nrow ? out[3 * (size_t)t0 + e] : 0.0;
+}
+
+__global__ void k_shard_unpack(const double* __restrict__ recv, int world, int rows, int np, int nq,
+                               double* __restrict__ out) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 3LL * rows * world) return;
+  const int r = (int)(e / (3LL * rows)), k = (int)(e - 3LL * rows * r);
+  const int s0 = (int)((long long)np * r / world), s1 = (int)((long long)np * (r + 1) / world);
+  if (k < 3 * (s1 - s0) * nq) out[3 * (size_t)s0 * nq + k] = recv[e];
+}
+
+static void shard_exchange(Geom& g, double* out, cudaStream_t st) {
+  const int nrow = g.sh_t1 - g.sh_t0;
+  k_shard_pack<<<(3 * g.sh_rows + 255) / 256, 256, 0, st>>>(out, g.sh_t0, nrow, g.sh_send, g.sh_rows);
+  BPQN_CHECK_LAUNCH();
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  if (g.sh_fn(g.sh_user) != 0) throw Error{BPQN_ERR_CUDA, "shard all-gather callback failed"};
+  const long long tot = 3LL * g.sh_rows * g.shard_world;
+  k_shard_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.sh_recv, g.shard_world, g.sh_rows, g.np, g.nq, out);
   BPQN_CHECK_LAUNCH();
   g.prof.launches += 2;
 }
@@ -233,20 +274,24 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
   if (ev) {
     BPQN_CUDA(cudaEventRecord(ev[1], st));
-    P.allpairs_flop += (double)g.n * (double)g.n * allpairs_flops_per_pair(mode);
+    const double ntg = g.shard_world > 1 ? (double)(g.sh_t1 - g.sh_t0) : (double)g.n;  // this rank's targets
+    P.allpairs_flop += (double)g.n * ntg * allpairs_flops_per_pair(mode);
   }
   if (overlap) {
     BPQN_CUDA(cudaEventRecord(g.ev_join, g.side));
     BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
   }
+  const bool sharded = g.shard_world > 1;
+  const int s0 = sharded ? g.sh_s0 : 0, s1 = sharded ? g.sh_s1 : g.np;
   if (sigS && sigD) {
-    launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st);
-    launch_self_gemm(g, Ed, sigD, nullptr, nullptr, out, 1, st);
+    launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st, s0, s1);
+    launch_self_gemm(g, Ed, sigD, nullptr, nullptr, out, 1, st, s0, s1);
   } else if (sigS) {
-    launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st);
+    launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st, s0, s1);
   } else {
-    launch_self_gemm(g, Ed, sigD, g.far.p, g.nearout.p, out, 0, st);
+    launch_self_gemm(g, Ed, sigD, g.far.p, g.nearout.p, out, 0, st, s0, s1);
   }
+  if (sharded) shard_exchange(g, out, st);
   if (ev) BPQN_CUDA(cudaEventRecord(ev[4], st));
 }
 
