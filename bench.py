@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--solvers", default="bi")          # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--shard", action="store_true")     # N > 1: shard one MVP over the ranks (NCCL all-gather)
+    ap.add_argument("--sub-forcing", type=float, default=0.0)   # Bi-PQN inexact subproblems (off = R22)
     ap.add_argument("--c5-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-targets", type=int, default=0)
     return ap.parse_args()
@@ -371,7 +372,7 @@ def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
     torch.cuda.synchronize()
     ms_b = e0.elapsed_time(e1)
     o = bp.default_solve_opts(method=1 if lo is not None else (2 if meth == "bb" else 0), eps_kkt_abs=1e-8,
-                              eps_kkt_rel=1e-8, k_max=500)
+                              eps_kkt_rel=1e-8, k_max=500, sub_forcing=args.sub_forcing)
     o.gm_hi = gmo
     o.gm_lo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart, recycle=int(args.recycle))
     lam = torch.zeros(g.nc, dtype=torch.float64, device=dev)

@@ -96,6 +96,9 @@ typedef struct {
   double curv_skip;           /* BFGS curvature skip threshold (R16, default 1e-12) */
   bpqn_gmres_opts gm_hi, gm_lo;
   double cost_ratio;          /* t_lo/t_hi for E-MVPs; <= 0 -> measured */
+  double sub_forcing;         /* Bi-PQN only, default 0 (off, R22): > 0 solves each subproblem to
+                                 max(sub_eps_factor eps, sub_forcing * current hi KKT error)
+                                 (inexact proximal Newton; not in the paper) */
 } bpqn_solve_opts;
 
 typedef struct {

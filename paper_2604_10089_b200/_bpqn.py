@@ -34,7 +34,7 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("method", c_int), ("k_max", c_int), ("eps_kkt_abs", c_double), ("eps_kkt_rel", c_double),
                 ("tau", c_double), ("refresh_period", c_int), ("sub_eps_factor", c_double),
                 ("sub_k_max", c_int), ("prox_tol", c_double), ("prox_jmax", c_int), ("curv_skip", c_double),
-                ("gm_hi", GmresOpts), ("gm_lo", GmresOpts), ("cost_ratio", c_double)]
+                ("gm_hi", GmresOpts), ("gm_lo", GmresOpts), ("cost_ratio", c_double), ("sub_forcing", c_double)]
 
 
 class Report(ctypes.Structure):

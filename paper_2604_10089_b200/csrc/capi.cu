@@ -204,6 +204,7 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o) {
   bpqn_default_gmres_opts(&o->gm_lo);
   o->gm_hi.recycle = o->gm_lo.recycle = 1;
   o->cost_ratio = 0.0;
+  o->sub_forcing = 0.0;
 }
 
 int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius, double mu,
@@ -457,6 +458,7 @@ static PqnOpts to_pqn(const bpqn_solve_opts& o) {
   q.prox_tol = o.prox_tol;
   q.prox_jmax = o.prox_jmax;
   q.curv = o.curv_skip;
+  q.sub_forcing = o.sub_forcing;
   return q;
 }
 

@@ -616,6 +616,7 @@ BiResult bi_pqn(const MvpFn& hi, const MvpFn& lo, const Vec& b, const Vec& x_ini
     };
     PqnOpts so = o;
     so.eps_abs = o.sub_eps_factor * o.eps_abs;
+    if (o.sub_forcing > 0) so.eps_abs = std::max(so.eps_abs, o.sub_forcing * e);  // inexact subproblems
     so.eps_rel = 0;
     so.k_max = o.sub_k_max;
     MonoResult rs = mono_pqn(sub, c, x, so, &g, &Ahat_x, &low);

@@ -17,6 +17,7 @@ struct PqnOpts {
   double prox_tol = 0.0;
   int prox_jmax = 100;
   double curv = 1e-12;
+  double sub_forcing = 0.0;
 };
 
 struct Bfgs {
