@@ -401,3 +401,19 @@ def test_gmres_not_converged_reported(bp):
     assert e.value.code == 4
     _, st = bp.mobility_apply(g, T(z["FT_test"]), gmres=bp.default_gmres_opts(tol=1e-6))
     assert 1 <= st.iters < 60 and st.rel_resid <= 1e-6 and st.applies >= st.iters
+
+
+def test_bi_pqn_inexact_subproblems_same_solution(bp):
+    """The sub_forcing option changes the work, not the LCP solution (unique, R30)."""
+    z = fixture(2)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    pr, nr, gp = bp.contacts(g, 0.1)
+    lo = bp.Geometry(z["centers"], int(z["p_lo"]))
+    bp.set_contacts(lo, pr, nr, gp)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-10, sub_forcing=0.1)
+    o.gm_hi.tol = 1e-12
+    o.gm_lo.tol = 1e-12
+    lam, rep, rc = bp.solve_lcp(g, lo, T(z["b"]), T(np.zeros(g.nc)), opts=o)
+    assert rc == 0
+    assert rel(lam.cpu().numpy(), z["lam_bi"]) <= TOL_LAM
+    assert rep.lo_mvps <= int(z["bi_lo_mvps"])
