@@ -646,8 +646,8 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
 }
 
-// Launch shape per mode, measured on B200 at c4 (profiles/r01_k1_sym_shapes.md): D with 8
-// warps x 4 targets/lane at 1 CTA/SM, S with 12 x 3, S+D with 8 x 3.
+// Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps x 4 targets/lane
+// at 1 CTA/SM for N >= 6e4 (c4: D 16.0, S 16.05, S+D 23.95 ms), 8 x 3 below.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -661,7 +661,7 @@ static int k1_cfg() {
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
   int c = k1_cfg();
-  if (c < 0) c = MODE == MODE_SD ? 3 : (MODE == MODE_D ? (g.n >= 60000 ? 4 : 3) : 1);
+  if (c < 0) c = g.n >= 60000 ? 4 : 3;
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
@@ -674,6 +674,8 @@ static void launch_sym(Geom& g, double* out, cudaStream_t st) {
     case 9: launch_sym_cfg<MODE, 8, 3, 2>(g, out, st); break;
     case 10: launch_sym_cfg<MODE, 8, 4, 1, 1>(g, out, st); break;
     case 11: launch_sym_cfg<MODE, 4, 4, 2>(g, out, st); break;
+    case 12: launch_sym_cfg<MODE, 12, 4, 1>(g, out, st); break;
+    case 13: launch_sym_cfg<MODE, 12, 4, 1, 1>(g, out, st); break;
     default: launch_sym_cfg<MODE, 8, 2, 2>(g, out, st); break;
   }
 }
