@@ -120,7 +120,7 @@ struct Geom {
   DBuf<double> packed;   // K1 packed source records [npad][<=12]
   DBuf<double> far;      // [N][3] all-pairs accumulator
   DBuf<double> nearout;  // [N][3]
-  DBuf<double> rhs, sol, tmp, tmp2;  // [N][3]
+  DBuf<double> rhs, sol, tmp, tmp2, tmp3;  // [N][3]
   DBuf<double> V;        // GMRES basis [(m+1)][3N]
   DBuf<double> red;      // reduction scratch
   DBuf<double> scal;     // device scalars
@@ -128,6 +128,10 @@ struct Geom {
   // GMRES recycling store (gmres.cu): W orthonormal past rhs, Z = A_op^-1 W
   DBuf<double> rec_W, rec_Z;
   int rec_k = 0, rec_cap = 0;
+  // GCRO deflation space (gmres.cu, R33b): A~ U = C, C orthonormal, def_k vectors
+  DBuf<double> def_U, def_C;
+  int def_k = 0;
+  bool def_pre = false;
   double* host_scal = nullptr;  // pinned
   int gm_restart = 0;
 

@@ -3,6 +3,8 @@
 #include <chrono>
 #include <limits>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -280,6 +282,7 @@ int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream
     precompute(*g, st, false);  // near rows only; grid, SH analysis, self operators and inverse kept
     g->nc = 0;
     g->rec_k = 0;
+    g->def_k = 0;
     return BPQN_OK;
   });
 }
@@ -479,8 +482,8 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     BPQN_CUDA(cudaMemcpyAsync(x0.data(), lambda_dev, 8 * nc, cudaMemcpyDeviceToHost, s));
     BPQN_CUDA(cudaStreamSynchronize(s));
     for (double v : x0) BPQN_REQUIRE(v >= 0, "x_init must be >= 0");
-    if (o.gm_hi.recycle) hi->rec_k = 0;
-    if (bi && o.gm_lo.recycle) lo->rec_k = 0;
+    if (o.gm_hi.recycle) hi->rec_k = hi->def_k = 0;
+    if (bi && o.gm_lo.recycle) lo->rec_k = lo->def_k = 0;
     DBuf<double> dv, dw;
     dv.alloc(nc);
     dw.alloc(nc);
@@ -502,6 +505,10 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
         its += st.iters;
         cnt++;
         if (rc) gm_fail = rc;
+        static const bool log_mvp = getenv("BPQN_LOG_MVP") != nullptr;
+        if (log_mvp)
+          fprintf(stderr, "mvp %s #%d: rc %d its %d resid %.2e applies %d ms %.1f\n", g == hi ? "hi" : "lo", cnt, rc,
+                  st.iters, st.rel_resid, st.applies, st.ms);
         (void)aux;
       };
     };
@@ -676,11 +683,13 @@ int bpqn_dvi_step(bpqn_geom_t hi, bpqn_geom_t lo, double* centers_host, double* 
     precompute(g, s, false);
     g.nc = 0;
     g.rec_k = 0;
+    g.def_k = 0;
     if (lo) {
       set_centers(*lo, cn.data(), s);
       precompute(*lo, s, false);
       lo->nc = 0;
       lo->rec_k = 0;
+      lo->def_k = 0;
     }
     std::copy(cn.begin(), cn.end(), centers_host);
     std::copy(an.begin(), an.end(), axes_host);
@@ -745,6 +754,7 @@ int bpqn_gmres_recycle_reset(bpqn_geom_t g) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");
     g->rec_k = 0;
+    g->def_k = 0;
     return BPQN_OK;
   });
 }

@@ -8,6 +8,8 @@
 // tolerance eps_gmres is met"; the equation itself is reading R1.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <vector>
 
 #include "bpqn_internal.h"
 
@@ -91,9 +93,11 @@ __global__ void k_scale(double* y, const double* x, size_t n, const double* sc, 
 // Device GMRES state layout (doubles) inside g.scal:
 //   [0] beta0 (|b|)   [1] resid   [2] nrm2 scratch  [3] beta_{k+1}
 //   H at 8, (m+1)*m column-major ; cs, sn, gv after ; h1, h2 (m+1 each) ; y (m)
+constexpr int KD_MAX = 32;  // deflation (GCRO) space dimension cap
+
 struct GmLayout {
   int m;
-  size_t H, cs, sn, gv, h1, h2, y, total;
+  size_t H, cs, sn, gv, h1, h2, y, Hraw, Bm, cd, total;
   explicit GmLayout(int mm) : m(mm) {
     H = 8;
     cs = H + (size_t)(m + 1) * m;
@@ -102,7 +106,10 @@ struct GmLayout {
     h1 = gv + m + 1;
     h2 = h1 + m + 1;
     y = h2 + m + 1;
-    total = y + m + 1;
+    Hraw = y + m + 1;                 // unrotated Hessenberg (m+1) x m, column-major
+    Bm = Hraw + (size_t)(m + 1) * m;  // B = C^T A V, column k at Bm + k * KD_MAX
+    cd = Bm + (size_t)KD_MAX * m;     // KD_MAX coefficients
+    total = cd + KD_MAX;
   }
 };
 
@@ -111,10 +118,11 @@ struct GmLayout {
 __global__ void k_givens(double* S, GmLayout L, int k, double beta_b) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   double* H = S + L.H + (size_t)k * (L.m + 1);
-  for (int i = 0; i <= k; ++i) H[i] = S[L.h1 + i] + S[L.h2 + i];
+  double* Hr = S + L.Hraw + (size_t)k * (L.m + 1);
+  for (int i = 0; i <= k; ++i) Hr[i] = H[i] = S[L.h1 + i] + S[L.h2 + i];
   double bk = sqrt(S[2]);
   S[3] = bk;
-  H[k + 1] = bk;
+  Hr[k + 1] = H[k + 1] = bk;
   double* cs = S + L.cs;
   double* sn = S + L.sn;
   double* gv = S + L.gv;
@@ -167,6 +175,71 @@ __global__ void k_add_basis(const double* __restrict__ V, size_t ld, int kk, con
 
 __global__ void k_set(double* d, double v) { *d = v; }
 
+// c[i] = sum_{j<kk} B[j * KD_MAX + i] y[j], i < kd   (GCRO correction B y)
+__global__ void k_small_matvec(const double* B, const double* y, int kk, int kd, double* c) {
+  const int i = threadIdx.x;
+  if (i >= kd) return;
+  double acc = 0.0;
+  for (int j = 0; j < kk; ++j) acc = fma(B[(size_t)j * KD_MAX + i], y[j], acc);
+  c[i] = acc;
+}
+
+// out[i][e] = sum_{j<nv} V[j][e] coef[j * nout + i]   (recycle-space construction)
+__global__ void k_combine(const double* __restrict__ V, size_t ld, int nv, const double* __restrict__ coef,
+                          int nout, double* __restrict__ out, size_t n) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    double acc[KD_MAX];
+    for (int i = 0; i < nout; ++i) acc[i] = 0.0;
+    for (int j = 0; j < nv; ++j) {
+      const double v = V[(size_t)j * ld + e];
+      for (int i = 0; i < nout; ++i) acc[i] = fma(v, coef[j * nout + i], acc[i]);
+    }
+    for (int i = 0; i < nout; ++i) out[(size_t)i * ld + e] = acc[i];
+  }
+}
+
+// ---- host: small dense linear algebra for the recycle space
+// cyclic Jacobi eigen-decomposition of a symmetric n x n matrix (row-major, destroyed);
+// eigenvalues in w, eigenvectors as columns of Q (row-major)
+static void jacobi_eig(std::vector<double>& A, int n, std::vector<double>& w, std::vector<double>& Q) {
+  Q.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) Q[(size_t)i * n + i] = 1.0;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) {
+        tot += A[(size_t)i * n + j] * A[(size_t)i * n + j];
+        if (i != j) off += A[(size_t)i * n + j] * A[(size_t)i * n + j];
+      }
+    if (off <= 1e-30 * tot) break;
+    for (int p = 0; p < n; ++p)
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A[(size_t)p * n + q];
+        if (std::fabs(apq) < 1e-300) continue;
+        const double th = 0.5 * (A[(size_t)q * n + q] - A[(size_t)p * n + p]) / apq;
+        const double t = (th >= 0 ? 1.0 : -1.0) / (std::fabs(th) + std::sqrt(th * th + 1.0));
+        const double c = 1.0 / std::sqrt(t * t + 1.0), sn = t * c;
+        for (int k = 0; k < n; ++k) {  // rows p, q
+          const double a = A[(size_t)p * n + k], b = A[(size_t)q * n + k];
+          A[(size_t)p * n + k] = c * a - sn * b;
+          A[(size_t)q * n + k] = sn * a + c * b;
+        }
+        for (int k = 0; k < n; ++k) {  // columns p, q
+          const double a = A[(size_t)k * n + p], b = A[(size_t)k * n + q];
+          A[(size_t)k * n + p] = c * a - sn * b;
+          A[(size_t)k * n + q] = sn * a + c * b;
+        }
+        for (int k = 0; k < n; ++k) {
+          const double a = Q[(size_t)k * n + p], b = Q[(size_t)k * n + q];
+          Q[(size_t)k * n + p] = c * a - sn * b;
+          Q[(size_t)k * n + q] = sn * a + c * b;
+        }
+      }
+  }
+  w.resize(n);
+  for (int i = 0; i < n; ++i) w[i] = A[(size_t)i * n + i];
+}
+
 __global__ void k_sub(double* r, const double* b, const double* ax, size_t n) {
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     r[e] = b[e] - ax[e];
@@ -192,6 +265,100 @@ static double read_scalar(Geom& g, const double* dev, cudaStream_t st) {
   return g.host_scal[0];
 }
 
+// Recycle space for GCRO (R33b): from the last Arnoldi cycle A~ V_kk = V_{kk+1} Hbar
+// (A~ = A_op M^-1), the kd right singular vectors G of Hbar with the smallest singular
+// values; [Q, R] = qr(Hbar G); C = V_{kk+1} Q (orthonormal), U = V_kk G R^-1, so that
+// A~ U = C exactly (no operator applications).  Slow GMRES modes are deflated from
+// every later solve on the same operator.
+static void build_deflation(Geom& g, const GmLayout& L, int kk, int kd, bool pre, size_t n, cudaStream_t st) {
+  kd = std::min(kd, kk - 1);
+  if (kd < 1) return;
+  std::vector<double> Hr((size_t)(L.m + 1) * kk);
+  BPQN_CUDA(cudaMemcpyAsync(Hr.data(), g.scal.p + L.Hraw, Hr.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  auto H = [&](int i, int j) { return Hr[(size_t)j * (L.m + 1) + i]; };  // (kk+1) x kk
+  std::vector<double> M((size_t)kk * kk, 0.0), w, Q;
+  for (int i = 0; i < kk; ++i)
+    for (int j = 0; j < kk; ++j) {
+      double acc = 0.0;
+      for (int r = 0; r <= kk; ++r) acc += H(r, i) * H(r, j);
+      M[(size_t)i * kk + j] = acc;
+    }
+  jacobi_eig(M, kk, w, Q);
+  std::vector<int> ord(kk);
+  for (int i = 0; i < kk; ++i) ord[i] = i;
+  std::sort(ord.begin(), ord.end(), [&](int u, int v) { return w[u] < w[v]; });
+  // P = Hbar G, modified Gram-Schmidt twice -> Qp, R
+  std::vector<double> G((size_t)kk * kd), P((size_t)(kk + 1) * kd), R((size_t)kd * kd, 0.0);
+  for (int c = 0; c < kd; ++c)
+    for (int j = 0; j < kk; ++j) G[(size_t)j * kd + c] = Q[(size_t)j * kk + ord[c]];
+  for (int r = 0; r <= kk; ++r)
+    for (int c = 0; c < kd; ++c) {
+      double acc = 0.0;
+      for (int j = 0; j < kk; ++j) acc += H(r, j) * G[(size_t)j * kd + c];
+      P[(size_t)r * kd + c] = acc;
+    }
+  double hn = 0.0;
+  for (double v : Hr) hn = std::max(hn, std::fabs(v));
+  int kept = 0;
+  for (int c = 0; c < kd; ++c) {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int q = 0; q < kept; ++q) {
+        double d = 0.0;
+        for (int r = 0; r <= kk; ++r) d += P[(size_t)r * kd + q] * P[(size_t)r * kd + c];
+        R[(size_t)q * kd + c] += d;
+        for (int r = 0; r <= kk; ++r) P[(size_t)r * kd + c] -= d * P[(size_t)r * kd + q];
+      }
+    double nr = 0.0;
+    for (int r = 0; r <= kk; ++r) nr += P[(size_t)r * kd + c] * P[(size_t)r * kd + c];
+    nr = std::sqrt(nr);
+    if (!(nr > 1e-10 * hn)) break;  // (near) breakdown: stop the space here
+    for (int r = 0; r <= kk; ++r) P[(size_t)r * kd + c] /= nr;
+    R[(size_t)c * kd + c] = nr;
+    if (c != kept) {  // keep columns contiguous
+      for (int r = 0; r <= kk; ++r) P[(size_t)r * kd + kept] = P[(size_t)r * kd + c];
+      for (int j = 0; j < kk; ++j) G[(size_t)j * kd + kept] = G[(size_t)j * kd + c];
+    }
+    ++kept;
+  }
+  if (kept < 1) return;
+  kd = kept;
+  // Ucoef = G R^-1 (R upper triangular kd x kd, row-major with stride of the original kd)
+  const int ks = (int)std::sqrt((double)R.size());
+  std::vector<double> Uc((size_t)kk * kd), Cc((size_t)(kk + 1) * kd);
+  for (int j = 0; j < kk; ++j)
+    for (int c = 0; c < kd; ++c) {  // row j of G times R^-1 by forward substitution
+      double acc = G[(size_t)j * ks + c];
+      for (int q = 0; q < c; ++q) acc -= Uc[(size_t)j * kd + q] * R[(size_t)q * ks + c];
+      Uc[(size_t)j * kd + c] = acc / R[(size_t)c * ks + c];
+    }
+  for (int r = 0; r <= kk; ++r)
+    for (int c = 0; c < kd; ++c) Cc[(size_t)r * kd + c] = P[(size_t)r * ks + c];
+  DBuf<double> dUc, dCc;
+  dUc.alloc(Uc.size());
+  dCc.alloc(Cc.size());
+  BPQN_CUDA(cudaMemcpyAsync(dUc.p, Uc.data(), Uc.size() * 8, cudaMemcpyHostToDevice, st));
+  BPQN_CUDA(cudaMemcpyAsync(dCc.p, Cc.data(), Cc.size() * 8, cudaMemcpyHostToDevice, st));
+  g.def_U.ensure((size_t)KD_MAX * n);
+  g.def_C.ensure((size_t)KD_MAX * n);
+  const int blocks = std::min<int>((int)((n + 255) / 256), g.sms * 8);
+  k_combine<<<blocks, 256, 0, st>>>(g.V.p, n, kk, dUc.p, kd, g.def_U.p, n);
+  k_combine<<<blocks, 256, 0, st>>>(g.V.p, n, kk + 1, dCc.p, kd, g.def_C.p, n);
+  BPQN_CHECK_LAUNCH();
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  g.def_k = kd;
+  g.def_pre = pre;
+}
+
+static int deflation_dim() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BPQN_DEFLATE");
+    v = e ? std::max(0, std::min(KD_MAX, atoi(e))) : 0;  // experimental: off by default
+  }
+  return v;
+}
+
 int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, bpqn_gmres_stats& stt,
                 cudaStream_t st) {
   const size_t n = 3 * (size_t)g.n;
@@ -200,8 +367,9 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   GmLayout L(m);
   g.V.ensure((size_t)(m + 1) * n);
   int nbx = nbx_for(n, g.sms);
-  g.red.ensure((size_t)(m + 2) * nbx + 16);
+  g.red.ensure((size_t)(std::max(m, KD_MAX) + 2) * nbx + 16);
   g.scal.ensure(L.total);
+  g.tmp3.ensure(n);
   double* S = g.scal.p;
   const size_t ld = n;
   cudaEvent_t e0, e1;
@@ -216,19 +384,22 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   stt.restarts = 0;
   stt.rel_resid = 0.0;
   stt.applies = 0;
-  // Recycling: W orthonormal past right-hand sides, Z with
-  // A_op Z = W (to the past solves' tolerance).  Initial guess x0 = Z W^T b.
+  // Recycling (R33): W orthonormal past right-hand sides, Z with
+  // A_op Z = W (to the past solves' tolerance).  Initial guess x0 = Z W^T b.  Plus a
+  // deflation space (U, C = A~ U) built after the first solve (GCRO, R33b).
   const bool rec = o.recycle != 0 && beta_b > 0.0 && std::isfinite(beta_b);
   if (rec && g.rec_cap == 0) {  // lazily: up to 256 pairs within ~4 GB
     g.rec_cap = (int)std::max<size_t>(1, std::min<size_t>(256, (size_t)4e9 / (2 * n * sizeof(double))));
     g.rec_W.alloc((size_t)g.rec_cap * n);
     g.rec_Z.alloc((size_t)g.rec_cap * n);
     g.rec_k = 0;
+    g.def_k = 0;
   }
   const int kr = rec ? g.rec_k : 0;
+  const int kd = (rec && g.def_pre == pre) ? g.def_k : 0;  // active deflation dimension
   double* Sc = nullptr;
   if (rec) {
-    g.red.ensure((size_t)(std::max(m, g.rec_cap) + 2) * nbx + 16);
+    g.red.ensure((size_t)(std::max(std::max(m, g.rec_cap), KD_MAX) + 2) * nbx + 16);
     g.scal.ensure(L.total + 2 * (size_t)(g.rec_cap + 1));
     S = g.scal.p;
     Sc = S + L.total;
@@ -253,8 +424,15 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   }
   const int blocks_vec = std::min<int>((int)((n + 255) / 256), g.sms * 8);
   double* r = g.tmp.p;
-  bool first = kr == 0;
+  // x += M^-1 z (or z) for z in tmp3
+  auto add_prec = [&](const double* z) {
+    if (pre) launch_self_gemm(g, g.Minv.p, z, nullptr, nullptr, x, 1, st);
+    else launch_axpby(x, 1.0, z, 1.0, n, st);
+  };
+  bool first = kr == 0 && kd == 0;
+  bool have_x = kr > 0;
   double resid = 1.0;
+  int last_kk = 0;
   for (;;) {
     double beta;
     if (first) {
@@ -263,13 +441,31 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       k_scale<<<blocks_vec, 256, 0, st>>>(g.V.p, b, n, S + 3, 1);  // V0 = b / beta
       first = false;
     } else {
-      // r = b - A x (restart, or the recycled initial guess)
-      apply_operator(g, nullptr, x, nullptr, g.E_A.p, g.tmp2.p, st);
-      stt.applies++;
-      k_sub<<<blocks_vec, 256, 0, st>>>(r, b, g.tmp2.p, n);
+      if (have_x) {  // r = b - A x (restart, or the recycled initial guess)
+        apply_operator(g, nullptr, x, nullptr, g.E_A.p, g.tmp2.p, st);
+        stt.applies++;
+        k_sub<<<blocks_vec, 256, 0, st>>>(r, b, g.tmp2.p, n);
+        stt.restarts += stt.iters > 0;
+      } else {
+        BPQN_CUDA(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      }
+      have_x = true;
+      if (kd > 0) {  // GCRO projection: c = C^T r, x += M^-1 U c, r -= C c
+        k_mdot<<<dim3(nbx, kd), GT, 0, st>>>(g.def_C.p, n, r, n, g.red.p, nbx);
+        k_reduce_rows<<<kd, 256, 0, st>>>(g.red.p, nbx, S + L.cd, 0);
+        k_mupdate<<<nbx, GT, 0, st>>>(g.def_C.p, n, kd, S + L.cd, r, n, nullptr, nbx);
+        BPQN_CUDA(cudaMemsetAsync(g.tmp3.p, 0, n * sizeof(double), st));
+        k_add_basis<<<blocks_vec, 256, 0, st>>>(g.def_U.p, n, kd, S + L.cd, g.tmp3.p, n);
+        add_prec(g.tmp3.p);
+        BPQN_CHECK_LAUNCH();
+        g.prof.launches += 5;
+      }
       norm2(g, r, n, S + 2, st);
       beta = std::sqrt(read_scalar(g, S + 2, st));
-      if (!(beta > 0.0)) break;
+      if (!(beta > 0.0)) {
+        resid = 0.0;
+        break;
+      }
       resid = beta / beta_b;
       if (!std::isfinite(resid)) {
         status = BPQN_ERR_NAN;
@@ -278,7 +474,6 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       if (resid <= o.tol) break;
       k_set<<<1, 1, 0, st>>>(S + 3, beta);
       k_scale<<<blocks_vec, 256, 0, st>>>(g.V.p, r, n, S + 3, 1);
-      stt.restarts++;
     }
     BPQN_CHECK_LAUNCH();
     k_init_cycle<<<1, 64, 0, st>>>(S, L, beta);
@@ -294,6 +489,13 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
         apply_operator(g, nullptr, vk, nullptr, g.E_A.p, w, st);
       }
       stt.applies++;
+      if (kd > 0) {  // (I - C C^T) A~ v_k ; column k of B = C^T A~ v_k
+        double* Bk = S + L.Bm + (size_t)k * KD_MAX;
+        k_mdot<<<dim3(nbx, kd), GT, 0, st>>>(g.def_C.p, n, w, n, g.red.p, nbx);
+        k_reduce_rows<<<kd, 256, 0, st>>>(g.red.p, nbx, Bk, 0);
+        k_mupdate<<<nbx, GT, 0, st>>>(g.def_C.p, n, kd, Bk, w, n, nullptr, nbx);
+        g.prof.launches += 3;
+      }
       // CGS2
       k_mdot<<<dim3(nbx, k + 1), GT, 0, st>>>(g.V.p, ld, w, n, g.red.p, nbx);
       k_reduce_rows<<<k + 1, 256, 0, st>>>(g.red.p, nbx, S + L.h1, 0);
@@ -325,18 +527,26 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       }
     }
     k_backsolve<<<1, 32, 0, st>>>(S, L, kk);
-    if (pre) {  // x += M^-1 (V y)
-      BPQN_CUDA(cudaMemsetAsync(g.tmp2.p, 0, n * sizeof(double), st));
-      k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, kk, S + L.y, g.tmp2.p, n);
-      launch_self_gemm(g, g.Minv.p, g.tmp2.p, nullptr, nullptr, x, 1, st);
-    } else {
-      k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, kk, S + L.y, x, n);
+    // x += M^-1 (V y - U (B y))
+    BPQN_CUDA(cudaMemsetAsync(g.tmp3.p, 0, n * sizeof(double), st));
+    k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, kk, S + L.y, g.tmp3.p, n);
+    if (kd > 0) {
+      k_small_matvec<<<1, KD_MAX, 0, st>>>(S + L.Bm, S + L.y, kk, kd, S + L.cd);
+      k_mupdate<<<nbx, GT, 0, st>>>(g.def_U.p, n, kd, S + L.cd, g.tmp3.p, n, nullptr, nbx);
+      g.prof.launches += 2;
     }
+    add_prec(g.tmp3.p);
     BPQN_CHECK_LAUNCH();
-    g.prof.launches += 2;
+    g.prof.launches += 3;
+    have_x = true;
+    last_kk = kk;
     if (done) break;
   }
   stt.rel_resid = resid;
+  // first solve on this operator with recycling: build the deflation space from its last cycle
+  const int kdef = deflation_dim();
+  if (rec && status == BPQN_OK && g.def_k == 0 && kdef > 0 && last_kk >= kdef + 2)
+    build_deflation(g, L, last_kk, kdef, pre, n, st);
   if (rec && status == BPQN_OK && g.rec_k < g.rec_cap) {
     // append (b, x): CGS2 of b against W with the same coefficients applied to x vs Z
     const size_t ld2 = n;
