@@ -26,7 +26,10 @@
 //    own node) zeroes the seed with an integer select, so that pair contributes 0.
 #include <algorithm>
 #include <cstdlib>
+#include <mutex>
 #include <string>
+#include <utility>
+#include <vector>
 
 #include "bpqn_internal.h"
 
@@ -634,13 +637,27 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   const int nslot_max = KS_B / g.nq + 2;
   const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
                     (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * K1_TS)) * 8;
-  static int grid = 0, grid_smem = -1;  // per instantiation; smem grows with Np
-  if (smem != grid_smem) {
-    BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    int b = 0;
-    BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB, UNR>, 32 * W, smem));
-    grid = std::max(1, b) * g.sms;
-    grid_smem = smem;
+  // per instantiation: the opt-in smem limit only grows; occupancy cached per smem size
+  // (hi and lo fidelity handles alternate in Bi-PQN with different table sizes)
+  static std::mutex mu;
+  static int attr_smem = 0;
+  static std::vector<std::pair<int, int>> occ;  // (smem, grid)
+  int grid = 0;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    if (smem > attr_smem) {
+      BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     smem));
+      attr_smem = smem;
+    }
+    for (auto& e : occ)
+      if (e.first == smem) grid = e.second;
+    if (!grid) {
+      int b = 0;
+      BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB, UNR>, 32 * W, smem));
+      grid = std::max(1, b) * g.sms;
+      occ.emplace_back(smem, grid);
+    }
   }
   const int gr = (int)std::min<long long>(grid, P.units);
   k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
