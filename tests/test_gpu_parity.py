@@ -417,3 +417,43 @@ def test_bi_pqn_inexact_subproblems_same_solution(bp):
     assert rc == 0
     assert rel(lam.cpu().numpy(), z["lam_bi"]) <= TOL_LAM
     assert rep.lo_mvps <= int(z["bi_lo_mvps"])
+
+
+def test_geometry_update_equals_fresh_init(bp):
+    """bpqn_geometry_update (kept self operators, rebuilt near data) == a fresh handle."""
+    from synth import layer_densities, make_config
+    cfg = make_config(2)
+    C1 = 1.01 * cfg["centers"] + np.array([0.3, -0.2, 0.1])   # dilate + shift: gaps grow, near sets change
+    g = bp.Geometry(cfg["centers"], cfg["p"])
+    bp.geometry_update(g, C1)
+    h = bp.Geometry(C1, cfg["p"])
+    f, q = layer_densities(2, g.N)
+    u1 = bp.layer_apply(g, T(f), T(q)).cpu().numpy()
+    u2 = bp.layer_apply(h, T(f), T(q)).cpu().numpy()
+    assert rel(u1, u2) <= 1e-13
+    with pytest.raises(bp.BpqnError) as e:          # overlapping update is rejected
+        C2 = C1.copy()
+        C2[1] = C2[0] + np.array([1.9, 0.0, 0.0])
+        bp.geometry_update(g, C2)
+    assert e.value.code == 1
+
+
+def test_dvi_step_bi_pqn_vs_oracle(bp):
+    """One DVI step with the Bi-PQN solver (hi p = 6, lo p = 4 handles moved together)."""
+    from oracle import dvi
+    C0 = np.array([[0.0, 0.0, 0.0], [2.03, 0.05, 0.0], [4.07, -0.05, 0.04]])
+    ax0 = np.array([[0.0, 0.6, 0.8], [1.0, 0.0, 0.0], [0.0, -0.8, 0.6]])
+    F = np.array([[12.0, 0.0, 0.0], [0.0, 0.0, 0.0], [-12.0, 0.0, 0.0]])
+    hi, lo = bp.Geometry(C0, 6), bp.Geometry(C0, 4)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-12)
+    o.gm_hi.tol = o.gm_lo.tol = 1e-12
+    C, ax = C0.copy(), ax0.copy()
+    uo, rep, rc = bp.dvi_step(hi, lo, C, ax, F, slip_B=1.0, dt=0.2, delta=0.1, opts=o)
+    assert rc == 0 and rep.active_contacts > 0 and rep.lcp.lo_mvps > 0
+    Cn, an, Uo, lam, pairs = dvi.dvi_step(C0, ax0, F, p=6, dt=0.2, slip_B=1.0)
+    assert rel(C - C0, Cn - C0) <= 1e-7
+    np.testing.assert_allclose(ax, an, atol=1e-9)
+    # both handles now sit at the new centres: a fresh hi handle gives the same operator
+    f = np.random.default_rng(2).standard_normal((hi.N, 3))
+    fresh = bp.Geometry(C, 6)
+    assert rel(bp.layer_apply(hi, T(f)).cpu().numpy(), bp.layer_apply(fresh, T(f)).cpu().numpy()) <= 1e-13

@@ -1,4 +1,4 @@
-"""Sharded operator (bpqn_geometry_shard, NEXT-4) -- two ranks, one GPU, gloo all-gather.
+"""Sharded operator (bpqn_geometry_shard, NEXT-4) -- two or three ranks, one GPU, gloo all-gather.
 
 Each rank computes only its spheres' operator rows and the rows are all-gathered through
 the host (gloo); no kernel waits on another process, so two ranks may share the single
@@ -47,8 +47,8 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("c", [1, 2])
-def test_sharded_mvp_two_ranks(c, tmp_path):
+@pytest.mark.parametrize("c,world", [(1, 2), (2, 2), (1, 3)])
+def test_sharded_mvp_two_ranks(c, world, tmp_path):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -64,16 +64,17 @@ def test_sharded_mvp_two_ranks(c, tmp_path):
     del g
     script = tmp_path / "w.py"
     script.write_text(WORKER.format(root=ROOT, c=c))
-    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), WORLD_SIZE="2")
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), WORLD_SIZE=str(world))
     procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), LOCAL_RANK=str(r)),
-                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(2)]
+                              stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(world)]
     outs = [p.communicate(timeout=600) for p in procs]
     for p, (o, e) in zip(procs, outs):
         assert p.returncode == 0, e[-3000:]
     res = [json.loads(o.strip().splitlines()[-1]) for o, _ in outs]
-    w0, w1 = np.array(res[0]["w"]), np.array(res[1]["w"])
-    assert np.array_equal(w0, w1)                                     # replicated, deterministic
-    assert np.array_equal(np.array(res[0]["uo"]), np.array(res[1]["uo"]))
+    w0 = np.array(res[0]["w"])
+    for r in res[1:]:                                                  # replicated, deterministic
+        assert np.array_equal(w0, np.array(r["w"]))
+        assert np.array_equal(np.array(res[0]["uo"]), np.array(r["uo"]))
     assert np.linalg.norm(w0 - w_ref) / np.linalg.norm(w_ref) <= 1e-9
     uo = np.array(res[0]["uo"])
     assert np.linalg.norm(uo - uo_ref) / np.linalg.norm(uo_ref) <= 1e-9
