@@ -47,7 +47,23 @@ def build(force=False, verbose=False):
         raise RuntimeError("nvcc failed")
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", LIB] + objs +
                           ["-lcudart", "-lgomp"])
+    build_example()
     return LIB
+
+
+EXAMPLE_SRC = os.path.join(HERE, "..", "examples", "bpqn_mvp.c")
+EXAMPLE_BIN = os.path.join(HERE, "..", "examples", "bpqn_mvp")
+
+
+def build_example():
+    """examples/bpqn_mvp: a plain-C client of the C ABI (no Python), rpath to the in-tree .so."""
+    if not os.path.exists(EXAMPLE_SRC):
+        return None
+    cuda = os.path.dirname(os.path.dirname(NVCC))
+    subprocess.check_call(["gcc", "-O2", EXAMPLE_SRC, "-o", EXAMPLE_BIN, "-I" + os.path.join(cuda, "include"),
+                           "-L" + HERE, "-lbpqn", "-L" + os.path.join(cuda, "lib64"), "-lcudart", "-lm",
+                           "-Wl,-rpath,$ORIGIN/../paper_2604_10089_b200"])
+    return EXAMPLE_BIN
 
 
 if __name__ == "__main__":

@@ -457,3 +457,23 @@ def test_dvi_step_bi_pqn_vs_oracle(bp):
     f = np.random.default_rng(2).standard_normal((hi.N, 3))
     fresh = bp.Geometry(C, 6)
     assert rel(bp.layer_apply(hi, T(f)).cpu().numpy(), bp.layer_apply(fresh, T(f)).cpu().numpy()) <= 1e-13
+
+
+def test_plain_c_client(bp):
+    """examples/bpqn_mvp (pure C against include/bpqn.h) gives the binding's MVP."""
+    import json
+    import subprocess
+    exe = os.path.join(ROOT, "examples", "bpqn_mvp")
+    if not os.path.exists(exe):
+        from paper_2604_10089_b200 import build as b
+        b.build_example()
+    out = json.loads(subprocess.check_output([exe, "6"], timeout=300).decode().strip().splitlines()[-1])
+    C = np.array([[2.05 * i + 0.01 * l, 2.05 * j - 0.01 * i, 2.05 * l + 0.005 * j]
+                  for i in range(2) for j in range(2) for l in range(2)])
+    g = bp.Geometry(C, 6)
+    bp.contacts(g, 0.1)
+    assert g.nc == out["n_contacts"]
+    w, st = bp.lcp_mvp(g, T(1.0 / (1 + np.arange(g.nc))))
+    assert abs(np.linalg.norm(w.cpu().numpy()) - out["w_norm"]) <= 1e-9 * out["w_norm"]
+    assert out["hi_mvps"] == out["lcp_iterations"] + 1 + out["lcp_iterations"] // 20
+    assert out["kkt_abs"] <= 1e-10
