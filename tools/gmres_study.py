@@ -24,7 +24,7 @@ bp.contacts(g, cfg["delta"])
 lam = torch.tensor(lambda_test(a.config, g.nc, 0), device="cuda")
 ref = None
 for tol in (1e-8, 1e-12):
-    for pre in (0, 1, 2):
+    for pre in (0, 1):
         for rs in [int(x) for x in a.restarts.split(",")]:
             w, st = bp.lcp_mvp(g, lam, gmres=bp.default_gmres_opts(tol=tol, restart=rs, precond=pre))
             w = w.cpu().numpy()
