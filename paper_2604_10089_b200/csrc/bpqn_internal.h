@@ -80,6 +80,43 @@ struct Profile {
   long long allpairs_launches = 0, launches = 0;
 };
 
+// CUDA graphs of the GMRES Arnoldi steps (gmres.cu), one per step index k, valid for one
+// set of buffer addresses / restart length / preconditioner flag.
+struct GraphCache {
+  std::vector<cudaGraphExec_t> exec;
+  std::vector<char> warm;
+  std::vector<long long> launches;
+  cudaStream_t cap = nullptr;
+  bool ok = true;
+  const void* sig[5] = {};
+  int m = -1;
+  bool pre = false;
+  void clear() {
+    for (auto& e : exec)
+      if (e) cudaGraphExecDestroy(e);
+    exec.clear();
+    warm.clear();
+    launches.clear();
+  }
+  void validate(const void* a, const void* b, const void* c, const void* d, const void* e, int mm, bool pp) {
+    const void* s2[5] = {a, b, c, d, e};
+    bool same = mm == m && pp == pre;
+    for (int i = 0; i < 5; ++i) same = same && s2[i] == sig[i];
+    if (same) return;
+    clear();
+    for (int i = 0; i < 5; ++i) sig[i] = s2[i];
+    m = mm;
+    pre = pp;
+    exec.assign(m, nullptr);
+    warm.assign(m, 0);
+    launches.assign(m, 0);
+  }
+  ~GraphCache() {
+    clear();
+    if (cap) cudaStreamDestroy(cap);
+  }
+};
+
 struct Geom {
   int np = 0, p = 0, nq = 0, n = 0, nb = 0;
   double a = 1, mu = 1, d_near = 0;
@@ -136,6 +173,7 @@ struct Geom {
   int gm_restart = 0;
 
   Profile prof;
+  GraphCache gm_graphs;
   cudaStream_t side = nullptr;            // K2 overlapped with K1 (layer.cu)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool overlap_k2 = false;

@@ -77,6 +77,8 @@ static void shard_ranges(Geom& g) {
 // |x_i - c_m| - a < d_near (R8), sorted by (i, m).
 static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
   Geom* g = &G;
+  g->gm_graphs.clear();  // captured GMRES steps hold the old near data and grid sizes
+  g->gm_graphs.m = -1;
   const double radius = g->a;
   const int n_spheres = g->np;
   g->centers.assign(centers_host, centers_host + 3 * (size_t)n_spheres);
@@ -299,6 +301,8 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
     }
     BPQN_REQUIRE(world <= g->np, "more ranks than spheres");
     BPQN_REQUIRE(send_dev && recv_dev && allgather, "null buffer or callback");
+    g->gm_graphs.clear();
+    g->gm_graphs.m = -1;
     g->shard_rank = rank;
     g->shard_world = world;
     g->sh_send = send_dev;

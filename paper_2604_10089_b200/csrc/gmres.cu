@@ -115,8 +115,9 @@ struct GmLayout {
 
 // Arnoldi column k: H[:,k] = h1 + h2 (k+1 entries), H[k+1,k] = sqrt(nrm2); apply
 // previous rotations, new rotation, update gv; resid = |gv[k+1]| / beta_b.
-__global__ void k_givens(double* S, GmLayout L, int k, double beta_b) {
+__global__ void k_givens(double* S, GmLayout L, int k) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double beta_b = S[0];  // |b| (device-resident: the step is replayed as a CUDA graph)
   double* H = S + L.H + (size_t)k * (L.m + 1);
   double* Hr = S + L.Hraw + (size_t)k * (L.m + 1);
   for (int i = 0; i <= k; ++i) Hr[i] = H[i] = S[L.h1 + i] + S[L.h2 + i];
@@ -350,6 +351,15 @@ static void build_deflation(Geom& g, const GmLayout& L, int kk, int kd, bool pre
   g.def_pre = pre;
 }
 
+static bool graphs_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("BPQN_GRAPHS");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 static int deflation_dim() {
   static int v = -1;
   if (v < 0) {
@@ -433,6 +443,81 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   bool have_x = kr > 0;
   double resid = 1.0;
   int last_kk = 0;
+  k_set<<<1, 1, 0, st>>>(S + 0, beta_b);
+  // One Arnoldi step (operator, GCRO projection, CGS2, Givens) as device work only: it is
+  // captured once per k as a CUDA graph and replayed (launch-bound at small N), unless
+  // profiling events, deflation, sharding or BPQN_GRAPHS=0 make it non-capturable.
+  auto step_launches = [&](int k, cudaStream_t ss) {
+    double* vk = g.V.p + (size_t)k * ld;
+    double* w = g.V.p + (size_t)(k + 1) * ld;
+    if (pre) {  // right preconditioning: w = A_op M^-1 v_k
+      launch_self_gemm(g, g.Minv.p, vk, nullptr, nullptr, g.tmp2.p, 0, ss);
+      apply_operator(g, nullptr, g.tmp2.p, nullptr, g.E_A.p, w, ss);
+    } else {
+      apply_operator(g, nullptr, vk, nullptr, g.E_A.p, w, ss);
+    }
+    if (kd > 0) {  // (I - C C^T) A~ v_k ; column k of B = C^T A~ v_k
+      double* Bk = S + L.Bm + (size_t)k * KD_MAX;
+      k_mdot<<<dim3(nbx, kd), GT, 0, ss>>>(g.def_C.p, n, w, n, g.red.p, nbx);
+      k_reduce_rows<<<kd, 256, 0, ss>>>(g.red.p, nbx, Bk, 0);
+      k_mupdate<<<nbx, GT, 0, ss>>>(g.def_C.p, n, kd, Bk, w, n, nullptr, nbx);
+      g.prof.launches += 3;
+    }
+    // CGS2
+    k_mdot<<<dim3(nbx, k + 1), GT, 0, ss>>>(g.V.p, ld, w, n, g.red.p, nbx);
+    k_reduce_rows<<<k + 1, 256, 0, ss>>>(g.red.p, nbx, S + L.h1, 0);
+    k_mupdate<<<nbx, GT, 0, ss>>>(g.V.p, ld, k + 1, S + L.h1, w, n, nullptr, nbx);
+    k_mdot<<<dim3(nbx, k + 1), GT, 0, ss>>>(g.V.p, ld, w, n, g.red.p, nbx);
+    k_reduce_rows<<<k + 1, 256, 0, ss>>>(g.red.p, nbx, S + L.h2, 0);
+    k_mupdate<<<nbx, GT, 0, ss>>>(g.V.p, ld, k + 1, S + L.h2, w, n, g.red.p, nbx);
+    k_reduce_rows<<<1, 256, 0, ss>>>(g.red.p, nbx, S + 2, 0);
+    k_givens<<<1, 32, 0, ss>>>(S, L, k);
+    k_scale<<<blocks_vec, 256, 0, ss>>>(w, w, n, S + 3, 1);
+    BPQN_CHECK_LAUNCH();
+    g.prof.launches += 9;
+  };
+  GraphCache& GC = g.gm_graphs;
+  const bool use_graphs = graphs_enabled() && GC.ok && !g.prof.events && kd == 0 && g.shard_world == 1 &&
+                          !g.overlap_k2;
+  if (use_graphs) GC.validate(g.V.p, g.scal.p, g.red.p, g.tmp2.p, g.packed.p, m, pre);
+  auto run_step = [&](int k) {
+    if (!use_graphs || !GC.ok) {
+      step_launches(k, st);
+      return;
+    }
+    if (!GC.warm[k]) {  // first execution uncaptured (first-use allocations, attribute setup)
+      step_launches(k, st);
+      GC.warm[k] = 1;
+      return;
+    }
+    if (!GC.exec[k]) {
+      if (!GC.cap) BPQN_CUDA(cudaStreamCreateWithFlags(&GC.cap, cudaStreamNonBlocking));
+      const long long l0 = g.prof.launches;
+      cudaGraph_t graph = nullptr;
+      bool ok = cudaStreamBeginCapture(GC.cap, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+      if (ok) {
+        try {
+          step_launches(k, GC.cap);
+        } catch (...) {
+          ok = false;
+        }
+        ok = (cudaStreamEndCapture(GC.cap, &graph) == cudaSuccess) && ok && graph;
+      }
+      if (ok) ok = cudaGraphInstantiate(&GC.exec[k], graph, 0) == cudaSuccess;
+      if (graph) cudaGraphDestroy(graph);
+      if (!ok) {  // not capturable here: run uncaptured from now on
+        cudaGetLastError();
+        GC.ok = false;
+        GC.exec[k] = nullptr;
+        step_launches(k, st);
+        return;
+      }
+      GC.launches[k] = g.prof.launches - l0;
+      g.prof.launches = l0;
+    }
+    BPQN_CUDA(cudaGraphLaunch(GC.exec[k], st));
+    g.prof.launches += GC.launches[k];
+  };
   for (;;) {
     double beta;
     if (first) {
@@ -480,34 +565,8 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
     int kk = 0;
     bool done = false;
     for (int k = 0; k < m; ++k) {
-      double* vk = g.V.p + (size_t)k * ld;
-      double* w = g.V.p + (size_t)(k + 1) * ld;
-      if (pre) {  // right preconditioning: w = A_op M^-1 v_k
-        launch_self_gemm(g, g.Minv.p, vk, nullptr, nullptr, g.tmp2.p, 0, st);
-        apply_operator(g, nullptr, g.tmp2.p, nullptr, g.E_A.p, w, st);
-      } else {
-        apply_operator(g, nullptr, vk, nullptr, g.E_A.p, w, st);
-      }
+      run_step(k);
       stt.applies++;
-      if (kd > 0) {  // (I - C C^T) A~ v_k ; column k of B = C^T A~ v_k
-        double* Bk = S + L.Bm + (size_t)k * KD_MAX;
-        k_mdot<<<dim3(nbx, kd), GT, 0, st>>>(g.def_C.p, n, w, n, g.red.p, nbx);
-        k_reduce_rows<<<kd, 256, 0, st>>>(g.red.p, nbx, Bk, 0);
-        k_mupdate<<<nbx, GT, 0, st>>>(g.def_C.p, n, kd, Bk, w, n, nullptr, nbx);
-        g.prof.launches += 3;
-      }
-      // CGS2
-      k_mdot<<<dim3(nbx, k + 1), GT, 0, st>>>(g.V.p, ld, w, n, g.red.p, nbx);
-      k_reduce_rows<<<k + 1, 256, 0, st>>>(g.red.p, nbx, S + L.h1, 0);
-      k_mupdate<<<nbx, GT, 0, st>>>(g.V.p, ld, k + 1, S + L.h1, w, n, nullptr, nbx);
-      k_mdot<<<dim3(nbx, k + 1), GT, 0, st>>>(g.V.p, ld, w, n, g.red.p, nbx);
-      k_reduce_rows<<<k + 1, 256, 0, st>>>(g.red.p, nbx, S + L.h2, 0);
-      k_mupdate<<<nbx, GT, 0, st>>>(g.V.p, ld, k + 1, S + L.h2, w, n, g.red.p, nbx);
-      k_reduce_rows<<<1, 256, 0, st>>>(g.red.p, nbx, S + 2, 0);
-      k_givens<<<1, 32, 0, st>>>(S, L, k, beta_b);
-      k_scale<<<blocks_vec, 256, 0, st>>>(w, w, n, S + 3, 1);
-      BPQN_CHECK_LAUNCH();
-      g.prof.launches += 9;
       kk = k + 1;
       stt.iters++;
       resid = read_scalar(g, S + 1, st);
