@@ -477,3 +477,33 @@ def test_plain_c_client(bp):
     assert abs(np.linalg.norm(w.cpu().numpy()) - out["w_norm"]) <= 1e-9 * out["w_norm"]
     assert out["hi_mvps"] == out["lcp_iterations"] + 1 + out["lcp_iterations"] // 20
     assert out["kkt_abs"] <= 1e-10
+
+
+# ------------------------------------------------------------------ full-size properties (c4)
+def _rot_z(t):
+    c, s = np.cos(t), np.sin(t)
+    return np.array([[c, -s, 0.0], [s, c, 0.0], [0.0, 0.0, 1.0]])
+
+
+@pytest.mark.parametrize("kind", ["translation", "rotation_pi_over_p"])
+def test_lcp_mvp_c4_exact_covariance(bp, kind):
+    """At full c4 size, in the bench's launch configuration: the discrete operator is exactly
+    covariant under translations and under the rotation by pi/p about z, which maps every
+    sphere's grid onto itself -- so w = D^T M D lambda (a scalar per contact) is
+    unchanged to GMRES tolerance.  No oracle needed: a property at any size."""
+    from synth import lambda_test, make_config
+    cfg = make_config(4)
+    C = cfg["centers"]
+    if kind == "translation":
+        C2 = C + np.array([3.7, -1.1, 0.4])
+    else:
+        C2 = C @ _rot_z(np.pi / cfg["p"]).T
+    gm = bp.default_gmres_opts(tol=1e-12)
+    ws = []
+    for cc in (C, C2):
+        g = bp.Geometry(cc, cfg["p"])
+        bp.contacts(g, 0.1)
+        w, st = bp.lcp_mvp(g, T(lambda_test(4, g.nc, 0)), gmres=gm)
+        ws.append(w.cpu().numpy())
+        del g
+    assert rel(ws[1], ws[0]) <= 1e-10
