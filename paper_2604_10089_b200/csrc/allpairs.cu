@@ -663,8 +663,8 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
 }
 
-// Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps x 4 targets/lane
-// at 1 CTA/SM for N >= 6e4 (c4: D 16.0, S 16.05, S+D 23.95 ms), 8 x 3 below.
+// Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps at 1 CTA/SM with
+// 5 (D), 6 (S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 15.79, S 15.85, S+D 23.95 ms), 8 x 3 below.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -678,7 +678,7 @@ static int k1_cfg() {
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
   int c = k1_cfg();
-  if (c < 0) c = g.n >= 60000 ? 4 : 3;
+  if (c < 0) c = g.n >= 60000 ? (MODE == MODE_D ? 14 : (MODE == MODE_S ? 15 : 4)) : 3;
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
@@ -693,6 +693,9 @@ static void launch_sym(Geom& g, double* out, cudaStream_t st) {
     case 11: launch_sym_cfg<MODE, 4, 4, 2>(g, out, st); break;
     case 12: launch_sym_cfg<MODE, 12, 4, 1>(g, out, st); break;
     case 13: launch_sym_cfg<MODE, 12, 4, 1, 1>(g, out, st); break;
+    case 14: launch_sym_cfg<MODE, 8, 5, 1>(g, out, st); break;
+    case 15: launch_sym_cfg<MODE, 8, 6, 1>(g, out, st); break;
+    case 16: launch_sym_cfg<MODE, 4, 6, 2>(g, out, st); break;
     default: launch_sym_cfg<MODE, 8, 2, 2>(g, out, st); break;
   }
 }
