@@ -353,13 +353,21 @@ __global__ void k1_pack_sym(int mode, int N, int npad, const double* __restrict_
 // h[r][0|1] = (|x - c_m|^2 - a^2)/(2a) for the group's first / second source sphere,
 // sources with in-tile index >= jb belong to the second; Hg[slot * K1_TS + j] =
 // (|y_j - c_t|^2 - a^2)/(2a) for the block's target spheres (reverse r.n_t).
-template <int MODE, int R, bool SYM, int UNR>
+// SYM: off-diagonal tile, never a target's own node (rho > 0 for every pair, so the seed
+// needs no zero mask: padded targets occur only in the last block, whose tiles are all
+// diagonal).  MIXED: the group straddles the tile's sphere boundary (per-pair select of h);
+// otherwise h is chosen once per group (always so at p = 16, where Nq = 17 x 32).
+template <int MODE, int R, bool SYM, bool MIXED, int UNR>
 __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const double (&tg)[R][TgtN<MODE>::n],
                                          const double (&h)[R][2], int jl0, int jb, double inv2a,
                                          const double* __restrict__ Hg, const int (&slot)[R], double (&acc)[R][3],
                                          int lane, double& as0, double& as1, double& as2) {
   constexpr int REC = RecS<MODE>::n;
   constexpr int QO = MODE == MODE_D ? 3 : 6;  // offset of q~ in a source record
+  double hu[R];
+  const bool all_second = jl0 >= jb;
+#pragma unroll
+  for (int r = 0; r < R; ++r) hu[r] = all_second ? h[r][1] : h[r][0];
 #pragma unroll UNR
   for (int k = 0; k < 32; ++k) {
     const int j = (lane + k) & 31;
@@ -376,7 +384,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
     for (int r = 0; r < R; ++r) {
       const double r0 = tg[r][0] - sc[0], r1 = tg[r][1] - sc[1], r2 = tg[r][2] - sc[2];
       const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
-      const double y = seed_or_zero(rr);
+      const double y = SYM ? rsq_seed(rr) : seed_or_zero(rr);
       const double y2 = y * y;
       const double e = fma(-rr, y2, 1.0);
       if (MODE == MODE_S) {
@@ -395,7 +403,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           as2 = fma(tg[r][5], s, fma(r2, tb, as2));
         }
       } else {
-        const double hm = second ? h[r][1] : h[r][0];
+        const double hm = MIXED ? (second ? h[r][1] : h[r][0]) : hu[r];
         const double rn = fma(rr, -inv2a, hm);  // r . n_y on the source sphere
         const double rq = fma(r2, sc[QO + 2], fma(r1, sc[QO + 1], r0 * sc[QO]));
         double s, s3, s5;
@@ -560,10 +568,14 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     for (int grp = 0; grp < K1_TS / 32; ++grp) {
       const double* gr = ring[buf] + grp * 32 * REC;
       double as0 = 0.0, as1 = 0.0, as2 = 0.0;
+      const bool mixed = grp * 32 < jb && grp * 32 + 32 > jb;
       if (diag) {
-        k1_group<MODE, R, false, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, false, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
       } else {
-        k1_group<MODE, R, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
+        if (mixed)
+          k1_group<MODE, R, true, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
+        else
+          k1_group<MODE, R, true, false, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
         double* rw = red[par][warp] + (grp * 32 + lane) * 3;
         rw[0] = as0;
         rw[1] = as1;
@@ -664,7 +676,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
 }
 
 // Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps at 1 CTA/SM with
-// 5 (D), 6 (S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 15.79, S 15.85, S+D 23.95 ms), 8 x 3 below.
+// 5 (D, S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 15.16, S 15.65, S+D 23.09 ms), 8 x 3 below.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -678,7 +690,7 @@ static int k1_cfg() {
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
   int c = k1_cfg();
-  if (c < 0) c = g.n >= 60000 ? (MODE == MODE_D ? 14 : (MODE == MODE_S ? 15 : 4)) : 3;
+  if (c < 0) c = g.n >= 60000 ? (MODE == MODE_SD ? 4 : 14) : 3;
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
