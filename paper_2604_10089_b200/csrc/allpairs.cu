@@ -132,6 +132,12 @@ __device__ __forceinline__ double rsq_seed(double x) {
   return y;
 }
 
+__device__ __forceinline__ double lds_f64(unsigned addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
 // seed y ~ rr^-1/2 with rr == 0 -> y = 0 (integer select, no FP64 compare)
 __device__ __forceinline__ double seed_or_zero(double rr) {
   const double y = rsq_seed(rr);
@@ -351,7 +357,7 @@ __global__ void k1_pack_sym(int mode, int N, int npad, const double* __restrict_
 
 // One 32-source group.  tg[r] = {x(3), [f~(3)], [q~(3)]} (see TgtN / k1_sym);
 // h[r][0|1] = (|x - c_m|^2 - a^2)/(2a) for the group's first / second source sphere,
-// sources with in-tile index >= jb belong to the second; Hg[slot * K1_TS + j] =
+// sources with in-tile index >= jb belong to the second; Hg[slot * 2 K1_TS + 64 g + u] (u < 64) =
 // (|y_j - c_t|^2 - a^2)/(2a) for the block's target spheres (reverse r.n_t).
 // SYM: off-diagonal tile, never a target's own node (rho > 0 for every pair, so the seed
 // needs no zero mask: padded targets occur only in the last block, whose tiles are all
@@ -365,9 +371,13 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
   constexpr int REC = RecS<MODE>::n;
   constexpr int QO = MODE == MODE_D ? 3 : 6;  // offset of q~ in a source record
   double hu[R];
+  unsigned hb[R];  // shared address of this lane's window of the doubled H row: H(y_{(lane + k) & 31}) at hb + 8k
   const bool all_second = jl0 >= jb;
 #pragma unroll
-  for (int r = 0; r < R; ++r) hu[r] = all_second ? h[r][1] : h[r][0];
+  for (int r = 0; r < R; ++r) {
+    hu[r] = all_second ? h[r][1] : h[r][0];
+    hb[r] = smem_addr(Hg + slot[r] * (2 * K1_TS) + (jl0 >> 5) * 64 + lane);
+  }
 #pragma unroll UNR
   for (int k = 0; k < 32; ++k) {
     const int j = (lane + k) & 31;
@@ -422,7 +432,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           acc[r][1] = fma(r1, tf, acc[r][1]);
           acc[r][2] = fma(r2, tf, acc[r][2]);
           if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5, r.n_i = (rho^2 - H)/(2a)
-            const double rn2 = fma(rr, inv2a, -Hg[slot[r] * K1_TS + jl0 + j]);
+            const double rn2 = fma(rr, inv2a, -lds_f64(hb[r] + 8 * k));
             const double rq2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
             const double tb = (rn2 * rq2) * s5;
             as0 = fma(-r0, tb, as0);
@@ -436,7 +446,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
           acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
           if (SYM) {
-            const double rn2 = fma(rr, inv2a, -Hg[slot[r] * K1_TS + jl0 + j]);
+            const double rn2 = fma(rr, inv2a, -lds_f64(hb[r] + 8 * k));
             const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
             const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
             const double tb = fma(rf2, s3, -((rn2 * rq2) * s5));
@@ -470,7 +480,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   double (*red)[KS_W][K1_TS * 3] =
       reinterpret_cast<double (*)[KS_W][K1_TS * 3]>(k1_dyn + NS * TILE_DBL);             // [2][W][192]
   double* cs = k1_dyn + NS * TILE_DBL + 2 * KS_W * K1_TS * 3;                             // centres [Np][3]
-  double* Hs = cs + (MODE == MODE_S ? 0 : 3 * P.np);                                      // [slots][K1_TS]
+  double* Hs = cs + (MODE == MODE_S ? 0 : 3 * P.np);                                      // [slots][2 K1_TS]
   __shared__ __align__(8) uint64_t full[NS];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -554,13 +564,17 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     }
     const bool diag = t_cur < (b_cur + 1) * TPB;
     mbar_wait(&full[buf], parity);
-    if (MODE != MODE_S && !diag) {  // H[slot][j] = (|y_j - c_slot|^2 - a^2)/(2a) for this tile
+    if (MODE != MODE_S && !diag) {  // H[slot][j] = (|y_j - c_slot|^2 - a^2)/(2a) for this tile,
+      // each 32-source group stored twice in a row so that lane + k indexes it without a wrap
       for (int e = tid; e < nslot * K1_TS; e += blockDim.x) {
         const int sl = e / K1_TS, j = e - sl * K1_TS;
         const double* y = ring[buf] + j * REC;
         const double* c = cs + 3 * (fs + sl);
         const double d0 = y[0] - c[0], d1 = y[1] - c[1], d2 = y[2] - c[2];
-        Hs[e] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+        const double H = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+        double* row = Hs + sl * (2 * K1_TS) + (j >> 5) * 64 + (j & 31);
+        row[0] = H;
+        row[32] = H;
       }
       __syncthreads();
     }
@@ -648,7 +662,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   for (int b = 0; b < P.nb; ++b) P.units += P.nt - b * (KS_B / K1_TS);
   const int nslot_max = KS_B / g.nq + 2;
   const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
-                    (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * K1_TS)) * 8;
+                    (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * 2 * K1_TS)) * 8;
   // per instantiation: the opt-in smem limit only grows; occupancy cached per smem size
   // (hi and lo fidelity handles alternate in Bi-PQN with different table sizes)
   static std::mutex mu;
@@ -676,7 +690,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
 }
 
 // Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps at 1 CTA/SM with
-// 5 (D, S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 15.16, S 15.65, S+D 23.09 ms), 8 x 3 below.
+// 5 (D, S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 14.81, S 15.65, S+D 22.60 ms), 8 x 3 below.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
