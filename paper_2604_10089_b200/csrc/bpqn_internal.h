@@ -140,12 +140,20 @@ struct Geom {
   DBuf<double> E_A;   // E_L - I/2 + Pi_R (GMRES operator)
   DBuf<double> Minv;  // inverse of the same-sphere block D_self - I/2 + Pi_R (block-Jacobi, K4)
 
-  // near incidences (sorted by target); matrices [n_inc][3][3nq] per kernel kind
+  // near incidences (target i, source sphere m), sorted by (i, m)
   long long n_inc = 0;
   DBuf<int> inc_t, inc_m;        // [n_inc]
   DBuf<int> nt_list, nt_ptr;     // near targets (unique) and CSR into incidences
   int n_near_targets = 0;
-  DBuf<double> M_S, M_D;         // [n_inc][3][3nq]
+  // K2 order: the same incidences sorted by (m, i), cut into chunks of <= K2_CHUNK positions
+  // of one source sphere; refined-rule tensors in SH-coefficient space, symmetric (a, c)
+  // packed xx xy xz yy yz zz: u_i[a] += sum_c sum_b T[pos][sym(a,c)][b] coef_m[b][c]
+  DBuf<int> cm_t, cm_m;          // [n_inc] target node / source sphere per position
+  DBuf<int> chunks;              // [n_chunks][2] position ranges
+  int n_chunks = 0;
+  DBuf<double> T_S, T_D;         // [n_inc][6][nb]
+  DBuf<double> coef;             // [2][np][nb][3] SH coefficients of the densities (K2 workspace)
+  DBuf<double> analysis_t;       // [nq][nb] transpose of analysis
 
   // contacts
   int nc = 0, nc_cap = 0;
@@ -193,6 +201,7 @@ struct Geom {
 // ---------------------------------------------------------------- kernels / passes
 enum Mode { MODE_S = 0, MODE_D = 1, MODE_SD = 2 };
 
+constexpr int K2_CHUNK = 64;  // incidence positions per K2 block
 void precompute(Geom& g, cudaStream_t st, bool with_self);
 void invert_in_place(double* A, int n, cudaStream_t st);  // Gauss-Jordan, partial pivoting  // self E matrices + near matrices
 

@@ -138,6 +138,24 @@ static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
   upload_i(g->inc_m, im, st);
   upload_i(g->nt_list, ntl, st);
   upload_i(g->nt_ptr, ntp, st);
+  // K2 order: by (source sphere, target), chunks of one sphere
+  std::vector<std::pair<int, int>> bym(inc.size());
+  for (size_t k = 0; k < inc.size(); ++k) bym[k] = {inc[k].second, inc[k].first};
+  std::sort(bym.begin(), bym.end());
+  std::vector<int> ct(inc.size()), cm(inc.size()), ch;
+  for (size_t k = 0; k < bym.size(); ++k) {
+    cm[k] = bym[k].first;
+    ct[k] = bym[k].second;
+    if (k == 0 || bym[k].first != bym[k - 1].first || (int)k - ch.back() == K2_CHUNK) {
+      if (k) ch.push_back((int)k);
+      ch.push_back((int)k);
+    }
+  }
+  if (!bym.empty()) ch.push_back((int)bym.size());
+  g->n_chunks = (int)ch.size() / 2;
+  upload_i(g->cm_t, ct, st);
+  upload_i(g->cm_m, cm, st);
+  upload_i(g->chunks, ch, st);
   BPQN_CUDA(cudaStreamSynchronize(st));  // host staging vectors go out of scope
 }
 
@@ -323,7 +341,7 @@ int bpqn_geometry_info(bpqn_geom_t g, int* n_nodes, int* nq, long long* n_incide
     if (device_bytes) {
       long long b = 0;
       b += g->X.bytes() + g->src.bytes() + g->analysis.bytes() + g->E_S.bytes() + g->E_L.bytes() + g->E_A.bytes();
-      b += g->M_S.bytes() + g->M_D.bytes() + g->V.bytes() + g->far.bytes() * 6;
+      b += g->T_S.bytes() + g->T_D.bytes() + g->V.bytes() + g->far.bytes() * 6;
       *device_bytes = b;
     }
     return BPQN_OK;

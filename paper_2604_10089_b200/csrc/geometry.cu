@@ -7,8 +7,9 @@
 //  * the per-sphere self operators E_S, E_L, E_A  (rotated singular grid, R5/R6;
 //    computed for one target per polar ring and expanded by the exact z-rotation
 //    symmetry of the grid),
-//  * the near-incidence correction matrices M_S, M_D (refined sinh-graded polar
-//    rule minus the coarse rule, R8), one [3][3nq] block per (target, sphere).
+//  * the near-incidence refined tensors T_S, T_D (sinh-graded polar rule, R8) in
+//    SH-coefficient space, one [6][nb] block per (target, sphere); K2 applies them to
+//    the density's SH coefficients and subtracts the coarse rule on the fly.
 // The paper names none of this (PAPER.md P:425-426 only gives the dof count and
 // cost); it is the discretisation frozen in DESIGN.md, implemented independently
 // of the CPU oracle.
@@ -212,6 +213,14 @@ __device__ inline void rot_apply(const double R[9], double x, double y, double z
   oz = R[6] * x + R[7] * y + R[8] * z;
 }
 
+// out[c][r] = in[r][c], in [rows][cols]
+__global__ void k_transpose(const double* in, int rows, int cols, double* out) {
+  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (size_t)rows * cols) return;
+  const size_t r = e / cols, c = e - r * cols;
+  out[c * rows + r] = in[e];
+}
+
 __global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
   extern __shared__ double sm[];
   const int prob = blockIdx.x;
@@ -383,7 +392,18 @@ __global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
     }
   }
   __syncthreads();
-  // phase C: rows over source nodes j
+  if (P.kind == 1) {  // near incidence: the refined tensors in SH-coefficient space (K2 applies them),
+    // rows padded to an even length nbp (16-byte loads in K2) with zeros
+    const int nbp = (nb + 1) & ~1;
+    const size_t o = (size_t)prob * 6 * nbp;
+    for (int e = threadIdx.x; e < 6 * nbp; e += QT) {
+      const int q = e / nbp, b = e - q * nbp;
+      P.outD[o + e] = b < nb ? Tm[(6 + q) * nb + b] : 0.0;
+      if (P.want_s) P.outS[o + e] = b < nb ? Tm[q * nb + b] : 0.0;
+    }
+    return;
+  }
+  // phase C (self rings): rows over source nodes j
   const int sym[9] = {0, 1, 2, 1, 3, 4, 2, 4, 5};  // (a,c) -> packed symmetric index
   double* oS = P.outS + (size_t)prob * 9 * nq;
   double* oD = P.outD + (size_t)prob * 9 * nq;
@@ -610,6 +630,9 @@ void precompute(Geom& g, cudaStream_t st, bool with_self) {
   g.analysis.alloc((size_t)nb * nq);
   k_analysis<<<(nq + 127) / 128, 128, 0, st>>>(p, nq, g.xi_d.p, d_wunit.p, T, Yn.p, g.analysis.p, nb);
   BPQN_CHECK_LAUNCH();
+  g.analysis_t.alloc((size_t)nq * nb);
+  k_transpose<<<(unsigned)(((size_t)nb * nq + 255) / 256), 256, 0, st>>>(g.analysis.p, nb, nq, g.analysis_t.p);
+  BPQN_CHECK_LAUNCH();
   BPQN_CUDA(cudaStreamSynchronize(st));  // d_wunit / Yn are released at the end of this scope
   }
 
@@ -659,24 +682,24 @@ void precompute(Geom& g, cudaStream_t st, bool with_self) {
   invert_in_place(g.Minv.p, 3 * nq, st);
   }
 
-  // near incidences
-  g.M_D.release();
-  g.M_S.release();
+  // near incidences, in K2 order (by source sphere)
+  g.T_D.release();
+  g.T_S.release();
   if (g.n_inc > 0) {
-    size_t per = (size_t)9 * nq;
-    g.M_D.alloc((size_t)g.n_inc * per);
-    if (g.single_layer) g.M_S.alloc((size_t)g.n_inc * per);
-    P.kind = 1; P.inc_t = g.inc_t.p; P.inc_m = g.inc_m.p;
+    size_t per = (size_t)6 * ((nb + 1) & ~1);
+    g.T_D.alloc((size_t)g.n_inc * per);
+    if (g.single_layer) g.T_S.alloc((size_t)g.n_inc * per);
+    P.kind = 1; P.inc_t = g.cm_t.p; P.inc_m = g.cm_m.p;
     P.want_s = g.single_layer ? 1 : 0;
     // batch to keep grids modest
     const long long batch = 65535;
     for (long long b0 = 0; b0 < g.n_inc; b0 += batch) {
       long long nbt = std::min(batch, g.n_inc - b0);
       QuadParams Q = P;
-      Q.inc_t = g.inc_t.p + b0;
-      Q.inc_m = g.inc_m.p + b0;
-      Q.outD = g.M_D.p + b0 * per;
-      Q.outS = g.single_layer ? g.M_S.p + b0 * per : g.M_D.p + b0 * per;  // unused when !want_s
+      Q.inc_t = g.cm_t.p + b0;
+      Q.inc_m = g.cm_m.p + b0;
+      Q.outD = g.T_D.p + b0 * per;
+      Q.outS = g.single_layer ? g.T_S.p + b0 * per : g.T_D.p + b0 * per;  // unused when !want_s
       k_quad_rows<<<(unsigned)nbt, QT, smem, st>>>(Q);
       BPQN_CHECK_LAUNCH();
     }

@@ -7,76 +7,258 @@
 // black box).  Kernels written for sm_100a; no tcgen05 kind supports f64, so K3
 // uses the DMMA path (measured 37.2 TFLOP/s on B200, same as DFMA).
 #include <algorithm>
+#include <atomic>
 
 #include "bpqn_internal.h"
 
 namespace bpqn {
 
 // ------------------------------------------------------------------ K2
-// One warp per (near target, component a): sum over the target's incidences of
-// dot(M[inc][a][:], sigma_m[:]) (length 3nq, even).  The correction rows stream from
-// HBM exactly once per apply (16-byte streaming loads, 4 in flight per lane); the
-// densities are L2-resident.  Deterministic, no atomics.
-__device__ __forceinline__ double dot_row(const double* __restrict__ row, const double* __restrict__ sg, int len2,
-                                          int lane, double acc) {
-  const double2* r2 = reinterpret_cast<const double2*>(row);
-  const double2* s2 = reinterpret_cast<const double2*>(sg);
-  int c = lane;
-  for (; c + 96 < len2; c += 128) {
-    const double2 a0 = __ldcs(r2 + c), a1 = __ldcs(r2 + c + 32), a2 = __ldcs(r2 + c + 64), a3 = __ldcs(r2 + c + 96);
-    const double2 b0 = __ldg(s2 + c), b1 = __ldg(s2 + c + 32), b2 = __ldg(s2 + c + 64), b3 = __ldg(s2 + c + 96);
-    acc = fma(a0.x, b0.x, acc);
-    acc = fma(a0.y, b0.y, acc);
-    acc = fma(a1.x, b1.x, acc);
-    acc = fma(a1.y, b1.y, acc);
-    acc = fma(a2.x, b2.x, acc);
-    acc = fma(a2.y, b2.y, acc);
-    acc = fma(a3.x, b3.x, acc);
-    acc = fma(a3.y, b3.y, acc);
+// Near-incidence correction, per incidence (target x_i, source sphere m):
+//   u_i += sum_c sum_b T[sym(a,c)][b] coef_m[b][c]          refined rule (R8), SH space
+//        - sum_{j in m} w_j K(x_i, y_j) sigma_j               the coarse pairs K1 added
+// coef_m = analysis sigma_m (the Pi_p projection's SH coefficients, R7).  Blocks take
+// chunks of incidences of one source sphere (K2 order, bpqn_internal.h), stage that
+// sphere's nodes, weighted densities and coefficients in shared memory, and stream the
+// [6][nb] tensors from HBM once per application (16-byte streaming loads); the coarse
+// subtraction is recomputed from the staged nodes (~30 flops per pair, FP64 pipe).
+// Each incidence adds its 3 values to the target with fp64 atomics (<= a few per target).
+
+// coef[m][b][c] = sum_j A[b][j] sigma[m][j][c] (A row-major [nb][nq]); rows b in [nb, nbp) are zero.
+// A small tiled GEMM: block = 32 rows of A x 8 spheres; its 256 threads form 4 groups that take
+// interleaved slabs of 16 nodes (each thread 4 rows x 1 sphere x 3 components), then add their
+// partial sums through shared memory; gridDim.z blocks split the nodes and add atomically.  A is
+// read once per 8 spheres (L2 traffic nb nq Np bytes).
+constexpr int KC_BM = 32, KC_BS = 8, KC_JT = 16, KC_G = 4;
+__global__ void __launch_bounds__(256) k2_coef(int nq, int nb, int nbp, int np, const double* __restrict__ A,
+                                               const double* __restrict__ sig, double* __restrict__ coef) {
+  constexpr int NA = KC_G * KC_BM * (KC_JT + 1), NS = KC_G * KC_BS * KC_JT * 3;
+  static_assert(NA + NS >= KC_G * 64 * 12, "reduction buffer");
+  __shared__ double sm[NA + NS];
+  double (*As)[KC_BM][KC_JT + 1] = reinterpret_cast<double (*)[KC_BM][KC_JT + 1]>(sm);
+  double (*Ss)[KC_BS][KC_JT * 3] = reinterpret_cast<double (*)[KC_BS][KC_JT * 3]>(sm + NA);
+  const int b0 = blockIdx.x * KC_BM, s0 = blockIdx.y * KC_BS;
+  const int tid = threadIdx.x, grp = tid >> 6, t = tid & 63, tr = t & 7, ts = t >> 3;
+  double c[4][3];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) c[u][0] = c[u][1] = c[u][2] = 0.0;
+  const int jlen = (nq + gridDim.z - 1) / gridDim.z;  // this block's node range [ja, je)
+  const int ja = blockIdx.z * jlen, je = min(nq, ja + jlen);
+  for (int jr = ja; jr < je; jr += KC_G * KC_JT) {
+    // every thread helps stage all KC_G slabs of this round
+    for (int e = tid; e < KC_G * KC_BM * KC_JT; e += 256) {
+      const int g = e / (KC_BM * KC_JT), rem = e - g * (KC_BM * KC_JT), r = rem / KC_JT, jj = rem - r * KC_JT;
+      const int j = jr + g * KC_JT + jj;
+      As[g][r][jj] = (b0 + r < nb && j < je) ? A[(size_t)(b0 + r) * nq + j] : 0.0;
+    }
+    for (int e = tid; e < KC_G * KC_BS * KC_JT * 3; e += 256) {
+      const int g = e / (KC_BS * KC_JT * 3), rem = e - g * (KC_BS * KC_JT * 3), sp = rem / (KC_JT * 3),
+                k = rem - sp * (KC_JT * 3);
+      const int j = jr + g * KC_JT + k / 3;
+      Ss[g][sp][k] = (s0 + sp < np && j < je) ? sig[((size_t)(s0 + sp) * nq + jr + g * KC_JT) * 3 + k] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int jj = 0; jj < KC_JT; ++jj) {
+      const double q0 = Ss[grp][ts][3 * jj], q1 = Ss[grp][ts][3 * jj + 1], q2 = Ss[grp][ts][3 * jj + 2];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double av = As[grp][4 * tr + u][jj];
+        c[u][0] = fma(av, q0, c[u][0]);
+        c[u][1] = fma(av, q1, c[u][1]);
+        c[u][2] = fma(av, q2, c[u][2]);
+      }
+    }
+    __syncthreads();
   }
-  for (; c < len2; c += 32) {
-    const double2 a0 = __ldcs(r2 + c), b0 = __ldg(s2 + c);
-    acc = fma(a0.x, b0.x, acc);
-    acc = fma(a0.y, b0.y, acc);
+  // reduce the KC_G groups' partial sums (the staging buffer reused as [KC_G][64 threads][12])
+  double* red = sm;
+#pragma unroll
+  for (int u = 0; u < 4; ++u)
+#pragma unroll
+    for (int k = 0; k < 3; ++k) red[(grp * 64 + t) * 12 + 3 * u + k] = c[u][k];
+  __syncthreads();
+  if (grp != 0 || s0 + ts >= np) return;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int bb = b0 + 4 * tr + u;
+    if (bb >= nbp) continue;
+    double* o = coef + ((size_t)(s0 + ts) * nbp + bb) * 3;
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      double v = 0.0;
+#pragma unroll
+      for (int g = 0; g < KC_G; ++g) v += red[(g * 64 + t) * 12 + 3 * u + k];
+      if (gridDim.z == 1) o[k] = v;
+      else atomicAdd(o + k, v);  // node ranges split over gridDim.z blocks (coef zeroed)
+    }
   }
-  return acc;
 }
 
-__global__ void k2_near(int n_targets, const int* nt_list, const int* nt_ptr, const int* inc_m, int nq,
-                        const double* MS, const double* sigS, const double* MD, const double* sigD, double* out) {
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (warp >= 3 * n_targets) return;
-  const int tix = warp / 3, a = warp - 3 * tix;
-  const int i = nt_list[tix];
-  const size_t len = 3 * (size_t)nq;
-  const int len2 = (int)(len / 2);
-  double acc = 0.0;
-  for (int k = nt_ptr[tix]; k < nt_ptr[tix + 1]; ++k) {
-    const int m = inc_m[k];
-    const size_t base = ((size_t)k * 3 + a) * len;
-    if (MD) acc = dot_row(MD + base, sigD + (size_t)m * len, len2, lane, acc);
-    if (MS) acc = dot_row(MS + base, sigS + (size_t)m * len, len2, lane, acc);
-  }
+struct K2Params {
+  const int *chunks, *cm_t, *cm_m;
+  const double *X, *src;         // node positions [N][3]; records {y, w, n, 0} [N][8]
+  const double* centers;         // [np][3]
+  double a;
+  const double *TS, *TD;         // [n_inc][6][nbp] or null (nbp = nb rounded up to even)
+  const double *coefS, *coefD;   // [np][nbp][3]
+  const double *sigS, *sigD;     // [N][3]
+  int nq, nbp, t0, t1;           // targets outside [t0, t1) are skipped (sharding)
+  double cS, cD;                 // 1/(8 pi mu), -3/(4 pi)
+  double* out;                   // [N][3], zeroed
+};
+
+// u[a] += sum_c T[sym(a,c)] c[c] over the packed symmetric rows, streamed in b pairs
+__device__ __forceinline__ void k2_refined(const double* __restrict__ T, const double* __restrict__ cf, int nbp,
+                                           int lane, double& u0, double& u1, double& u2) {
+  const double2* T2 = reinterpret_cast<const double2*>(T);
+  const int nb2 = nbp >> 1;
+#pragma unroll 2
+  for (int b2 = lane; b2 < nb2; b2 += 32) {
+    double2 t[6];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) out[3 * (size_t)i + a] = acc;
+    for (int q = 0; q < 6; ++q) t[q] = __ldcs(T2 + q * nb2 + b2);
+    const double* c = cf + 6 * b2;  // coefficients of b = 2 b2 and 2 b2 + 1
+    u0 = fma(t[0].x, c[0], fma(t[1].x, c[1], fma(t[2].x, c[2], u0)));
+    u1 = fma(t[1].x, c[0], fma(t[3].x, c[1], fma(t[4].x, c[2], u1)));
+    u2 = fma(t[2].x, c[0], fma(t[4].x, c[1], fma(t[5].x, c[2], u2)));
+    u0 = fma(t[0].y, c[3], fma(t[1].y, c[4], fma(t[2].y, c[5], u0)));
+    u1 = fma(t[1].y, c[3], fma(t[3].y, c[4], fma(t[4].y, c[5], u1)));
+    u2 = fma(t[2].y, c[3], fma(t[4].y, c[4], fma(t[5].y, c[5], u2)));
+  }
+}
+
+__global__ void __launch_bounds__(256, 4) k2_near(K2Params P) {
+  extern __shared__ __align__(16) double k2s[];
+  const int nq = P.nq, nb = P.nbp;
+  const bool doS = P.TS != nullptr, doD = P.TD != nullptr;
+  double* sy = k2s;                            // [nq][3] node positions
+  double* sqD = sy + 3 * nq;                   // [nq][3] cD w sigmaD
+  double* sqS = sqD + (doD ? 3 * nq : 0);      // [nq][3] cS w sigmaS
+  double* scD = sqS + (doS ? 3 * nq : 0);      // [nb][3]
+  double* scS = scD + (doD ? 3 * nb : 0);      // [nb][3]
+  const int beg = P.chunks[2 * blockIdx.x], end = P.chunks[2 * blockIdx.x + 1];
+  const int m = P.cm_m[beg];
+  const size_t j0 = (size_t)m * nq;
+  for (int e = threadIdx.x; e < 3 * nq; e += blockDim.x) {
+    const double w = P.src[8 * (j0 + e / 3) + 3];
+    sy[e] = P.X[3 * j0 + e];
+    if (doD) sqD[e] = P.cD * w * P.sigD[3 * j0 + e];
+    if (doS) sqS[e] = P.cS * w * P.sigS[3 * j0 + e];
+  }
+  for (int e = threadIdx.x; e < 3 * nb; e += blockDim.x) {
+    if (doD) scD[e] = P.coefD[(size_t)m * nb * 3 + e];
+    if (doS) scS[e] = P.coefS[(size_t)m * nb * 3 + e];
+  }
+  const double cm0 = P.centers[3 * m], cm1 = P.centers[3 * m + 1], cm2 = P.centers[3 * m + 2];
+  const double inv2a = 0.5 / P.a, a2 = P.a * P.a;
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int pos = beg + warp; pos < end; pos += nw) {
+    const int i = P.cm_t[pos];
+    if (i < P.t0 || i >= P.t1) continue;
+    const double x0 = P.X[3 * (size_t)i], x1 = P.X[3 * (size_t)i + 1], x2 = P.X[3 * (size_t)i + 2];
+    double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+    if (doD) k2_refined(P.TD + (size_t)pos * 6 * nb, scD, nb, lane, u0, u1, u2);
+    if (doS) k2_refined(P.TS + (size_t)pos * 6 * nb, scS, nb, lane, u0, u1, u2);
+    // minus the coarse pairs: K_D q = cD w (r.n)(r.q) r / rho^5, G f = cS w (f / rho + (r.f) r / rho^3);
+    // on sphere m, r.n_y = h - rho^2 / (2a) with h = (|x - c_m|^2 - a^2) / (2a)
+    const double d0 = x0 - cm0, d1 = x1 - cm1, d2 = x2 - cm2;
+    const double h = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a2) * inv2a;
+#pragma unroll 4
+    for (int j = lane; j < nq; j += 32) {
+      const double r0 = x0 - sy[3 * j], r1 = x1 - sy[3 * j + 1], r2 = x2 - sy[3 * j + 2];
+      const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+      double ir;  // rr^-1/2: MUFU.RSQ64H seed + (1-e)^-1/2 series to e^2 (|e| <= 2^-19, as K1)
+      asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(ir) : "d"(rr));
+      {
+        const double e = fma(-rr, ir * ir, 1.0);
+        ir = fma(ir * e, fma(e, 0.375, 0.5), ir);
+      }
+      const double ir2 = ir * ir, ir3 = ir * ir2;
+      double t = 0.0;
+      if (doD) {
+        const double rn = fma(rr, -inv2a, h);
+        const double rq = fma(r2, sqD[3 * j + 2], fma(r1, sqD[3 * j + 1], r0 * sqD[3 * j]));
+        t = (rn * rq) * (ir3 * ir2);
+      }
+      if (doS) {
+        const double rf = fma(r2, sqS[3 * j + 2], fma(r1, sqS[3 * j + 1], r0 * sqS[3 * j]));
+        t = fma(rf, ir3, t);
+        u0 = fma(-sqS[3 * j], ir, u0);
+        u1 = fma(-sqS[3 * j + 1], ir, u1);
+        u2 = fma(-sqS[3 * j + 2], ir, u2);
+      }
+      u0 = fma(-t, r0, u0);
+      u1 = fma(-t, r1, u1);
+      u2 = fma(-t, r2, u2);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      u0 += __shfl_xor_sync(0xffffffffu, u0, o);
+      u1 += __shfl_xor_sync(0xffffffffu, u1, o);
+      u2 += __shfl_xor_sync(0xffffffffu, u2, o);
+    }
+    if (lane == 0) {
+      atomicAdd(P.out + 3 * (size_t)i, u0);
+      atomicAdd(P.out + 3 * (size_t)i + 1, u1);
+      atomicAdd(P.out + 3 * (size_t)i + 2, u2);
+    }
+  }
 }
 
 void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
   g.prof.launches++;
-  if (g.n_near_targets == 0) return;
-  const double* MS = (sigS && g.M_S.p) ? g.M_S.p : nullptr;
-  const double* MD = sigD ? g.M_D.p : nullptr;
-  // sharded: only this rank's near targets (the list is sorted by target node)
-  const int k0 = g.shard_world > 1 ? g.sh_k0 : 0, k1 = g.shard_world > 1 ? g.sh_k1 : g.n_near_targets;
-  if (k1 <= k0) return;
-  int warps = 3 * (k1 - k0);
-  int threads = 256;
-  int blocks = (warps * 32 + threads - 1) / threads;
-  k2_near<<<blocks, threads, 0, st>>>(k1 - k0, g.nt_list.p + k0, g.nt_ptr.p + k0, g.inc_m.p, g.nq, MS, sigS, MD,
-                                      sigD, out);
+  if (g.n_inc == 0) return;
+  const bool doS = sigS && g.T_S.p, doD = sigD != nullptr;
+  if (!doS && !doD) return;
+  const int nq = g.nq, nb = g.nb;
+  const int nbp = (nb + 1) & ~1;
+  g.coef.ensure((size_t)2 * g.np * nbp * 3);
+  double* coefD = g.coef.p;
+  double* coefS = g.coef.p + (size_t)g.np * nbp * 3;
+  // node ranges split over 4 blocks for parallelism (atomic sums into zeroed coefficients)
+  const dim3 cgrid((nbp + KC_BM - 1) / KC_BM, (g.np + KC_BS - 1) / KC_BS, 4);
+  BPQN_CUDA(cudaMemsetAsync(g.coef.p, 0, sizeof(double) * 2 * (size_t)g.np * nbp * 3, st));
+  if (doD) {
+    k2_coef<<<cgrid, 256, 0, st>>>(nq, nb, nbp, g.np, g.analysis.p, sigD, coefD);
+    BPQN_CHECK_LAUNCH();
+    g.prof.launches++;
+  }
+  if (doS) {
+    k2_coef<<<cgrid, 256, 0, st>>>(nq, nb, nbp, g.np, g.analysis.p, sigS, coefS);
+    BPQN_CHECK_LAUNCH();
+    g.prof.launches++;
+  }
+  K2Params P{};
+  P.chunks = g.chunks.p;
+  P.cm_t = g.cm_t.p;
+  P.cm_m = g.cm_m.p;
+  P.X = g.X.p;
+  P.src = g.src.p;
+  P.centers = g.centers_d.p;
+  P.a = g.a;
+  P.TS = doS ? g.T_S.p : nullptr;
+  P.TD = doD ? g.T_D.p : nullptr;
+  P.coefS = coefS;
+  P.coefD = coefD;
+  P.sigS = sigS;
+  P.sigD = sigD;
+  P.nq = nq;
+  P.nbp = nbp;
+  P.t0 = g.shard_world > 1 ? g.sh_t0 : 0;
+  P.t1 = g.shard_world > 1 ? g.sh_t1 : g.n;
+  P.cS = 1.0 / (8.0 * 3.14159265358979323846 * g.mu);
+  P.cD = -3.0 / (4.0 * 3.14159265358979323846);
+  P.out = out;
+  const int smem = (3 * nq + (doD ? 3 * nq + 3 * nbp : 0) + (doS ? 3 * nq + 3 * nbp : 0)) * 8;
+  static std::atomic<int> attr{48 * 1024};  // the opt-in limit only grows
+  if (smem > attr.load()) {
+    BPQN_CUDA(cudaFuncSetAttribute(k2_near, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr.store(smem);
+  }
+  k2_near<<<g.n_chunks, 256, smem, st>>>(P);
   BPQN_CHECK_LAUNCH();
   g.prof.launches++;
 }
