@@ -690,7 +690,8 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
 }
 
 // Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps at 1 CTA/SM with
-// 5 (D, S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 14.81, S 15.65, S+D 22.60 ms), 8 x 3 below.
+// 5 (D, S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 14.81, S 15.65, S+D 22.60 ms), 4 targets/lane
+// for N >= 2e4 (c3 D 1.355 vs 1.46 ms with 3; c4 centres at p = 8: 1.14 vs 1.17 ms), 8 x 3 below.
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -704,7 +705,7 @@ static int k1_cfg() {
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
   int c = k1_cfg();
-  if (c < 0) c = g.n >= 60000 ? (MODE == MODE_SD ? 4 : 14) : 3;
+  if (c < 0) c = g.n >= 60000 ? (MODE == MODE_SD ? 4 : 14) : (g.n >= 20000 ? 4 : 3);
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;

@@ -22,7 +22,7 @@ namespace bpqn {
 // sphere's nodes, weighted densities and coefficients in shared memory, and stream the
 // [6][nb] tensors from HBM once per application (16-byte streaming loads); the coarse
 // subtraction is recomputed from the staged nodes (~30 flops per pair, FP64 pipe).
-// Each incidence adds its 3 values to the target with fp64 atomics (<= a few per target).
+// One incidence per half-warp; each adds its 3 values to the target with fp64 atomics.
 
 // coef[m][b][c] = sum_j A[b][j] sigma[m][j][c] (A row-major [nb][nq]); rows b in [nb, nbp) are zero.
 // A small tiled GEMM: block = 32 rows of A x 8 spheres; its 256 threads form 4 groups that take
@@ -110,11 +110,11 @@ struct K2Params {
 
 // u[a] += sum_c T[sym(a,c)] c[c] over the packed symmetric rows, streamed in b pairs
 __device__ __forceinline__ void k2_refined(const double* __restrict__ T, const double* __restrict__ cf, int nbp,
-                                           int lane, double& u0, double& u1, double& u2) {
+                                           int hl, double& u0, double& u1, double& u2) {
   const double2* T2 = reinterpret_cast<const double2*>(T);
   const int nb2 = nbp >> 1;
 #pragma unroll 2
-  for (int b2 = lane; b2 < nb2; b2 += 32) {
+  for (int b2 = hl; b2 < nb2; b2 += 16) {
     double2 t[6];
 #pragma unroll
     for (int q = 0; q < 6; ++q) t[q] = __ldcs(T2 + q * nb2 + b2);
@@ -153,20 +153,22 @@ __global__ void __launch_bounds__(256, 4) k2_near(K2Params P) {
   const double cm0 = P.centers[3 * m], cm1 = P.centers[3 * m + 1], cm2 = P.centers[3 * m + 2];
   const double inv2a = 0.5 / P.a, a2 = P.a * P.a;
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int pos = beg + warp; pos < end; pos += nw) {
+  // one incidence per half-warp (two latency chains per warp, better lane use at small p)
+  const int lane = threadIdx.x & 31, hl = lane & 15, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned hmask = 0xffffu << (lane & 16);
+  for (int pos = beg + 2 * warp + (lane >> 4); pos < end; pos += 2 * nw) {
     const int i = P.cm_t[pos];
     if (i < P.t0 || i >= P.t1) continue;
     const double x0 = P.X[3 * (size_t)i], x1 = P.X[3 * (size_t)i + 1], x2 = P.X[3 * (size_t)i + 2];
     double u0 = 0.0, u1 = 0.0, u2 = 0.0;
-    if (doD) k2_refined(P.TD + (size_t)pos * 6 * nb, scD, nb, lane, u0, u1, u2);
-    if (doS) k2_refined(P.TS + (size_t)pos * 6 * nb, scS, nb, lane, u0, u1, u2);
+    if (doD) k2_refined(P.TD + (size_t)pos * 6 * nb, scD, nb, hl, u0, u1, u2);
+    if (doS) k2_refined(P.TS + (size_t)pos * 6 * nb, scS, nb, hl, u0, u1, u2);
     // minus the coarse pairs: K_D q = cD w (r.n)(r.q) r / rho^5, G f = cS w (f / rho + (r.f) r / rho^3);
     // on sphere m, r.n_y = h - rho^2 / (2a) with h = (|x - c_m|^2 - a^2) / (2a)
     const double d0 = x0 - cm0, d1 = x1 - cm1, d2 = x2 - cm2;
     const double h = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a2) * inv2a;
 #pragma unroll 4
-    for (int j = lane; j < nq; j += 32) {
+    for (int j = hl; j < nq; j += 16) {
       const double r0 = x0 - sy[3 * j], r1 = x1 - sy[3 * j + 1], r2 = x2 - sy[3 * j + 2];
       const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
       double ir;  // rr^-1/2: MUFU.RSQ64H seed + (1-e)^-1/2 series to e^2 (|e| <= 2^-19, as K1)
@@ -194,12 +196,12 @@ __global__ void __launch_bounds__(256, 4) k2_near(K2Params P) {
       u2 = fma(-t, r2, u2);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      u0 += __shfl_xor_sync(0xffffffffu, u0, o);
-      u1 += __shfl_xor_sync(0xffffffffu, u1, o);
-      u2 += __shfl_xor_sync(0xffffffffu, u2, o);
+    for (int o = 8; o > 0; o >>= 1) {
+      u0 += __shfl_xor_sync(hmask, u0, o);
+      u1 += __shfl_xor_sync(hmask, u1, o);
+      u2 += __shfl_xor_sync(hmask, u2, o);
     }
-    if (lane == 0) {
+    if (hl == 0) {
       atomicAdd(P.out + 3 * (size_t)i, u0);
       atomicAdd(P.out + 3 * (size_t)i + 1, u1);
       atomicAdd(P.out + 3 * (size_t)i + 2, u2);

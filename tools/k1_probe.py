@@ -27,13 +27,14 @@ f, q = layer_densities(a.config, g.N)
 f = torch.tensor(f, device="cuda") if "s" in a.mode else None
 q = torch.tensor(q, device="cuda") if "d" in a.mode else None
 u = torch.empty((g.N, 3), dtype=torch.float64, device="cuda")
-per = []
+per, per2 = [], []
 tot = dict(ms_allpairs=0.0, allpairs_gflop=0.0, ms_near=0.0, ms_self=0.0)
 for _ in range(a.reps):
     bp.profile_reset(g, events=True)
     bp.layer_apply(g, f=f, q=q, out=u)
     pr1 = bp.profile_get(g)
     per.append(round(pr1["ms_allpairs"], 3))
+    per2.append(round(pr1["ms_near"], 3))
     for k in tot:
         tot[k] += pr1[k]
 torch.cuda.synchronize()
@@ -41,6 +42,6 @@ pr = tot
 print("N", g.N, "mode", a.mode, "k1 ms/launch %.3f" % (pr["ms_allpairs"] / a.reps),
       "TFLOP/s %.2f" % (pr["allpairs_gflop"] / pr["ms_allpairs"]), "k2 %.3f k3 %.3f" % (pr["ms_near"] / a.reps,
                                                                                      pr["ms_self"] / a.reps),
-      "per-launch", per)
+      "per-launch", per, "k2 per-launch", per2)
 if a.save:
     np.save(a.save, u.cpu().numpy())
