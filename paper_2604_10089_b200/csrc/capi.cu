@@ -543,6 +543,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     if (bi) {
       MvpFn flo = make(lo, glo, ms_lo, it_lo, n_lo);
       BiResult r = bi_pqn(fhi, flo, b, x0, q);
+      prox_profile_flush();
       x = r.x;
       iters = r.iterations;
       term = r.termination;
@@ -552,6 +553,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       kkt_rel = r.kkt_rel;
     } else {
       MonoResult r = o.method == 2 ? bb_pgd(fhi, b, x0, q) : mono_pqn(fhi, b, x0, q, nullptr, nullptr, nullptr);
+      prox_profile_flush();
       x = r.x;
       iters = r.iterations;
       term = r.termination;

@@ -10,6 +10,7 @@
 // crosses PCIe per MVP.  C^{-1} = (D + UU^T)^{-1} is applied by the Woodbury identity.
 #include <algorithm>
 #include <chrono>
+#include <omp.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cmath>
@@ -72,6 +73,7 @@ void Bfgs::clear() {
   V.clear();
   S.clear();
   Y.clear();
+  wc = WoodburyCache();
 }
 Vec Bfgs::B(const Vec& x) const {
   Vec out = x;
@@ -176,29 +178,42 @@ static void chol_solve(const std::vector<double>& L, int n, double* X, int m) {
   }
 }
 
-// LU with partial pivoting, one right-hand side; trailing update threaded by rows
+// LU with partial pivoting, one right-hand side.  One OpenMP team for the whole
+// factorisation (no fork/join per column): the pivot search and swap run on one thread,
+// the trailing update is split by rows; the solve is serial.
 static bool lu_solve_par(std::vector<double>& A, int n, Vec& b) {
-  for (int k = 0; k < n; ++k) {
-    int pm = k;
-    for (int i = k + 1; i < n; ++i)
-      if (std::fabs(A[(size_t)i * n + k]) > std::fabs(A[(size_t)pm * n + k])) pm = i;
-    if (A[(size_t)pm * n + k] == 0.0) return false;
-    if (pm != k) {
-      for (int j = 0; j < n; ++j) std::swap(A[(size_t)k * n + j], A[(size_t)pm * n + j]);
-      std::swap(b[k], b[pm]);
-    }
-    const double piv = A[(size_t)k * n + k];
-    const double* rk = &A[(size_t)k * n];
-#pragma omp parallel for schedule(static) if (par((long long)(n - k) * (n - k)))
-    for (int i = k + 1; i < n; ++i) {
-      double* ri = &A[(size_t)i * n];
-      const double f = ri[k] / piv;
-      if (f == 0.0) continue;
+  bool ok = true;
+  const int nt = par((long long)n * n * n / 3) ? 0 : 1;  // 0: default team size
+#pragma omp parallel num_threads(nt > 0 ? nt : omp_get_max_threads())
+  {
+    for (int k = 0; k < n; ++k) {
+#pragma omp single
+      {
+        int pm = k;
+        for (int i = k + 1; i < n; ++i)
+          if (std::fabs(A[(size_t)i * n + k]) > std::fabs(A[(size_t)pm * n + k])) pm = i;
+        if (A[(size_t)pm * n + k] == 0.0) {
+          ok = false;
+        } else if (pm != k) {
+          for (int j = 0; j < n; ++j) std::swap(A[(size_t)k * n + j], A[(size_t)pm * n + j]);
+          std::swap(b[k], b[pm]);
+        }
+      }  // implicit barrier
+      if (!ok) break;
+      const double piv = A[(size_t)k * n + k];
+      const double* rk = &A[(size_t)k * n];
+#pragma omp for schedule(static)
+      for (int i = k + 1; i < n; ++i) {
+        double* ri = &A[(size_t)i * n];
+        const double f = ri[k] / piv;
+        if (f == 0.0) continue;
 #pragma omp simd
-      for (int j = k; j < n; ++j) ri[j] -= f * rk[j];
-      b[i] -= f * b[k];
+        for (int j = k; j < n; ++j) ri[j] -= f * rk[j];
+        b[i] -= f * b[k];
+      }  // implicit barrier
     }
   }
+  if (!ok) return false;
   for (int i = n - 1; i >= 0; --i) {
     double s = b[i];
     for (int j = i + 1; j < n; ++j) s -= A[(size_t)i * n + j] * b[j];
@@ -223,8 +238,123 @@ struct ProxTimers {
   }
 };
 static ProxTimers g_pt;
+void prox_profile_flush() {  // BPQN_PQN_PROFILE: report and reset (called after each solve)
+  if (!getenv("BPQN_PQN_PROFILE")) return;
+  fprintf(stderr, "prox: calls %ld newton %ld avg r %.1f | setup %.3fs jac %.3fs lu %.3fs resid %.3fs\n", g_pt.calls,
+          g_pt.newton, g_pt.calls ? (double)g_pt.rsum / g_pt.calls : 0.0, g_pt.setup, g_pt.jac, g_pt.lu, g_pt.resid);
+  g_pt.setup = g_pt.jac = g_pt.lu = g_pt.resid = 0;
+  g_pt.calls = g_pt.newton = g_pt.rsum = 0;
+}
 static double now_s() {
   return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+// Bring q.wc up to date with q.U / q.V (see WoodburyCache).  Full build: CU = U K^-1,
+// CV = V - U K^-1 U^T V with K = I + U^T U (Cholesky); append of (u, v): w = C^-1 u,
+// den = 1 + u.w, CU_i -= w (w.U_i)/den, CV_i -= w (w.V_i)/den, then CU_new = w/den,
+// CV_new = C^-1 v - w (w.v)/den with C^-1 x = x - sum_i CU_i (U_i.x) of the old memory.
+static void woodbury_update(const Bfgs& q, int n) {
+  WoodburyCache& W = q.wc;
+  const int r = (int)q.U.size();
+  const bool full = W.n != n || W.r > r || W.appends + (r - W.r) > 64 || W.r == 0 ||
+                    (r > 0 && W.r > 0 && !std::equal(q.U[W.r - 1].begin(), q.U[W.r - 1].end(),
+                                                     W.Um.begin() + (size_t)(W.r - 1) * n));
+  if (full) {
+    W = WoodburyCache();
+    W.n = n;
+    W.r = r;
+    W.Um.resize((size_t)r * n);
+    W.Vm.resize((size_t)r * n);
+    W.CU.resize((size_t)r * n);
+    W.CV.resize((size_t)r * n);
+    for (int c = 0; c < r; ++c) {
+      std::copy(q.U[c].begin(), q.U[c].end(), W.Um.begin() + (size_t)c * n);
+      std::copy(q.V[c].begin(), q.V[c].end(), W.Vm.begin() + (size_t)c * n);
+    }
+    if (r == 0) return;
+    // K = I + U^T U; X = K^-1 [U^T U | U^T V]; CU_c = U_c - sum_i X[i][c] U_i ... written as
+    // CU = U K^-1 (columns c: sum_i U_i Kinv[i][c]) and CV = V - U K^-1 U^T V
+    std::vector<double> K((size_t)r * r), X((size_t)r * 2 * r, 0.0), G((size_t)r * r);
+    gemm_nt(W.Um.data(), W.Um.data(), K.data(), r, r, n, false);
+    for (int i = 0; i < r; ++i) K[(size_t)i * r + i] += 1.0;
+    if (!cholesky(K, r)) throw std::runtime_error("Woodbury core not positive definite");
+    gemm_nt(W.Um.data(), W.Vm.data(), G.data(), r, r, n, false);  // G[i][c] = U_i . V_c
+    for (int i = 0; i < r; ++i) {
+      X[(size_t)i * 2 * r + i] = 1.0;  // identity -> K^-1
+      for (int c = 0; c < r; ++c) X[(size_t)i * 2 * r + r + c] = G[(size_t)i * r + c];
+    }
+    chol_solve(K, r, X.data(), 2 * r);
+#pragma omp parallel for schedule(static) if (par((long long)r * r * n))
+    for (int c = 0; c < r; ++c) {
+      double* ou = &W.CU[(size_t)c * n];
+      double* ov = &W.CV[(size_t)c * n];
+      std::fill(ou, ou + n, 0.0);
+      std::copy(&W.Vm[(size_t)c * n], &W.Vm[(size_t)c * n] + n, ov);
+      for (int i = 0; i < r; ++i) {
+        const double fu = X[(size_t)i * 2 * r + c], fv = X[(size_t)i * 2 * r + r + c];
+        const double* u = &W.Um[(size_t)i * n];
+#pragma omp simd
+        for (int e = 0; e < n; ++e) {
+          ou[e] += fu * u[e];
+          ov[e] -= fv * u[e];
+        }
+      }
+    }
+    return;
+  }
+  for (int k = W.r; k < r; ++k) {  // append pair k
+    const Vec& u = q.U[k];
+    const Vec& v = q.V[k];
+    const int r0 = W.r;
+    // w = C^-1 u, z = C^-1 v with the current (old) memory
+    Vec cu(r0), cv(r0);
+#pragma omp parallel for schedule(static) if (par((long long)r0 * n * 2))
+    for (int i = 0; i < r0; ++i) {
+      const double* Ui = &W.Um[(size_t)i * n];
+      double su = 0.0, sv = 0.0;
+      for (int e = 0; e < n; ++e) {
+        su += Ui[e] * u[e];
+        sv += Ui[e] * v[e];
+      }
+      cu[i] = su;
+      cv[i] = sv;
+    }
+    Vec w = u, z = v;
+    for (int i = 0; i < r0; ++i) {
+      const double* Ci = &W.CU[(size_t)i * n];
+      for (int e = 0; e < n; ++e) {
+        w[e] -= Ci[e] * cu[i];
+        z[e] -= Ci[e] * cv[i];
+      }
+    }
+    const double den = 1.0 + dot(u, w);
+    // rank-one correction of the existing columns
+#pragma omp parallel for schedule(static) if (par((long long)r0 * n * 2))
+    for (int i = 0; i < r0; ++i) {
+      double* ci = &W.CU[(size_t)i * n];
+      double* vi = &W.CV[(size_t)i * n];
+      const double* Ui = &W.Um[(size_t)i * n];
+      const double* Vi = &W.Vm[(size_t)i * n];
+      double a = 0.0, b = 0.0;
+      for (int e = 0; e < n; ++e) {
+        a += w[e] * Ui[e];
+        b += w[e] * Vi[e];
+      }
+      a /= den;
+      b /= den;
+      for (int e = 0; e < n; ++e) {
+        ci[e] -= a * w[e];
+        vi[e] -= b * w[e];
+      }
+    }
+    const double wv = dot(w, v) / den;
+    W.Um.insert(W.Um.end(), u.begin(), u.end());
+    W.Vm.insert(W.Vm.end(), v.begin(), v.end());
+    for (int e = 0; e < n; ++e) W.CU.push_back(w[e] / den);
+    for (int e = 0; e < n; ++e) W.CV.push_back(z[e] - wv * w[e]);
+    W.r = k + 1;
+    W.appends++;
+  }
 }
 
 Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters) {
@@ -244,29 +374,10 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     for (double v : xt) mx = std::max(mx, std::fabs(v));
     tol = 1e-12 * mx;
   }
-  std::vector<double> Um((size_t)r * n), Vm((size_t)r * n), CV((size_t)r * n);
-  for (int c = 0; c < r; ++c) {
-    std::copy(q.U[c].begin(), q.U[c].end(), Um.begin() + (size_t)c * n);
-    std::copy(q.V[c].begin(), q.V[c].end(), Vm.begin() + (size_t)c * n);
-  }
-  // C^{-1} V = V - U (I + U^T U)^{-1} U^T V   (rows: CV_c = V_c - sum_i X[i][c] U_i)
-  std::vector<double> K((size_t)r * r), X((size_t)r * r);
-  gemm_nt(Um.data(), Um.data(), K.data(), r, r, n, false);
-  for (int i = 0; i < r; ++i) K[(size_t)i * r + i] += 1.0;
-  if (!cholesky(K, r)) throw std::runtime_error("Woodbury core not positive definite");
-  gemm_nt(Um.data(), Vm.data(), X.data(), r, r, n, false);  // X[i][c] = U_i . V_c
-  chol_solve(K, r, X.data(), r);
-#pragma omp parallel for schedule(static) if (par((long long)r * r * n))
-  for (int c = 0; c < r; ++c) {
-    double* o = &CV[(size_t)c * n];
-    std::copy(&Vm[(size_t)c * n], &Vm[(size_t)c * n] + n, o);
-    for (int i = 0; i < r; ++i) {
-      const double f = X[(size_t)i * r + c];
-      const double* u = &Um[(size_t)i * n];
-#pragma omp simd
-      for (int e = 0; e < n; ++e) o[e] -= f * u[e];
-    }
-  }
+  woodbury_update(q, n);
+  const std::vector<double>& Um = q.wc.Um;
+  const std::vector<double>& Vm = q.wc.Vm;
+  const std::vector<double>& CV = q.wc.CV;
   const int d = 2 * r;
   g_pt.setup += now_s() - t_0;
   Vec al(d, 0.0);  // [alpha; alpha~]

@@ -20,8 +20,17 @@ struct PqnOpts {
   double sub_forcing = 0.0;
 };
 
+// C^-1 U and C^-1 V (C = I + U U^T) for the prox's Woodbury step, kept across prox calls
+// on the same memory and extended by Sherman-Morrison as pairs are appended (O(r n) per
+// pair instead of O(r^2 n) per call); rebuilt after a clear or every 64 appends.
+struct WoodburyCache {
+  int r = 0, n = 0, appends = 0;
+  std::vector<double> Um, Vm, CU, CV;  // [r][n] row-major
+};
+
 struct Bfgs {
   std::vector<std::vector<double>> U, V, S, Y;
+  mutable WoodburyCache wc;
   void clear();
   std::vector<double> B(const std::vector<double>& x) const;
   std::vector<double> H(const std::vector<double>& g) const;
@@ -44,6 +53,7 @@ struct BiResult {
 };
 
 double kkt_abs(const std::vector<double>& x, const std::vector<double>& g);
+void prox_profile_flush();
 std::vector<double> weighted_prox(const Bfgs& q, const std::vector<double>& xt, double tol, int jmax, int* iters);
 double optimal_eta(const std::vector<double>& x, const std::vector<double>& p, const std::vector<double>& g,
                    const std::vector<double>& Ap, std::vector<char>& bind);
