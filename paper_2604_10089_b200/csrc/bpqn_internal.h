@@ -151,9 +151,8 @@ struct Geom {
   DBuf<int> cm_t, cm_m;          // [n_inc] target node / source sphere per position
   DBuf<int> chunks;              // [n_chunks][2] position ranges
   int n_chunks = 0;
-  DBuf<double> T_S, T_D;         // [n_inc][6][nb]
-  DBuf<double> coef;             // [2][np][nb][3] SH coefficients of the densities (K2 workspace)
-  DBuf<double> analysis_t;       // [nq][nb] transpose of analysis
+  DBuf<double> T_S, T_D;         // [n_inc][6][nb'], nb' = nb rounded up to even (zero pad)
+  DBuf<double> coef;             // [2][np][nb'][3] SH coefficients of the densities (K2 workspace)
 
   // contacts
   int nc = 0, nc_cap = 0;

@@ -213,14 +213,6 @@ __device__ inline void rot_apply(const double R[9], double x, double y, double z
   oz = R[6] * x + R[7] * y + R[8] * z;
 }
 
-// out[c][r] = in[r][c], in [rows][cols]
-__global__ void k_transpose(const double* in, int rows, int cols, double* out) {
-  const size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (size_t)rows * cols) return;
-  const size_t r = e / cols, c = e - r * cols;
-  out[c * rows + r] = in[e];
-}
-
 __global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
   extern __shared__ double sm[];
   const int prob = blockIdx.x;
@@ -629,9 +621,6 @@ void precompute(Geom& g, cudaStream_t st, bool with_self) {
   BPQN_CUDA(cudaMemcpyAsync(d_wunit.p, wunit.data(), nq * 8, cudaMemcpyHostToDevice, st));
   g.analysis.alloc((size_t)nb * nq);
   k_analysis<<<(nq + 127) / 128, 128, 0, st>>>(p, nq, g.xi_d.p, d_wunit.p, T, Yn.p, g.analysis.p, nb);
-  BPQN_CHECK_LAUNCH();
-  g.analysis_t.alloc((size_t)nq * nb);
-  k_transpose<<<(unsigned)(((size_t)nb * nq + 255) / 256), 256, 0, st>>>(g.analysis.p, nb, nq, g.analysis_t.p);
   BPQN_CHECK_LAUNCH();
   BPQN_CUDA(cudaStreamSynchronize(st));  // d_wunit / Yn are released at the end of this scope
   }
