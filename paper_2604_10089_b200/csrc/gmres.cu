@@ -23,8 +23,21 @@ __global__ void k_mdot(const double* __restrict__ V, size_t ld, const double* __
                        double* red, int nbx) {
   const int i = blockIdx.y;
   const double* v = V + (size_t)i * ld;
-  double acc = 0.0;
-  for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n; e += (size_t)nbx * GT) acc = fma(v[e], w[e], acc);
+  double acc = 0.0, acc2 = 0.0;
+  if ((n & 1) == 0 && (ld & 1) == 0) {  // 16-byte loads (n = 3N is even for every grid)
+    const double2* v2 = reinterpret_cast<const double2*>(v);
+    const double2* w2 = reinterpret_cast<const double2*>(w);
+    const size_t n2 = n >> 1;
+#pragma unroll 4
+    for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n2; e += (size_t)nbx * GT) {
+      const double2 a = v2[e], b = w2[e];
+      acc = fma(a.x, b.x, acc);
+      acc2 = fma(a.y, b.y, acc2);
+    }
+    acc += acc2;
+  } else {
+    for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n; e += (size_t)nbx * GT) acc = fma(v[e], w[e], acc);
+  }
   __shared__ double sred[GT / 32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -63,11 +76,28 @@ __global__ void k_mupdate(const double* __restrict__ V, size_t ld, int kv, const
   for (int i = threadIdx.x; i < kv; i += blockDim.x) sh[i] = h[i];
   __syncthreads();
   double nrm = 0.0;
-  for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n; e += (size_t)nbx * GT) {
-    double acc = w[e];
-    for (int i = 0; i < kv; ++i) acc = fma(-V[(size_t)i * ld + e], sh[i], acc);
-    w[e] = acc;
-    nrm = fma(acc, acc, nrm);
+  if ((n & 1) == 0 && (ld & 1) == 0) {  // 16-byte loads, two independent chains per thread
+    double2* w2 = reinterpret_cast<double2*>(w);
+    const size_t n2 = n >> 1, ld2 = ld >> 1;
+    const double2* V2 = reinterpret_cast<const double2*>(V);
+    for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n2; e += (size_t)nbx * GT) {
+      double2 acc = w2[e];
+#pragma unroll 8
+      for (int i = 0; i < kv; ++i) {
+        const double2 v = V2[(size_t)i * ld2 + e];
+        acc.x = fma(-v.x, sh[i], acc.x);
+        acc.y = fma(-v.y, sh[i], acc.y);
+      }
+      w2[e] = acc;
+      nrm = fma(acc.x, acc.x, fma(acc.y, acc.y, nrm));
+    }
+  } else {
+    for (size_t e = (size_t)blockIdx.x * GT + threadIdx.x; e < n; e += (size_t)nbx * GT) {
+      double acc = w[e];
+      for (int i = 0; i < kv; ++i) acc = fma(-V[(size_t)i * ld + e], sh[i], acc);
+      w[e] = acc;
+      nrm = fma(acc, acc, nrm);
+    }
   }
   if (!red) return;
   __shared__ double sred[GT / 32];
