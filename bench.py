@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--solvers", default="bi")          # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--shard", action="store_true")     # N > 1: shard one MVP over the ranks (NCCL all-gather)
+    ap.add_argument("--shard-asym", action="store_true")  # sharded K1 as the one-directional kernel (no reduce-scatter)
     ap.add_argument("--sub-forcing", type=float, default=0.0)   # Bi-PQN inexact subproblems (off = R22)
     ap.add_argument("--c5-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-targets", type=int, default=0)
@@ -229,7 +230,7 @@ def run_ours(args, ws, rank, local):
     nc = g.nc
     shard = args.shard and ws > 1
     if shard:   # strong scaling of one MVP: each rank owns Np/N spheres' rows
-        bp.geometry_shard(g, rank, ws)
+        bp.geometry_shard(g, rank, ws, symmetric=not args.shard_asym)
     rng = np.random.default_rng(20260000 + args.config + 2000)     # synth.lambda_test recipe
     lam_h = rng.uniform(0.0, 1.0, size=nc)
     lam = torch.tensor(lam_h, dtype=torch.float64, device=dev)
@@ -308,7 +309,10 @@ def run_ours(args, ws, rank, local):
                    "contacts": nc, "gmres_tol": args.gmres_tol, "gmres_restart": gm.restart,
                    "gmres_iters_per_mvp": k_g, "near_incidences": g.n_incidences,
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
-                   "parallelism": ("shard-targets (NCCL all-gather per operator application)" if shard
+                   "parallelism": (("shard-targets (one-directional K1, NCCL all-gather per operator application)"
+                                    if args.shard_asym else
+                                    "shard (symmetric K1 units split, NCCL reduce-scatter + all-gather per operator "
+                                    "application)") if shard
                                    else ("replicas" if ws > 1 else "single GPU")),
                    "geometry_init_s": round(t_init, 3)},
         "pair_interactions_per_s": n_pairs_step * (1 if shard else ws) / (ms_per_step * 1e-3),

@@ -221,6 +221,19 @@ int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, c
 int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, double* recv_dev,
                         int (*allgather)(void* user), void* user);
 
+/* Symmetric K1 on a sharded handle (after bpqn_geometry_shard with world > 1): instead of the
+ * one-directional kernel over the owned target rows, every rank runs an equal share of the
+ * symmetric kernel's unordered (target block, source tile) units -- half the pair work of the
+ * one-directional split -- whose partial sums cover all rows.  Each operator application then
+ * fills rs_send_dev ([world][rows][3], rank-major, rows as in bpqn_geometry_shard, zero-padded)
+ * and, after synchronising the handle's stream, calls reduce_scatter(user), which must write
+ * into rs_recv_dev ([rows][3]) the element-wise sum over ranks of their chunk for this rank
+ * (e.g. NCCL reduce_scatter_tensor) and return 0; K2 / K3 and the all-gather follow as in
+ * bpqn_geometry_shard.  Needs Nq >= 64 and Np <= 4096 (else error 1).  A NULL callback
+ * switches back to the one-directional kernel.  Buffers and user stay owned by the caller. */
+int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs_recv_dev,
+                                  int (*reduce_scatter)(void* user), void* user);
+
 /* Empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
 int bpqn_gmres_recycle_reset(bpqn_geom_t g);
 

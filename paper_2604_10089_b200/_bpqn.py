@@ -74,6 +74,7 @@ SYMBOLS = {
     "bpqn_last_error": (ctypes.c_char_p, []),
     "bpqn_gmres_recycle_reset": (c_int, [c_void_p]),
     "bpqn_geometry_shard": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
+    "bpqn_geometry_shard_symmetric": (c_int, [c_void_p, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
     "bpqn_dvi_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                               P(SolveOpts), c_void_p, P(StepReport), c_void_p]),
@@ -338,9 +339,38 @@ def _torch_allgather(send, recv):
     torch.cuda.current_stream().synchronize()
 
 
-def geometry_shard(g, rank, world, allgather=None):
+def _torch_reduce_scatter(send, recv):
+    """reduce-scatter (sum) of [world][rows] device buffers with torch.distributed (NCCL directly;
+    other backends, e.g. gloo in tests, as an all-reduce of host copies)."""
+    import torch
+    import torch.distributed as dist
+    if dist.get_backend() == "nccl":
+        dist.reduce_scatter_tensor(recv, send)
+    else:
+        h = send.cpu()
+        dist.all_reduce(h)
+        r, n = dist.get_rank(), recv.numel()
+        recv.copy_(h[r * n:(r + 1) * n].to(recv.device))
+    torch.cuda.current_stream().synchronize()
+
+
+def _callback(fn, a, b):
+    def cb(_user):
+        try:
+            fn(a, b)
+            return 0
+        except Exception:  # reported as BPQN_ERR_CUDA by the library
+            import traceback
+            traceback.print_exc()
+            return 1
+    return ALLGATHER_FN(cb)
+
+
+def geometry_shard(g, rank, world, allgather=None, symmetric=False, reduce_scatter=None):
     """Shard the layer operator's target side over `world` ranks (bpqn_geometry_shard);
     `allgather(send, recv)` performs the collective on the two CUDA tensors (default:
+    torch.distributed).  symmetric=True also runs K1 as the symmetric kernel split over the
+    ranks (bpqn_geometry_shard_symmetric) with `reduce_scatter(send, recv)` (default:
     torch.distributed).  world = 1 restores the single-GPU operator."""
     import torch
     if world == 1:
@@ -364,6 +394,12 @@ def geometry_shard(g, rank, world, allgather=None):
     cfun = ALLGATHER_FN(cb)
     g._shard = (send, recv, cfun)  # keep alive as long as the sharding
     _check(lib().bpqn_geometry_shard(g.h, rank, world, _ptr(send), _ptr(recv), cfun, None))
+    if symmetric:
+        rs_send = torch.zeros(world * 3 * rows, dtype=torch.float64, device="cuda")
+        rs_recv = torch.zeros(3 * rows, dtype=torch.float64, device="cuda")
+        rfun = _callback(reduce_scatter or _torch_reduce_scatter, rs_send, rs_recv)
+        g._shard = g._shard + (rs_send, rs_recv, rfun)
+        _check(lib().bpqn_geometry_shard_symmetric(g.h, _ptr(rs_send), _ptr(rs_recv), rfun, None))
 
 
 def gmres_recycle_reset(g):

@@ -311,7 +311,8 @@ struct K1SymParams {
   double* out;            // [N][3], zeroed, atomically accumulated
   int N, nb, nt, nq, np;  // blocks of KS_B points, tiles of K1_TS points, nodes per sphere, spheres
   double a;
-  long long units;
+  long long units;        // units this launch processes: [ubeg, ubeg + units) of the block-major list
+  long long ubeg;         // (ubeg > 0 only when sharded over ranks, bpqn_geometry_shard_symmetric)
 };
 
 // compact records of the symmetric kernel: S {y, f~}, D {y, q~}, S+D {y, f~, q~, pad}
@@ -484,8 +485,8 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   __shared__ __align__(8) uint64_t full[NS];
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const long long u0 = P.units * blockIdx.x / gridDim.x;
-  const long long u1 = P.units * (blockIdx.x + 1) / gridDim.x;
+  const long long u0 = P.ubeg + P.units * blockIdx.x / gridDim.x;
+  const long long u1 = P.ubeg + P.units * (blockIdx.x + 1) / gridDim.x;
   if (u0 >= u1) return;
   if (MODE != MODE_S)
     for (int e = tid; e < 3 * P.np; e += blockDim.x) cs[e] = P.centers[e];
@@ -658,8 +659,11 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   P.a = g.a;
   P.nb = (g.n + KS_B - 1) / KS_B;
   P.nt = P.nb * (KS_B / K1_TS);
-  P.units = 0;
-  for (int b = 0; b < P.nb; ++b) P.units += P.nt - b * (KS_B / K1_TS);
+  long long tot = 0;
+  for (int b = 0; b < P.nb; ++b) tot += P.nt - b * (KS_B / K1_TS);
+  // sharded symmetric K1: this rank's equal share of the unordered (block, tile) units
+  P.ubeg = g.shard_world > 1 ? tot * g.shard_rank / g.shard_world : 0;
+  P.units = g.shard_world > 1 ? tot * (g.shard_rank + 1) / g.shard_world - P.ubeg : tot;
   const int nslot_max = KS_B / g.nq + 2;
   const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
                     (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * 2 * K1_TS)) * 8;
@@ -744,6 +748,15 @@ static void launch_asym(Geom& g, double* out, cudaStream_t st, int t0, int t1) {
   k1_allpairs<MODE><<<gr, K1_THREADS, 0, st>>>(P);
 }
 
+// the symmetric kernel needs tiles that span <= 2 spheres and the centres in shared memory
+static bool k1_sym_eligible(const Geom& g) { return g.nq >= K1_TS && g.np <= 4096; }
+
+// Sharded handle whose K1 runs the symmetric kernel over this rank's share of the units: the
+// partial sums cover every target row and must be reduce-scattered (layer.cu).
+bool k1_sharded_symmetric(const Geom& g) {
+  return g.shard_world > 1 && g.sh_rs_fn != nullptr && k1_symmetric() && k1_sym_eligible(g);
+}
+
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   const bool sym = k1_symmetric();
   constexpr int KS_B_MAX = 9216;  // multiple of every block size used (384 ... 1152)
@@ -751,7 +764,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
   g.packed.ensure((size_t)npad * 14);
   // symmetric kernel: tile spans <= 2 spheres, centres fit smem, all targets on this GPU
-  const bool use_sym = sym && g.nq >= K1_TS && g.np <= 4096 && g.shard_world == 1;
+  const bool use_sym = sym && k1_sym_eligible(g) && (g.shard_world == 1 || g.sh_rs_fn != nullptr);
   if (use_sym)
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
                                                    1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);

@@ -193,6 +193,12 @@ struct Geom {
   double *sh_send = nullptr, *sh_recv = nullptr;
   int (*sh_fn)(void* user) = nullptr;
   void* sh_user = nullptr;
+  // optional symmetric K1 when sharded (bpqn_geometry_shard_symmetric): every rank runs an equal
+  // share of the symmetric kernel's units over all targets; the partial sums go through
+  // sh_rs_fn (a reduce-scatter of [world][sh_rows][3] from sh_rs_send into sh_rs_recv)
+  double *sh_rs_send = nullptr, *sh_rs_recv = nullptr;
+  int (*sh_rs_fn)(void* user) = nullptr;
+  void* sh_rs_user = nullptr;
   std::vector<int> nt_list_h;  // host copy of the near-target list (shard ranges)
   ~Geom();
 };
@@ -212,6 +218,7 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
 double allpairs_flops_per_pair(int mode);
 void profile_collect(Geom& g);
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st);
+bool k1_sharded_symmetric(const Geom& g);
 void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st);
 void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
                       double* out, int accumulate, cudaStream_t st, int s0 = 0, int s1 = -1);

@@ -315,6 +315,7 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
     if (world == 1) {
       g->shard_world = 1;
       g->shard_rank = 0;
+      g->sh_rs_fn = nullptr;
       return BPQN_OK;
     }
     BPQN_REQUIRE(world <= g->np, "more ranks than spheres");
@@ -328,6 +329,29 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
     g->sh_fn = allgather;
     g->sh_user = user;
     shard_ranges(*g);
+    return BPQN_OK;
+  });
+}
+
+int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs_recv_dev,
+                                  int (*reduce_scatter)(void* user), void* user) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g, "null handle");
+    g->gm_graphs.clear();
+    g->gm_graphs.m = -1;
+    if (!reduce_scatter) {  // back to the one-directional K1 over the owned target rows
+      g->sh_rs_fn = nullptr;
+      g->sh_rs_send = g->sh_rs_recv = nullptr;
+      g->sh_rs_user = nullptr;
+      return BPQN_OK;
+    }
+    BPQN_REQUIRE(g->shard_world > 1, "handle is not sharded (call bpqn_geometry_shard first)");
+    BPQN_REQUIRE(rs_send_dev && rs_recv_dev, "null buffer");
+    BPQN_REQUIRE(g->nq >= 64 && g->np <= 4096, "symmetric K1 needs Nq >= 64 and Np <= 4096");
+    g->sh_rs_send = rs_send_dev;
+    g->sh_rs_recv = rs_recv_dev;
+    g->sh_rs_fn = reduce_scatter;
+    g->sh_rs_user = user;
     return BPQN_OK;
   });
 }

@@ -408,6 +408,28 @@ __global__ void k_shard_unpack(const double* __restrict__ recv, int world, int r
   if (k < 3 * (s1 - s0) * nq) out[3 * (size_t)s0 * nq + k] = recv[e];
 }
 
+// reduce-scatter of the sharded symmetric K1's partial sums: send[r][k] = far rows of rank r
+__global__ void k_rs_pack(const double* __restrict__ far, int world, int rows, int np, int nq,
+                          double* __restrict__ send) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= 3LL * rows * world) return;
+  const int r = (int)(e / (3LL * rows)), k = (int)(e - 3LL * rows * r);
+  const int s0 = (int)((long long)np * r / world), s1 = (int)((long long)np * (r + 1) / world);
+  send[e] = k < 3 * (s1 - s0) * nq ? far[3 * (size_t)s0 * nq + k] : 0.0;
+}
+
+static void shard_reduce_scatter(Geom& g, double* far, cudaStream_t st) {
+  const long long tot = 3LL * g.sh_rows * g.shard_world;
+  k_rs_pack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(far, g.shard_world, g.sh_rows, g.np, g.nq, g.sh_rs_send);
+  BPQN_CHECK_LAUNCH();
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  if (g.sh_rs_fn(g.sh_rs_user) != 0) throw Error{BPQN_ERR_CUDA, "shard reduce-scatter callback failed"};
+  // the owned rows of far <- the sum over ranks
+  BPQN_CUDA(cudaMemcpyAsync(far + 3 * (size_t)g.sh_t0, g.sh_rs_recv, sizeof(double) * 3 * (size_t)(g.sh_t1 - g.sh_t0),
+                            cudaMemcpyDeviceToDevice, st));
+  g.prof.launches += 1;
+}
+
 static void shard_exchange(Geom& g, double* out, cudaStream_t st) {
   const int nrow = g.sh_t1 - g.sh_t0;
   k_shard_pack<<<(3 * g.sh_rows + 255) / 256, 256, 0, st>>>(out, g.sh_t0, nrow, g.sh_send, g.sh_rows);
@@ -458,7 +480,10 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
   if (ev) {
     BPQN_CUDA(cudaEventRecord(ev[1], st));
-    const double ntg = g.shard_world > 1 ? (double)(g.sh_t1 - g.sh_t0) : (double)g.n;  // this rank's targets
+    // this rank's share of the nominal N^2 pairs
+    const double ntg = g.shard_world > 1 ? (k1_sharded_symmetric(g) ? (double)g.n / g.shard_world
+                                                                     : (double)(g.sh_t1 - g.sh_t0))
+                                         : (double)g.n;
     P.allpairs_flop += (double)g.n * ntg * allpairs_flops_per_pair(mode);
   }
   if (overlap) {
@@ -466,6 +491,7 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
     BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
   }
   const bool sharded = g.shard_world > 1;
+  if (sharded && k1_sharded_symmetric(g)) shard_reduce_scatter(g, g.far.p, st);
   const int s0 = sharded ? g.sh_s0 : 0, s1 = sharded ? g.sh_s1 : g.np;
   if (sigS && sigD) {
     launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st, s0, s1);

@@ -1,8 +1,10 @@
 """Sharded operator (bpqn_geometry_shard, NEXT-4) -- two or three ranks, one GPU, gloo all-gather.
 
 Each rank computes only its spheres' operator rows and the rows are all-gathered through
-the host (gloo); no kernel waits on another process, so two ranks may share the single
-GPU of the test box.  The sharded LCP MVP and mobility must equal the single-GPU result
+the host (gloo); with symmetric=True (bpqn_geometry_shard_symmetric) K1 is the symmetric
+kernel over each rank's share of the units and its partial sums are reduce-scattered (gloo:
+all-reduce of host copies) first.  No kernel waits on another process, so the ranks may
+share the single GPU of the test box.  The sharded LCP MVP and mobility must equal the single-GPU result
 (to GMRES tolerance: the sharded K1 is the one-directional kernel) and be bit-identical
 on both ranks (replicated deterministic GMRES)."""
 import json
@@ -29,7 +31,7 @@ torch.cuda.set_device(0)
 cfg = make_config({c})
 g = bp.Geometry(cfg["centers"], cfg["p"])
 bp.contacts(g, 0.1)
-bp.geometry_shard(g, rank, world)
+bp.geometry_shard(g, rank, world, symmetric={sym})
 gm = bp.default_gmres_opts(tol=1e-12)
 w, st = bp.lcp_mvp(g, torch.tensor(lambda_test({c}, g.nc, 0), device="cuda"), gmres=gm)
 uo, st2 = bp.mobility_apply(g, torch.tensor(np.ones((g.np, 6)) * 0.3, device="cuda"), gmres=gm)
@@ -47,8 +49,9 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("c,world", [(1, 2), (2, 2), (1, 3)])
-def test_sharded_mvp_two_ranks(c, world, tmp_path):
+@pytest.mark.parametrize("c,world,sym", [(1, 2, False), (2, 2, False), (1, 3, False),
+                                         (1, 2, True), (2, 2, True), (2, 3, True)])
+def test_sharded_mvp_two_ranks(c, world, sym, tmp_path):
     import torch
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
@@ -63,7 +66,7 @@ def test_sharded_mvp_two_ranks(c, world, tmp_path):
     w_ref, uo_ref = w_ref.cpu().numpy(), uo_ref.cpu().numpy().ravel()
     del g
     script = tmp_path / "w.py"
-    script.write_text(WORKER.format(root=ROOT, c=c))
+    script.write_text(WORKER.format(root=ROOT, c=c, sym=sym))
     env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_port()), WORLD_SIZE=str(world))
     procs = [subprocess.Popen([sys.executable, str(script)], env=dict(env, RANK=str(r), LOCAL_RANK=str(r)),
                               stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True) for r in range(world)]
