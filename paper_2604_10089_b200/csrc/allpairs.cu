@@ -689,6 +689,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
       occ.emplace_back(smem, grid);
     }
   }
+  if (P.units == 0) return;  // a rank with no share (more ranks than units); out stays zero
   const int gr = (int)std::min<long long>(grid, P.units);
   k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
 }
