@@ -237,7 +237,7 @@ struct ProxTimers {
               newton, calls ? (double)rsum / calls : 0.0, setup, jac, lu, resid);
   }
 };
-static ProxTimers g_pt;
+static thread_local ProxTimers g_pt;  // per solving thread (handles are single-owner)
 void prox_profile_flush() {  // BPQN_PQN_PROFILE: report and reset (called after each solve)
   if (!getenv("BPQN_PQN_PROFILE")) return;
   fprintf(stderr, "prox: calls %ld newton %ld avg r %.1f | setup %.3fs jac %.3fs lu %.3fs resid %.3fs\n", g_pt.calls,
