@@ -507,3 +507,17 @@ def test_lcp_mvp_c4_exact_covariance(bp, kind):
         ws.append(w.cpu().numpy())
         del g
     assert rel(ws[1], ws[0]) <= 1e-10
+
+
+def test_shard_argument_errors(bp):
+    """bpqn_geometry_shard / _symmetric reject bad ranks and an unsharded handle (code 1)."""
+    import ctypes
+    C, p = _scene("two_near_p6")
+    g = bp.Geometry(C, p)
+    L = bp.lib()
+    cb = bp._bpqn.ALLGATHER_FN(lambda _u: 0)
+    buf = ctypes.c_void_p(1)
+    assert L.bpqn_geometry_shard(g.h, 2, 2, buf, buf, cb, None) == 1          # rank >= world
+    assert L.bpqn_geometry_shard(g.h, 0, 3, buf, buf, cb, None) == 1          # more ranks than spheres
+    assert L.bpqn_geometry_shard_symmetric(g.h, buf, buf, cb, None) == 1      # not sharded
+    assert L.bpqn_geometry_shard_symmetric(g.h, None, None, bp._bpqn.ALLGATHER_FN(0), None) == 0  # disable: ok
