@@ -115,7 +115,8 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o);
 /* Build one discretisation of Np spheres of radius a in fluid of viscosity mu at
  * SH order p (grids R10, projection R7, self quadrature R5/R6, near rule R8):
  * grids, SH analysis, the per-sphere self operators E (FP64 tensor-core GEMM
- * operands) and the per-incidence near-correction matrices; workspace for GMRES.
+ * operands) and the per-incidence refined near-rule tensors in SH-coefficient space
+ * ([6][nb] per (target node, source sphere) incidence); workspace for GMRES.
  * centers_host [Np][3].  Fails with BPQN_ERR_INVALID if two spheres overlap. */
 int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius,
                        double mu, int p, const bpqn_disc_opts* opts, void* stream);

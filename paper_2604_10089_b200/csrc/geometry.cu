@@ -198,7 +198,7 @@ struct QuadParams {
   const double* w;         // [nq]
   const double* A;         // [nb][nq]
   ShTables T;
-  double* outS;            // [nprob][3][3nq]
+  double* outS;            // self rings: [nprob][3][3nq]; near incidences: [nprob][6][nb'] (K2 tensors)
   double* outD;
   int want_s;
 };

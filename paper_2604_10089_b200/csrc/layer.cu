@@ -1,6 +1,6 @@
 // The discrete layer operator on B200:
 //   K1  all-pairs coarse-rule Stokeslet / stresslet summation (FP64 pipe bound),
-//   K2  near-incidence correction: per (target, sphere) [3][3nq] blocks (HBM bound),
+//   K2  near-incidence correction: per (target, sphere) refined tensors in SH space [6][nb'] (HBM bound),
 //   K3  per-sphere self operator Y = E X on FP64 tensor cores (mma.sync f64, DMMA),
 //       whose epilogue also adds the K1 and K2 results.
 // Operator definition O6 of DESIGN.md (paper: P:130-136, P:423-426 treat it as a
