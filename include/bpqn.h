@@ -34,7 +34,7 @@ extern "C" {
 
 enum {
   BPQN_OK = 0,
-  BPQN_ERR_INVALID = 1,   /* null pointer, bad size, p < 2, a <= 0, mu <= 0, overlap, lambda < 0 */
+  BPQN_ERR_INVALID = 1,   /* null pointer, bad size, p < 2 or p > BPQN_P_MAX, a <= 0, mu <= 0, overlap, lambda < 0 */
   BPQN_ERR_CUDA = 2,      /* CUDA runtime error (message has the CUDA string) */
   BPQN_ERR_OOM = 3,       /* device allocation failed */
   BPQN_ERR_NOCONV = 4,    /* GMRES or PQN reached max iterations; outputs hold the last iterate */
@@ -118,6 +118,7 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o);
  * operands) and the per-incidence refined near-rule tensors in SH-coefficient space
  * ([6][nb] per (target node, source sphere) incidence); workspace for GMRES.
  * centers_host [Np][3].  Fails with BPQN_ERR_INVALID if two spheres overlap. */
+#define BPQN_P_MAX 25 /* largest SH order: the rule precompute holds 3 ceil(nb/2) <= 1024 tiles, nb = p^2 + 2p */
 int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius,
                        double mu, int p, const bpqn_disc_opts* opts, void* stream);
 int bpqn_geometry_destroy(bpqn_geom_t g);

@@ -235,6 +235,7 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
     BPQN_REQUIRE(out && centers_host, "null pointer");
     BPQN_REQUIRE(n_spheres >= 1, "n_spheres must be >= 1");
     BPQN_REQUIRE(p >= 2, "p must be >= 2");
+    BPQN_REQUIRE(p <= BPQN_P_MAX, "p must be <= 25 (precompute tile capacity)");
     BPQN_REQUIRE(radius > 0 && mu > 0, "radius and mu must be > 0");
     *out = nullptr;
     int dev = 0;
@@ -257,6 +258,9 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       g->n1 = o.near_n1 > 0 ? o.near_n1 : 2 * p + 16;
       g->n2 = o.near_n2 > 0 ? o.near_n2 : p + 8;
       g->nphi = o.near_nphi > 0 ? o.near_nphi : 4 * p;
+      // shared-memory tables of the rule precompute (geometry.cu k_quad_rows)
+      BPQN_REQUIRE(g->p_s + 1 <= 128 && 2 * g->p_s <= 256 && g->n1 + g->n2 <= 128 && g->nphi <= 256,
+                   "discretisation options exceed the precompute tables (p_s <= 63, n1 + n2 <= 128, nphi <= 256)");
       g->single_layer = o.build_single_layer != 0;
       const char* ov = getenv("BPQN_OVERLAP_K2");
       g->overlap_k2 = ov && ov[0] == '1';

@@ -296,7 +296,7 @@ __global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
   // accumulator tiles: 3 kk-blocks (4 each) x nb/2 b-blocks
   const int nbb = (nb + 1) / 2;
   const int ntile = 3 * nbb;
-  constexpr int MAXT = 4;  // tiles per thread (nb <= 2*QT*MAXT/3 ... checked on host)
+  constexpr int MAXT = 4;  // tiles per thread: 3 ceil(nb/2) <= QT MAXT, i.e. p <= BPQN_P_MAX (checked on host)
   double acc[MAXT][8];
 #pragma unroll
   for (int u = 0; u < MAXT; ++u)

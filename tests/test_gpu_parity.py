@@ -133,10 +133,12 @@ def test_mobility_small(bp, name):
     assert st.rel_resid <= 1e-12
 
 
-def test_mobility_single_sphere_stokes_drag(bp):
-    """GPU path against the closed form U = F/(6 pi mu a), Omega = T/(8 pi mu a^3) (App. A.1)."""
+@pytest.mark.parametrize("p", [10, 25])
+def test_mobility_single_sphere_stokes_drag(bp, p):
+    """GPU path against the closed form U = F/(6 pi mu a), Omega = T/(8 pi mu a^3) (App. A.1);
+    p = 25 is the largest supported order (the precompute's full tile capacity)."""
     a, mu = 1.3, 0.7
-    g = bp.Geometry(np.array([[1.0, -2.0, 0.5]]), 10, radius=a, mu=mu)
+    g = bp.Geometry(np.array([[1.0, -2.0, 0.5]]), p, radius=a, mu=mu)
     FT = np.array([[0.3, -1.2, 0.8, 0.5, 0.1, -0.7]])
     uo, _ = bp.mobility_apply(g, T(FT), gmres=bp.default_gmres_opts(**GM_PARITY))
     uo = uo.cpu().numpy()[0]
@@ -202,6 +204,10 @@ def test_overlap_and_bad_args_rejected(bp):
     with pytest.raises(bp.BpqnError) as e:
         bp.Geometry(np.array([[0.0, 0.0, 0.0]]), 1)
     assert e.value.code == 1
+    with pytest.raises(bp.BpqnError) as e:          # beyond the precompute's tile capacity
+        bp.Geometry(np.array([[0.0, 0.0, 0.0]]), 26)
+    assert e.value.code == 1
+    bp.Geometry(np.array([[0.0, 0.0, 0.0]]), 25)    # the largest supported order builds
 
 
 def test_nan_input_reported(bp):
