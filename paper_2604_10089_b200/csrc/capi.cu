@@ -316,10 +316,14 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");
     BPQN_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+    // any (re)sharding drops a previous symmetric-K1 registration: its buffers were sized for
+    // the old world (bpqn_geometry_shard_symmetric must be called again)
+    g->sh_rs_fn = nullptr;
+    g->sh_rs_send = g->sh_rs_recv = nullptr;
+    g->sh_rs_user = nullptr;
     if (world == 1) {
       g->shard_world = 1;
       g->shard_rank = 0;
-      g->sh_rs_fn = nullptr;
       return BPQN_OK;
     }
     BPQN_REQUIRE(world <= g->np, "more ranks than spheres");
