@@ -707,10 +707,34 @@ static int k1_cfg() {
   return v;
 }
 
+static int sym_cfg(const Geom& g, int mode) {
+  const int c = k1_cfg();
+  if (c >= 0) return c;
+  return g.n >= 60000 ? (mode == MODE_SD ? 4 : 14) : (g.n >= 20000 ? 4 : 3);
+}
+
+// target-block size 32 W R of each launch shape (must match launch_sym's table): the packed
+// records must cover nb blocks of it
+static int sym_block_points(int c) {
+  switch (c) {
+    case 1: case 5: case 8: return 32 * 12 * 3;
+    case 2: return 32 * 16 * 2;
+    case 3: case 9: return 32 * 8 * 3;
+    case 4: case 10: return 32 * 8 * 4;
+    case 6: return 32 * 4 * 3;
+    case 7: return 32 * 6 * 3;
+    case 11: return 32 * 4 * 4;
+    case 12: case 13: return 32 * 12 * 4;
+    case 14: return 32 * 8 * 5;
+    case 15: return 32 * 8 * 6;
+    case 16: return 32 * 4 * 6;
+    default: return 32 * 8 * 2;
+  }
+}
+
 template <int MODE>
 static void launch_sym(Geom& g, double* out, cudaStream_t st) {
-  int c = k1_cfg();
-  if (c < 0) c = g.n >= 60000 ? (MODE == MODE_SD ? 4 : 14) : (g.n >= 20000 ? 4 : 3);
+  const int c = sym_cfg(g, MODE);
   switch (c) {
     case 1: launch_sym_cfg<MODE, 12, 3, 1>(g, out, st); break;
     case 2: launch_sym_cfg<MODE, 16, 2, 1>(g, out, st); break;
@@ -760,12 +784,13 @@ bool k1_sharded_symmetric(const Geom& g) {
 
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   const bool sym = k1_symmetric();
-  constexpr int KS_B_MAX = 9216;  // multiple of every block size used (384 ... 1152)
-  // packed records cover every target block / source tile of either variant
-  const int npad = ((g.n + KS_B_MAX - 1) / KS_B_MAX) * KS_B_MAX;
-  g.packed.ensure((size_t)npad * 14);
   // symmetric kernel: tile spans <= 2 spheres, centres fit smem, all targets on this GPU
   const bool use_sym = sym && k1_sym_eligible(g) && (g.shard_world == 1 || g.sh_rs_fn != nullptr);
+  // packed records cover every target block (symmetric: nb blocks of the launch shape) and
+  // source tile (one-directional: 64-point tiles); the padding is far away, zero strength
+  const int blk = use_sym ? sym_block_points(sym_cfg(g, mode)) : K1_TS;
+  const int npad = ((g.n + blk - 1) / blk) * blk;
+  g.packed.ensure((size_t)npad * 14);
   if (use_sym)
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
                                                    1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);

@@ -118,6 +118,27 @@ def test_layer_apply_config_sampled(bp, c):
     assert np.isfinite(u).all()
 
 
+def test_layer_apply_block_padding_regression(bp):
+    """118 spheres at p = 16: N = 64 192 lies just above a multiple of the symmetric K1's
+    1280-point target block but below the next 9216 -- the packed records must cover the
+    last block for every launch shape.  An S+D apply first leaves 80-byte records in the
+    buffer; the D and S applies that follow must not read them as sources."""
+    from oracle.layer import Disc
+    rng = np.random.default_rng(7)
+    g1 = np.arange(5) * 2.05
+    C = np.array([[x, y, z] for x in g1 for y in g1 for z in g1])[:118] + rng.uniform(-0.01, 0.01, (118, 3))
+    d = Disc(C, 16)
+    g = bp.Geometry(C, 16)
+    assert g.N == 64192
+    f, q = rng.standard_normal((g.N, 3)), rng.standard_normal((g.N, 3))
+    bp.layer_apply(g, f=T(f), q=T(q))
+    tg = _sample_targets(d, 24, 7)
+    ud = bp.layer_apply(g, q=T(q)).cpu().numpy()
+    assert rel(ud[tg], d.apply(q=q, targets=tg)) <= TOL_SUM
+    us = bp.layer_apply(g, f=T(f)).cpu().numpy()
+    assert rel(us[tg], d.apply(f=f, targets=tg)) <= TOL_SUM
+
+
 # ------------------------------------------------------------------ mobility (K4 GMRES)
 @pytest.mark.parametrize("name", ["two_near_p6", "three_p5", "single_p7"])
 def test_mobility_small(bp, name):
