@@ -128,19 +128,52 @@ bool Bfgs::update(const Vec& s, const Vec& y, const Vec* Bs_in, double curv) {
 // earlier secant pair, so r reaches a few hundred, "full memory").
 static bool par(long long work) { return work > 200000; }
 
-// C[m x p] = A[m x k] B[p x k]^T (+ C if acc)
+// C[m x p] = A[m x k] B[p x k]^T (+ C if acc).  2 x 4 register blocks of C (each A / B row
+// chunk is reused 4 / 2 times from registers), the k loop vectorised; OpenMP over row pairs.
 static void gemm_nt(const double* A, const double* B, double* C, int m, int p, int k, bool acc) {
-#pragma omp parallel for schedule(static) if (par((long long)m * p * k))
-  for (int i = 0; i < m; ++i) {
-    const double* a = A + (size_t)i * k;
-    for (int j = 0; j < p; ++j) {
-      const double* bb = B + (size_t)j * k;
-      double s = 0.0;
+  const int m2 = m / 2 * 2, p4 = p / 4 * 4;
+  auto put = [&](int i, int j, double s) { C[(size_t)i * p + j] = acc ? C[(size_t)i * p + j] + s : s; };
+  auto dot = [&](const double* a, const double* b) {
+    double s = 0.0;
 #pragma omp simd reduction(+ : s)
-      for (int e = 0; e < k; ++e) s += a[e] * bb[e];
-      C[(size_t)i * p + j] = acc ? C[(size_t)i * p + j] + s : s;
+    for (int e = 0; e < k; ++e) s += a[e] * b[e];
+    return s;
+  };
+#pragma omp parallel for schedule(static) if (par((long long)m * p * k))
+  for (int i = 0; i < m2; i += 2) {
+    const double* a0 = A + (size_t)i * k;
+    const double* a1 = a0 + k;
+    for (int j = 0; j < p4; j += 4) {
+      const double *b0 = B + (size_t)j * k, *b1 = b0 + k, *b2 = b1 + k, *b3 = b2 + k;
+      double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s10 = 0, s11 = 0, s12 = 0, s13 = 0;
+#pragma omp simd reduction(+ : s00, s01, s02, s03, s10, s11, s12, s13)
+      for (int e = 0; e < k; ++e) {
+        const double x0 = a0[e], x1 = a1[e];
+        s00 += x0 * b0[e];
+        s01 += x0 * b1[e];
+        s02 += x0 * b2[e];
+        s03 += x0 * b3[e];
+        s10 += x1 * b0[e];
+        s11 += x1 * b1[e];
+        s12 += x1 * b2[e];
+        s13 += x1 * b3[e];
+      }
+      put(i, j, s00);
+      put(i, j + 1, s01);
+      put(i, j + 2, s02);
+      put(i, j + 3, s03);
+      put(i + 1, j, s10);
+      put(i + 1, j + 1, s11);
+      put(i + 1, j + 2, s12);
+      put(i + 1, j + 3, s13);
+    }
+    for (int j = p4; j < p; ++j) {
+      put(i, j, dot(a0, B + (size_t)j * k));
+      put(i + 1, j, dot(a1, B + (size_t)j * k));
     }
   }
+  for (int i = m2; i < m; ++i)
+    for (int j = 0; j < p; ++j) put(i, j, dot(A + (size_t)i * k, B + (size_t)j * k));
 }
 
 // in-place Cholesky K = L L^T (lower), false if not positive definite
