@@ -413,7 +413,6 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
   const std::vector<double>& CV = q.wc.CV;
   const int d = 2 * r;
   g_pt.setup += now_s() - t_0;
-  Vec al(d, 0.0);  // [alpha; alpha~]
   auto residual = [&](const Vec& a, Vec& L, Vec& z, std::vector<char>& act) {
     Vec y = xt, v(n);
     for (int c = 0; c < r; ++c) {
@@ -452,90 +451,112 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     for (double x : v) m = std::max(m, std::fabs(x));
     return m;
   };
-  Vec L, z;
-  std::vector<char> act;
-  residual(al, L, z, act);
-  double nr = infn(L);
+  // semi-smooth Newton from a0 (Alg. 4); returns the residual norm reached
+  Vec z;
   int j = 0;
-  std::vector<double> Ua, Va, CVa, Ui, CVi, blk((size_t)r * r);
-  for (j = 0; j < jmax && nr > tol; ++j) {
-    g_pt.newton++;
-    double t_1 = now_s();
-    // J = [[U^T Lam U, U^T (I-Lam) CV], [V^T Lam U, -V^T Lam CV]] + I
-    std::vector<int> ia, ii;
-    for (int e = 0; e < n; ++e) (act[e] ? ia : ii).push_back(e);
-    const int na = (int)ia.size(), ni = (int)ii.size();
-    Ua.assign((size_t)r * na, 0.0);
-    Va.assign((size_t)r * na, 0.0);
-    CVa.assign((size_t)r * na, 0.0);
-    Ui.assign((size_t)r * ni, 0.0);
-    CVi.assign((size_t)r * ni, 0.0);
-    for (int c = 0; c < r; ++c) {
-      for (int t = 0; t < na; ++t) {
-        Ua[(size_t)c * na + t] = Um[(size_t)c * n + ia[t]];
-        Va[(size_t)c * na + t] = Vm[(size_t)c * n + ia[t]];
-        CVa[(size_t)c * na + t] = CV[(size_t)c * n + ia[t]];
+  auto newton = [&](Vec al) -> double {
+    Vec L;
+    std::vector<char> act;
+    residual(al, L, z, act);
+    double nr = infn(L);
+    std::vector<double> Ua, Va, CVa, Ui, CVi, blk((size_t)r * r);
+    int jj;
+    for (jj = 0; jj < jmax && nr > tol; ++jj) {
+      g_pt.newton++;
+      double t_1 = now_s();
+      // J = [[U^T Lam U, U^T (I-Lam) CV], [V^T Lam U, -V^T Lam CV]] + I
+      std::vector<int> ia, ii;
+      for (int e = 0; e < n; ++e) (act[e] ? ia : ii).push_back(e);
+      const int na = (int)ia.size(), ni = (int)ii.size();
+      Ua.assign((size_t)r * na, 0.0);
+      Va.assign((size_t)r * na, 0.0);
+      CVa.assign((size_t)r * na, 0.0);
+      Ui.assign((size_t)r * ni, 0.0);
+      CVi.assign((size_t)r * ni, 0.0);
+      for (int c = 0; c < r; ++c) {
+        for (int t = 0; t < na; ++t) {
+          Ua[(size_t)c * na + t] = Um[(size_t)c * n + ia[t]];
+          Va[(size_t)c * na + t] = Vm[(size_t)c * n + ia[t]];
+          CVa[(size_t)c * na + t] = CV[(size_t)c * n + ia[t]];
+        }
+        for (int t = 0; t < ni; ++t) {
+          Ui[(size_t)c * ni + t] = Um[(size_t)c * n + ii[t]];
+          CVi[(size_t)c * ni + t] = CV[(size_t)c * n + ii[t]];
+        }
       }
-      for (int t = 0; t < ni; ++t) {
-        Ui[(size_t)c * ni + t] = Um[(size_t)c * n + ii[t]];
-        CVi[(size_t)c * ni + t] = CV[(size_t)c * n + ii[t]];
+      std::vector<double> J((size_t)d * d, 0.0);
+      auto put = [&](int r0, int c0, double sgn) {
+        for (int a = 0; a < r; ++a)
+          for (int b = 0; b < r; ++b) J[(size_t)(r0 + a) * d + c0 + b] = sgn * blk[(size_t)a * r + b];
+      };
+      gemm_nt(Ua.data(), Ua.data(), blk.data(), r, r, na, false);
+      put(0, 0, 1.0);
+      gemm_nt(Ui.data(), CVi.data(), blk.data(), r, r, ni, false);
+      put(0, r, 1.0);
+      gemm_nt(Va.data(), Ua.data(), blk.data(), r, r, na, false);
+      put(r, 0, 1.0);
+      gemm_nt(Va.data(), CVa.data(), blk.data(), r, r, na, false);
+      put(r, r, -1.0);
+      for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1.0;
+      double t_2 = now_s();
+      g_pt.jac += t_2 - t_1;
+      Vec step = L;
+      std::vector<double> Jc = J;
+      const bool lu_ok = lu_solve_par(Jc, d, step);
+      g_pt.lu += now_s() - t_2;
+      t_2 = now_s();
+      if (!lu_ok) {
+        double jn = 0;
+        for (double v : J) jn = std::max(jn, std::fabs(v));
+        for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1e-10 * jn * d;
+        step = L;
+        if (!lu_solve_par(J, d, step)) break;
       }
-    }
-    std::vector<double> J((size_t)d * d, 0.0);
-    auto put = [&](int r0, int c0, double sgn) {
-      for (int a = 0; a < r; ++a)
-        for (int b = 0; b < r; ++b) J[(size_t)(r0 + a) * d + c0 + b] = sgn * blk[(size_t)a * r + b];
-    };
-    gemm_nt(Ua.data(), Ua.data(), blk.data(), r, r, na, false);
-    put(0, 0, 1.0);
-    gemm_nt(Ui.data(), CVi.data(), blk.data(), r, r, ni, false);
-    put(0, r, 1.0);
-    gemm_nt(Va.data(), Ua.data(), blk.data(), r, r, na, false);
-    put(r, 0, 1.0);
-    gemm_nt(Va.data(), CVa.data(), blk.data(), r, r, na, false);
-    put(r, r, -1.0);
-    for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1.0;
-    double t_2 = now_s();
-    g_pt.jac += t_2 - t_1;
-    Vec step = L;
-    std::vector<double> Jc = J;
-    const bool lu_ok = lu_solve_par(Jc, d, step);
-    g_pt.lu += now_s() - t_2;
-    t_2 = now_s();
-    if (!lu_ok) {
-      double jn = 0;
-      for (double v : J) jn = std::max(jn, std::fabs(v));
-      for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1e-10 * jn * d;
-      step = L;
-      if (!lu_solve_par(J, d, step)) break;
-    }
-    double t = 1.0;
-    bool ok = false;
-    Vec a2(d), L2, z2;
-    std::vector<char> act2;
-    double n2 = nr;
-    for (int h = 0; h < 30; ++h) {
-      for (int i = 0; i < d; ++i) a2[i] = al[i] - t * step[i];
-      residual(a2, L2, z2, act2);
-      n2 = infn(L2);
-      if (n2 < nr || n2 <= tol) {
-        ok = true;
+      double t = 1.0;
+      bool ok = false;
+      Vec a2(d), L2, z2;
+      std::vector<char> act2;
+      double n2 = nr;
+      for (int h = 0; h < 30; ++h) {
+        for (int i = 0; i < d; ++i) a2[i] = al[i] - t * step[i];
+        residual(a2, L2, z2, act2);
+        n2 = infn(L2);
+        if (n2 < nr || n2 <= tol) {
+          ok = true;
+          break;
+        }
+        t *= 0.5;
+      }
+      if (!ok) break;
+      double smax = t * infn(step);
+      g_pt.resid += now_s() - t_2;
+      al = a2;
+      L = L2;
+      z = z2;
+      act = act2;
+      nr = n2;
+      if (smax < tol) {
+        ++jj;
         break;
       }
-      t *= 0.5;
     }
-    if (!ok) break;
-    double smax = t * infn(step);
-    g_pt.resid += now_s() - t_2;
-    al = a2;
-    L = L2;
-    z = z2;
-    act = act2;
-    nr = n2;
-    if (smax < tol) {
-      ++j;
-      break;
+    j += jj;
+    if (nr <= tol) {  // keep the root for the next call on this memory
+      q.wc.alpha = al;
+      q.wc.alpha_r = r;
     }
+    return nr;
+  };
+  const WoodburyCache& W = q.wc;
+  if (W.alpha_r > 0 && W.alpha_r <= r && (int)W.alpha.size() == 2 * W.alpha_r) {
+    Vec a0(d, 0.0);
+    for (int c = 0; c < W.alpha_r; ++c) {
+      a0[c] = W.alpha[c];
+      a0[r + c] = W.alpha[W.alpha_r + c];
+    }
+    if (newton(a0) > tol) newton(Vec(d, 0.0));  // warm start failed: from zero as before
+  } else {
+    newton(Vec(d, 0.0));
   }
   if (iters) *iters = j;
   return z;

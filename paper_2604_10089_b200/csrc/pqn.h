@@ -26,6 +26,10 @@ struct PqnOpts {
 struct WoodburyCache {
   int r = 0, n = 0, appends = 0;
   std::vector<double> Um, Vm, CU, CV;  // [r][n] row-major
+  // dual root [alpha; alpha~] of the last prox call and its rank: the next call on the same
+  // (appended) memory starts its semi-smooth Newton from it, padded with zeros
+  std::vector<double> alpha;
+  int alpha_r = 0;
 };
 
 struct Bfgs {
