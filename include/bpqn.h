@@ -231,7 +231,7 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
  * and, after synchronising the handle's stream, calls reduce_scatter(user), which must write
  * into rs_recv_dev ([rows][3]) the element-wise sum over ranks of their chunk for this rank
  * (e.g. NCCL reduce_scatter_tensor) and return 0; K2 / K3 and the all-gather follow as in
- * bpqn_geometry_shard.  Needs Nq >= 64 and Np <= 4096 (else error 1).  A NULL callback
+ * bpqn_geometry_shard.  Needs Nq >= 32 (p >= 4) and Np <= 4096 (else error 1).  A NULL callback
  * switches back to the one-directional kernel, and so does every later bpqn_geometry_shard
  * call (the buffers are sized for one world).  Buffers and user stay owned by the caller. */
 int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs_recv_dev,

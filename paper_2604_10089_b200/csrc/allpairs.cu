@@ -303,8 +303,9 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
 //    are reduced through shared memory and added with one fp64 atomic per value.
 //  * sources are points of spheres of radius a, so r.n_y = (h_m(x) - rho^2) / (2a) with
 //    h_m(x) = |x - c_m|^2 - a^2 per (target, source sphere): the forward r.n costs one FMA
-//    and the records carry no normals.  A 64-point tile spans at most two spheres
-//    (Nq >= 64 is checked), so each target keeps h for both (recomputed per tile).
+//    and the records carry no normals.  A 32-point source group spans at most two spheres
+//    (Nq >= 32 is checked), so each target keeps h for both (recomputed when the group's first
+//    sphere changes).
 struct K1SymParams {
   const double* pk;       // packed records [npad][RecS] (targets and sources)
   const double* centers;  // [Np][3]
@@ -545,24 +546,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
         acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
       }
     }
-    // source spheres of this tile: first m0, second from in-tile index jb on
     const int s0 = t_cur * K1_TS;
-    const int m0 = min(s0 / P.nq, P.np - 1);
-    const int m1 = min(m0 + 1, P.np - 1);
-    const int jb = (m0 + 1) * P.nq - s0;
-    if (MODE != MODE_S && (m0 != h_m0 || b_cur != h_b)) {  // h per (target, source sphere)
-      h_m0 = m0;
-      h_b = b_cur;
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const double* c = cs + 3 * (q ? m1 : m0);
-          const double d0 = tg[r][0] - c[0], d1 = tg[r][1] - c[1], d2 = tg[r][2] - c[2];
-          hs[r][q] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
-        }
-      }
-    }
     const bool diag = t_cur < (b_cur + 1) * TPB;
     mbar_wait(&full[buf], parity);
     if (MODE != MODE_S && !diag) {  // H[slot][j] = (|y_j - c_slot|^2 - a^2)/(2a) for this tile,
@@ -581,9 +565,28 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     }
 #pragma unroll 1
     for (int grp = 0; grp < K1_TS / 32; ++grp) {
+      // source spheres of this 32-point group (Nq >= 32: at most two): the first m0, the
+      // second from in-tile index jb on; h per (target, source sphere) when m0 changes
+      const int sg0 = s0 + 32 * grp;
+      const int m0 = min(sg0 / P.nq, P.np - 1);
+      const int m1 = min(m0 + 1, P.np - 1);
+      const int jb = 32 * grp + (m0 + 1) * P.nq - sg0;
+      if (MODE != MODE_S && (m0 != h_m0 || b_cur != h_b)) {
+        h_m0 = m0;
+        h_b = b_cur;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double* c = cs + 3 * (q ? m1 : m0);
+            const double d0 = tg[r][0] - c[0], d1 = tg[r][1] - c[1], d2 = tg[r][2] - c[2];
+            hs[r][q] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+          }
+        }
+      }
       const double* gr = ring[buf] + grp * 32 * REC;
       double as0 = 0.0, as1 = 0.0, as2 = 0.0;
-      const bool mixed = grp * 32 < jb && grp * 32 + 32 > jb;
+      const bool mixed = jb < grp * 32 + 32;
       if (diag) {
         k1_group<MODE, R, false, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
       } else {
@@ -774,7 +777,7 @@ static void launch_asym(Geom& g, double* out, cudaStream_t st, int t0, int t1) {
 }
 
 // the symmetric kernel needs tiles that span <= 2 spheres and the centres in shared memory
-static bool k1_sym_eligible(const Geom& g) { return g.nq >= K1_TS && g.np <= 4096; }
+static bool k1_sym_eligible(const Geom& g) { return g.nq >= 32 && g.np <= 4096; }
 
 // Sharded handle whose K1 runs the symmetric kernel over this rank's share of the units: the
 // partial sums cover every target row and must be reduce-scattered (layer.cu).
@@ -784,7 +787,8 @@ bool k1_sharded_symmetric(const Geom& g) {
 
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   const bool sym = k1_symmetric();
-  // symmetric kernel: tile spans <= 2 spheres, centres fit smem, all targets on this GPU
+  // symmetric kernel: a 32-point group spans <= 2 spheres, centres fit smem, all targets on this
+  // GPU (or the sharded symmetric split with its reduce-scatter)
   const bool use_sym = sym && k1_sym_eligible(g) && (g.shard_world == 1 || g.sh_rs_fn != nullptr);
   // packed records cover every target block (symmetric: nb blocks of the launch shape) and
   // source tile (one-directional: 64-point tiles); the padding is far away, zero strength

@@ -355,7 +355,7 @@ int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs
     }
     BPQN_REQUIRE(g->shard_world > 1, "handle is not sharded (call bpqn_geometry_shard first)");
     BPQN_REQUIRE(rs_send_dev && rs_recv_dev, "null buffer");
-    BPQN_REQUIRE(g->nq >= 64 && g->np <= 4096, "symmetric K1 needs Nq >= 64 and Np <= 4096");
+    BPQN_REQUIRE(g->nq >= 32 && g->np <= 4096, "symmetric K1 needs Nq >= 32 (p >= 4) and Np <= 4096");
     g->sh_rs_send = rs_send_dev;
     g->sh_rs_recv = rs_recv_dev;
     g->sh_rs_fn = reduce_scatter;
