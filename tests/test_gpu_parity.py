@@ -84,6 +84,38 @@ def test_layer_apply_small(bp, name):
     assert rel(usd, ref_s + ref_d) <= TOL_SUM
 
 
+def _random_scene(seed):
+    """Seeded random packing: 2-12 unit spheres, gaps >= 0.01, order p in 3..9 (both K1 variants,
+    ragged target blocks and source tiles, near and far pairs)."""
+    rng = np.random.default_rng(1000 + seed)
+    np_, p = int(rng.integers(2, 13)), int(rng.integers(3, 10))
+    C = []
+    while len(C) < np_:
+        c = rng.uniform(0.0, 2.6 * np_ ** (1 / 3) + 1.0, 3)
+        if all(np.linalg.norm(c - o) >= 2.01 for o in C):
+            C.append(c)
+    return np.array(C), p
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_layer_apply_random_scenes(bp, seed):
+    """All targets of seeded random scenes (every mode) against the oracle's full apply."""
+    from oracle.layer import Disc
+    C, p = _random_scene(seed)
+    d = Disc(C, p)
+    g = bp.Geometry(C, p)
+    assert g.N == d.N and g.n_incidences == len(d.inc)
+    rng = np.random.default_rng(seed)
+    f, q = rng.standard_normal((d.N, 3)), rng.standard_normal((d.N, 3))
+    ref_s, ref_d = d.apply_all(f=f), d.apply_all(q=q)
+    usd = bp.layer_apply(g, f=T(f), q=T(q)).cpu().numpy()
+    ud = bp.layer_apply(g, q=T(q)).cpu().numpy()
+    us = bp.layer_apply(g, f=T(f)).cpu().numpy()
+    assert rel(us, ref_s) <= TOL_SUM, (C.shape[0], p)
+    assert rel(ud, ref_d) <= TOL_SUM, (C.shape[0], p)
+    assert rel(usd, ref_s + ref_d) <= TOL_SUM, (C.shape[0], p)
+
+
 def test_layer_apply_none_is_zero(bp):
     C, p = _scene("three_p5")
     g = bp.Geometry(C, p)
