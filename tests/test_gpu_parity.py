@@ -171,6 +171,24 @@ def test_layer_apply_block_padding_regression(bp):
     assert rel(us[tg], d.apply(f=f, targets=tg)) <= TOL_SUM
 
 
+@pytest.mark.parametrize("nsph,p", [(70, 12), (41, 16)])
+def test_layer_apply_ragged_blocks(bp, nsph, p):
+    """Mid-size scenes whose N is not a multiple of the K1 target block (70 x 312 = 21 840
+    with 1024-point blocks; 41 x 544 = 22 304), sampled targets against the oracle."""
+    from oracle.layer import Disc
+    rng = np.random.default_rng(nsph)
+    g1 = np.arange(5) * 2.04
+    C = np.array([[x, y, z] for x in g1 for y in g1 for z in g1])[:nsph] + rng.uniform(-0.01, 0.01, (nsph, 3))
+    d = Disc(C, p)
+    g = bp.Geometry(C, p)
+    f, q = rng.standard_normal((g.N, 3)), rng.standard_normal((g.N, 3))
+    u = bp.layer_apply(g, f=T(f), q=T(q)).cpu().numpy()
+    tg = _sample_targets(d, 24, nsph)
+    assert rel(u[tg], d.apply(f=f, q=q, targets=tg)) <= TOL_SUM
+    ud = bp.layer_apply(g, q=T(q)).cpu().numpy()
+    assert rel(ud[tg], d.apply(q=q, targets=tg)) <= TOL_SUM
+
+
 # ------------------------------------------------------------------ mobility (K4 GMRES)
 @pytest.mark.parametrize("name", ["two_near_p6", "three_p5", "single_p7"])
 def test_mobility_small(bp, name):
