@@ -17,6 +17,7 @@ namespace bpqn {
 
 constexpr int GT = 256;
 constexpr int GM_MAX_RESTART = 500;
+constexpr int GM_MAX_COEF = 1024;  // coefficient vectors in shared memory: restart or recycle count
 
 // partial dots red[i * nbx + bx] = sum_{e in slice bx} V_i[e] * w[e], i = blockIdx.y
 __global__ void k_mdot(const double* __restrict__ V, size_t ld, const double* __restrict__ w, size_t n,
@@ -72,7 +73,7 @@ __global__ void k_reduce_rows(const double* red, int nbx, double* out, int accum
 // w -= sum_{i<kv} V_i h_i ; red[bx] = partial |w|^2 (if red)
 __global__ void k_mupdate(const double* __restrict__ V, size_t ld, int kv, const double* __restrict__ h,
                           double* w, size_t n, double* red, int nbx) {
-  __shared__ double sh[GM_MAX_RESTART + 1];
+  __shared__ double sh[GM_MAX_COEF + 1];
   for (int i = threadIdx.x; i < kv; i += blockDim.x) sh[i] = h[i];
   __syncthreads();
   double nrm = 0.0;
@@ -194,7 +195,7 @@ __global__ void k_init_cycle(double* S, GmLayout L, double beta) {
 
 // x += V[0:kk] y  (y on device)
 __global__ void k_add_basis(const double* __restrict__ V, size_t ld, int kk, const double* y, double* x, size_t n) {
-  __shared__ double sy[GM_MAX_RESTART + 1];
+  __shared__ double sy[GM_MAX_COEF + 1];
   for (int i = threadIdx.x; i < kk; i += blockDim.x) sy[i] = y[i];
   __syncthreads();
   for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
@@ -428,8 +429,9 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   // A_op Z = W (to the past solves' tolerance).  Initial guess x0 = Z W^T b.  Plus a
   // deflation space (U, C = A~ U) built after the first solve (GCRO, R33b).
   const bool rec = o.recycle != 0 && beta_b > 0.0 && std::isfinite(beta_b);
-  if (rec && g.rec_cap == 0) {  // lazily: up to 256 pairs within ~4 GB
-    g.rec_cap = (int)std::max<size_t>(1, std::min<size_t>(256, (size_t)4e9 / (2 * n * sizeof(double))));
+  if (rec && g.rec_cap == 0) {  // lazily: up to GM_MAX_COEF pairs within ~4 GB (the right-hand sides of
+    // LCP MVPs span at most Nc dimensions, so a store of >= Nc pairs ends up predicting them exactly)
+    g.rec_cap = (int)std::max<size_t>(1, std::min<size_t>(GM_MAX_COEF, (size_t)4e9 / (2 * n * sizeof(double))));
     g.rec_W.alloc((size_t)g.rec_cap * n);
     g.rec_Z.alloc((size_t)g.rec_cap * n);
     g.rec_k = 0;
