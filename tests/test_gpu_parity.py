@@ -420,6 +420,27 @@ def test_gmres_recycling_same_result_fewer_iterations(bp):
     assert abs(st_reset.iters - st_cold.iters) <= 1   # fp64 atomics: summation order may differ
 
 
+def test_gmres_recycling_spans_rhs_space(bp):
+    """An LCP's MVP right-hand sides are linear in lambda (<= Nc dimensions): once the store
+    holds Nc independent solves (c1: Nc = 12), any further MVP starts from an exact guess,
+    converges in a few iterations (the stored solves' own 1e-12 residuals combine) instead of
+    ~60 cold, and equals the oracle's A lambda (the store's capacity, up to 1024 pairs,
+    exceeds Nc)."""
+    z = fixture(1)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    bp.contacts(g, 0.1)
+    warm = bp.default_gmres_opts(tol=1e-12, recycle=1)
+    bp.gmres_recycle_reset(g)
+    rng = np.random.default_rng(3)
+    for _ in range(g.nc):
+        bp.lcp_mvp(g, T(rng.uniform(0.0, 1.0, g.nc)), gmres=warm)
+    lam = rng.uniform(0.0, 1.0, g.nc)
+    w, st = bp.lcp_mvp(g, T(lam), gmres=warm)
+    _, st_cold = bp.lcp_mvp(g, T(lam), gmres=bp.default_gmres_opts(tol=1e-12))
+    assert st.iters <= 6 and st.iters * 5 < st_cold.iters, (st.iters, st_cold.iters)
+    assert rel(w.cpu().numpy(), z["A_dense"] @ lam) <= TOL_VEL
+
+
 @pytest.mark.parametrize("c", [1, 2])
 def test_solve_lcp_bb_pgd(bp, c):
     """BB-PGD (method 2) on the device MVP reaches the unique LCP solution (R30)."""
