@@ -99,12 +99,17 @@ typedef struct {
   double sub_forcing;         /* Bi-PQN only, default 0 (off, R22): > 0 solves each subproblem to
                                  max(sub_eps_factor eps, sub_forcing * current hi KKT error)
                                  (inexact proximal Newton; not in the paper) */
+  int verify_secants;         /* Bi-PQN, test-only (default 0): before every subproblem measure
+                                 max_j |B^(k) s_j - y_j|_inf / max(1, |y_j|_inf) over the re-used
+                                 secant pairs (reading R34) with extra, uncounted lo MVPs;
+                                 reported in bpqn_report.secant_residual */
 } bpqn_solve_opts;
 
 typedef struct {
   int iterations, hi_mvps, lo_mvps, gmres_iters_hi, gmres_iters_lo;
   double e_mvps, cost_ratio, kkt_abs, kkt_rel, objective, ms_total, ms_hi, ms_lo;
   int termination;            /* 0 KKT_ABS, 1 KKT_REL, 2 MAX_ITER, 3 STALLED */
+  double secant_residual;     /* see bpqn_solve_opts.verify_secants (0 otherwise) */
 } bpqn_report;
 
 /* Defaults for the option structs above. */

@@ -21,7 +21,11 @@ Follows PAPER.md in the paper's order and notation, with the readings of SURVEY
   on the new iterate (A x_{k+1} directly, no cache drift);
 * Alg. 3 Bi-PQN with the subproblem eq. (pqnSubproblem) P:468-470,
   secant re-use P:475-487, cached low-fidelity secant A^ s = eta(A^ x^ - A^ x)
-  (App. D.2), sub-solver settings R22.
+  (App. D.2), sub-solver settings R22.  The re-used secants follow the
+  paper's stated requirement B^(k+1) S = Y rather than its printed
+  display (P:486 / Alg. 3, "Y^ - (uu^T - vv^T) S^"): with y' = B^(k) s' the
+  pair for B^(k+1) = B^(k) + uu^T - vv^T is Y = Y^ + (uu^T - vv^T) S^ (reading R34,
+  DESIGN.md; pinned by SPEC S:229's dense identity in tests/test_oracle_pqn.py).
 
 Pins: tests/test_oracle_pqn.py (SPEC.md unit vectors S:62-64, S:147, S:197-199,
 S:215-217; prox vs a dense QP on 500 random
@@ -301,9 +305,19 @@ def bb_pgd(mvp, b, x0, eps_abs=1e-10, eps_rel=0.0, k_max=500):
     return x, g, rep
 
 
+def transform_secants(S_hat, Y_hat, u, v):
+    """Secant re-use across Bi-PQN subproblems (reading R34): pairs with
+    B^(k) S^ = Y^ become pairs of B^(k+1) = B^(k) + u u^T - v v^T, i.e.
+    S = S^,  Y = Y^ + (u u^T - v v^T) S^."""
+    return [yp + u * np.dot(u, sp) - v * np.dot(v, sp) for sp, yp in zip(S_hat, Y_hat)]
+
+
 def bi_pqn(mvp_hi, mvp_lo, b, x_init, eps_abs=1e-10, eps_rel=0.0, k_max=100,
-           sub_eps_factor=1e-2, sub_k_max=50, refresh=20, curv=1e-12, prox_tol=None):
-    """Alg. 3.  mvp_hi(v) -> A v, mvp_lo(v) -> A^ v.  Returns (x, report)."""
+           sub_eps_factor=1e-2, sub_k_max=50, refresh=20, curv=1e-12, prox_tol=None,
+           verify_secants=False):
+    """Alg. 3.  mvp_hi(v) -> A v, mvp_lo(v) -> A^ v.  Returns (x, report).
+    verify_secants: before every subproblem, record max_j |B^(k) s_j - y_j|_inf /
+    max(1, |y_j|_inf) over the seeded pairs (extra lo MVPs, not counted; tests only)."""
     n = b.size
     cnt = dict(hi=0, lo=0)
 
@@ -332,6 +346,7 @@ def bi_pqn(mvp_hi, mvp_lo, b, x_init, eps_abs=1e-10, eps_rel=0.0, k_max=100,
 
     trace, prev, it, term = [], None, 0, TERM_MAX_ITER
     sub_iters = []
+    secant_res = []
     for k in range(k_max):
         e_abs, e_rel = kkt_errors(x, g, prev)
         prev = e_abs
@@ -343,6 +358,10 @@ def bi_pqn(mvp_hi, mvp_lo, b, x_init, eps_abs=1e-10, eps_rel=0.0, k_max=100,
             term = TERM_KKT_REL
             break
         c = g - Bhi(x, Ahat_x)
+        if verify_secants:
+            secant_res.append(max([0.0] + [float(np.abs(Bhi(sp, mvp_lo(sp)) - yp).max() /
+                                                 max(1.0, np.abs(yp).max()))
+                                           for sp, yp in zip(S_low, Y_low)]))
 
         def sub_op(v):
             cnt["lo"] += 1
@@ -377,7 +396,7 @@ def bi_pqn(mvp_hi, mvp_lo, b, x_init, eps_abs=1e-10, eps_rel=0.0, k_max=100,
             v = Bs / np.sqrt(sBs)
             U.append(u)
             V.append(v)
-            Y_low = [yp - u * np.dot(u, sp) + v * np.dot(v, sp) for sp, yp in zip(S_low, Y_low)]
+            Y_low = transform_secants(S_low, Y_low, u, v)
         Ahat_x = Ahat_x + Ahat_s
         if refresh and it % refresh == 0:
             cnt["hi"] += 1
@@ -387,5 +406,5 @@ def bi_pqn(mvp_hi, mvp_lo, b, x_init, eps_abs=1e-10, eps_rel=0.0, k_max=100,
         trace.append(e_abs)
     rep = Report(iterations=it, hi_mvps=cnt["hi"], lo_mvps=cnt["lo"], termination=term,
                  kkt_abs=trace[-1], kkt_trace=trace, init_iterations=rep0["iterations"],
-                 sub_iterations=sub_iters)
+                 sub_iterations=sub_iters, secant_residuals=secant_res)
     return x, rep

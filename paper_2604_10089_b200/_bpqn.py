@@ -34,14 +34,16 @@ class SolveOpts(ctypes.Structure):
     _fields_ = [("method", c_int), ("k_max", c_int), ("eps_kkt_abs", c_double), ("eps_kkt_rel", c_double),
                 ("tau", c_double), ("refresh_period", c_int), ("sub_eps_factor", c_double),
                 ("sub_k_max", c_int), ("prox_tol", c_double), ("prox_jmax", c_int), ("curv_skip", c_double),
-                ("gm_hi", GmresOpts), ("gm_lo", GmresOpts), ("cost_ratio", c_double), ("sub_forcing", c_double)]
+                ("gm_hi", GmresOpts), ("gm_lo", GmresOpts), ("cost_ratio", c_double), ("sub_forcing", c_double),
+                ("verify_secants", c_int)]
 
 
 class Report(ctypes.Structure):
     _fields_ = [("iterations", c_int), ("hi_mvps", c_int), ("lo_mvps", c_int), ("gmres_iters_hi", c_int),
                 ("gmres_iters_lo", c_int), ("e_mvps", c_double), ("cost_ratio", c_double),
                 ("kkt_abs", c_double), ("kkt_rel", c_double), ("objective", c_double),
-                ("ms_total", c_double), ("ms_hi", c_double), ("ms_lo", c_double), ("termination", c_int)]
+                ("ms_total", c_double), ("ms_hi", c_double), ("ms_lo", c_double), ("termination", c_int),
+                ("secant_residual", c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -227,6 +227,7 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o) {
   o->gm_hi.recycle = o->gm_lo.recycle = 1;
   o->cost_ratio = 0.0;
   o->sub_forcing = 0.0;
+  o->verify_secants = 0;
 }
 
 int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius, double mu,
@@ -516,6 +517,7 @@ static PqnOpts to_pqn(const bpqn_solve_opts& o) {
   q.prox_jmax = o.prox_jmax;
   q.curv = o.curv_skip;
   q.sub_forcing = o.sub_forcing;
+  q.verify_secants = o.verify_secants != 0;
   return q;
 }
 
@@ -571,7 +573,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     PqnOpts q = to_pqn(o);
     std::vector<double> x;
     int iters = 0, term = 2, hi_mvps = 0, lo_mvps = 0;
-    double kkt = 0, kkt_rel = 0;
+    double kkt = 0, kkt_rel = 0, secant_res = 0;
     if (bi) {
       MvpFn flo = make(lo, glo, ms_lo, it_lo, n_lo);
       BiResult r = bi_pqn(fhi, flo, b, x0, q);
@@ -583,6 +585,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       lo_mvps = r.lo_mvps;
       kkt = r.kkt;
       kkt_rel = r.kkt_rel;
+      secant_res = r.secant_residual;
     } else {
       MonoResult r = o.method == 2 ? bb_pgd(fhi, b, x0, q) : mono_pqn(fhi, b, x0, q, nullptr, nullptr, nullptr);
       prox_profile_flush();
@@ -613,6 +616,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       rep->ms_hi = ms_hi;
       rep->ms_lo = ms_lo;
       rep->termination = term;
+      rep->secant_residual = secant_res;
     }
     if (gm_fail) {
       set_error("an inner GMRES solve did not converge");
@@ -787,6 +791,7 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
         rep->lo_mvps = r.lo_mvps;
         rep->kkt_abs = r.kkt;
         rep->termination = term;
+        rep->secant_residual = r.secant_residual;
       }
     } else {
       MonoResult r = o.method == 2 ? bb_pgd(dense(A), b, x0, q) : mono_pqn(dense(A), b, x0, q, nullptr, nullptr, nullptr);

@@ -771,6 +771,19 @@ BiResult bi_pqn(const MvpFn& hi, const MvpFn& lo, const Vec& b, const Vec& x_ini
     }
     Vec Bx = Bhi(x, Ahat_x), c(n);
     for (size_t i = 0; i < n; ++i) c[i] = g[i] - Bx[i];
+    if (o.verify_secants) {  // max_j |B^(k) s_j - y_j|_inf / max(1, |y_j|_inf), uncounted lo MVPs
+      for (auto& sy : low) {
+        Vec As(n);
+        lo(sy.first, As, nullptr);
+        Vec Bs = Bhi(sy.first, As);
+        double e = 0, ym = 1.0;
+        for (size_t i = 0; i < n; ++i) {
+          e = std::max(e, std::fabs(Bs[i] - sy.second[i]));
+          ym = std::max(ym, std::fabs(sy.second[i]));
+        }
+        R.secant_residual = std::max(R.secant_residual, e / ym);
+      }
+    }
     int sub_lo = 0;
     MvpFn sub = [&](const Vec& v, Vec& out, Vec* aux) {
       Vec Av(n);
@@ -819,9 +832,12 @@ BiResult bi_pqn(const MvpFn& hi, const MvpFn& lo, const Vec& b, const Vec& x_ini
       }
       U.push_back(u);
       V.push_back(v);
+      // secant re-use: subproblem pairs satisfy B^(k) S = Y; for
+      // B^(k+1) = B^(k) + uu^T - vv^T they become Y + (uu^T - vv^T) S (reading R34:
+      // the sign the paper's requirement B^(k+1) S = Y fixes, not P:486's display)
       for (auto& sy : low) {
         double cu = dot(u, sy.first), cv = dot(v, sy.first);
-        for (size_t i = 0; i < n; ++i) sy.second[i] += -cu * u[i] + cv * v[i];
+        for (size_t i = 0; i < n; ++i) sy.second[i] += cu * u[i] - cv * v[i];
       }
     }
     for (size_t i = 0; i < n; ++i) Ahat_x[i] += Ahat_s[i];

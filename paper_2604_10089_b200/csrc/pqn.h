@@ -18,6 +18,7 @@ struct PqnOpts {
   int prox_jmax = 100;
   double curv = 1e-12;
   double sub_forcing = 0.0;
+  bool verify_secants = false;  // Bi-PQN: measure max |B^(k) s - y| of the re-used pairs (tests)
 };
 
 // C^-1 U and C^-1 V (C = I + U U^T) for the prox's Woodbury step, kept across prox calls
@@ -54,6 +55,7 @@ struct BiResult {
   int iterations = 0, hi_mvps = 0, lo_mvps = 0, termination = 2, init_iterations = 0;
   std::vector<int> sub_iterations;
   double kkt = 0, kkt_rel = 0;
+  double secant_residual = 0;  // with verify_secants: max over subproblems and seeded pairs
 };
 
 double kkt_abs(const std::vector<double>& x, const std::vector<double>& g);

@@ -1,6 +1,12 @@
 """Writes tests/fixtures/c{1..4}.npz -- every stored value comes from oracle/ only.
 
 Usage: python tests/fixtures/make_fixtures.py [c ...] [--no-lcp]
+       python tests/fixtures/make_fixtures.py --dense 2 3
+--dense adds to an existing c2/c3 fixture the oracle's densified LCP matrices
+(A = D^T M D column by column: one oracle MVP per unit vector, GMRES 1e-13; the
+low-fidelity A^ likewise) and re-runs the oracle's Mono-/Bi-PQN on them (O14's
+dense route; the matrix-free and dense operators agree to the GMRES tolerance).
+The -m gpu tests then evaluate R26's complementarity residual with the oracle's A.
 Runs the plain CPU oracle (oracle/) on the seeded synth/ inputs and stores the
 operator outputs and LCP solutions the -m gpu parity tests compare against
 (SURVEY 8(c).4).  Wall time and core count of each piece are recorded.
@@ -95,7 +101,51 @@ def run(c, do_lcp=True):
     log("wrote", path, "%.1fs" % out["total_s"])
 
 
+def run_dense(c):
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c%d.npz" % c)
+    out = dict(np.load(path, allow_pickle=True))
+    cfg = make_config(c)
+    pairs, nrm = out["pairs"], out["normals"]
+    b = out["b"]
+    nc = len(pairs)
+    times = {}
+    t = time.time()
+    d = Disc(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+    A = lcp.densify(lambda v: lcp.lcp_mvp(d, pairs, nrm, v, tol=GMRES_TOL), nc)
+    times["densify_hi"] = time.time() - t
+    log("c%d dense A (%d MVPs) %.1fs" % (c, nc, times["densify_hi"]))
+    out.update(A_dense=A)
+    if cfg["solve"] in ("mono", "both"):
+        t = time.time()
+        x, g, _, _, rep = pqn.mono_pqn(lambda v: (A @ v, None), b, np.zeros(nc), eps_abs=EPS_KKT)
+        times["mono_dense"] = time.time() - t
+        out.update(lam_mono=x, mono_iters=rep["iterations"], mono_mvps=rep["mvps"],
+                   mono_kkt=rep["kkt_abs"], mono_term=rep["termination"])
+        log("c%d mono-PQN (dense) iters %d mvps %d kkt %.2e" % (c, rep["iterations"], rep["mvps"],
+                                                                 rep["kkt_abs"]))
+    if cfg["solve"] in ("bi", "both"):
+        t = time.time()
+        dlo = Disc(cfg["centers"], cfg["p_lo"], cfg["radius"], cfg["mu"])
+        Alo = lcp.densify(lambda v: lcp.lcp_mvp(dlo, pairs, nrm, v, tol=GMRES_TOL), nc)
+        times["densify_lo"] = time.time() - t
+        x, rep = pqn.bi_pqn(lambda v: A @ v, lambda v: Alo @ v, b, np.zeros(nc), eps_abs=EPS_KKT)
+        out.update(A_lo_dense=Alo, lam_bi=x, bi_iters=rep["iterations"], bi_hi_mvps=rep["hi_mvps"],
+                   bi_lo_mvps=rep["lo_mvps"], bi_kkt=rep["kkt_abs"], bi_term=rep["termination"],
+                   p_lo=cfg["p_lo"])
+        log("c%d bi-PQN (dense, R34) iters %d hi %d lo %d kkt %.2e" % (c, rep["iterations"], rep["hi_mvps"],
+                                                                      rep["lo_mvps"], rep["kkt_abs"]))
+    out["dense_times_json"] = repr(times)
+    out["dense_cores"] = os.cpu_count()
+    np.savez_compressed(path, **out)
+    log("wrote", path)
+
+
 if __name__ == "__main__":
+    if "--dense" in sys.argv:
+        native.build()
+        for c in [int(a) for a in sys.argv[1:] if not a.startswith("--")]:
+            run_dense(c)
+        sys.exit(0)
     native.build()
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     cs = [int(a) for a in args] or [1, 2, 3, 4]

@@ -154,3 +154,24 @@ def test_dense_bb_pgd_vs_brute_force(lib, seed):
     assert rc == 0
     np.testing.assert_allclose(x, _brute(A, b), atol=1e-10)
     assert rep.hi_mvps == rep.iterations + 1
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_dense_bi_pqn_secant_reuse(lib, seed):
+    """C++ Bi-PQN behind the C ABI: every re-used subproblem secant pair fits the current model
+    B^(k) s = y (reading R34), and the LCP solution is unchanged."""
+    import paper_2604_10089_b200 as bp
+    rng = np.random.default_rng(300 + seed)
+    n = 24
+    M = rng.standard_normal((n, n))
+    A = M @ M.T / n + 0.2 * np.eye(n)
+    E = rng.standard_normal((n, n)) * 0.15 / np.sqrt(n)
+    Ahat = A + E + E.T
+    Ahat += max(0.0, 0.05 - np.linalg.eigvalsh(Ahat).min()) * np.eye(n)
+    b = rng.standard_normal(n)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-11, verify_secants=1)
+    x, rep, rc = bp.solve_lcp_dense(A, b, Ahat=Ahat, opts=o)
+    assert rc == 0
+    assert 0 < rep.secant_residual <= 1e-10, rep.secant_residual
+    xm, _, _ = bp.solve_lcp_dense(A, b, opts=bp.default_solve_opts(method=0, eps_kkt_abs=1e-12))
+    np.testing.assert_allclose(x, xm, atol=1e-9)

@@ -246,3 +246,58 @@ def test_bb_pgd_vs_brute_force(seed):
     ref, cnt = brute_force_lcp(A, b)
     assert cnt == 1 and rep["termination"] == 0
     np.testing.assert_allclose(x, ref, atol=1e-10)
+
+
+def _model(Ahat, U, V):
+    return Ahat + sum((np.outer(u, u) for u in U), np.zeros_like(Ahat)) - \
+        sum((np.outer(v, v) for v in V), np.zeros_like(Ahat))
+
+
+def test_secant_transform_dense_identity():
+    """SPEC S:224-229 / PAPER P:475-487 (reading R34): pairs with B^(k) S = Y become pairs of
+    B^(k+1) = B^(k) + uu^T - vv^T; checked with dense matrices (n = 6, m = 2 and larger)."""
+    assert pqn.transform_secants([], [], np.ones(3), np.ones(3)) == []            # empty cache
+    s0, y0 = np.arange(3.0), np.arange(3.0) + 1
+    y1 = pqn.transform_secants([s0], [y0], np.zeros(3), np.zeros(3))[0]           # u = v = 0
+    assert np.array_equal(y1, y0)
+    rng = np.random.default_rng(229)
+    for n, m in [(6, 2), (12, 5), (40, 9)]:
+        M = rng.standard_normal((n, n))
+        Ahat = M @ M.T + np.eye(n)
+        U = [rng.standard_normal(n) for _ in range(2)]
+        V = [0.3 * rng.standard_normal(n) for _ in range(2)]
+        Bk = _model(Ahat, U, V)
+        S = [rng.standard_normal(n) for _ in range(m)]
+        Y = [Bk @ s for s in S]
+        u, v = rng.standard_normal(n), 0.5 * rng.standard_normal(n)
+        Bk1 = Bk + np.outer(u, u) - np.outer(v, v)
+        Yn = pqn.transform_secants(S, Y, u, v)
+        for s, y in zip(S, Yn):
+            assert np.abs(Bk1 @ s - y).max() <= 1e-12 * max(1.0, np.abs(y).max())
+        # the display printed at P:486 / P:509 ("Y^ - (uu^T - vv^T) S^") breaks the identity
+        Yp = [y - u * (u @ s) + v * (v @ s) for s, y in zip(S, Y)]
+        assert max(np.abs(Bk1 @ s - y).max() for s, y in zip(S, Yp)) > 1e-3
+
+
+def _bifi_lcp(seed, n):
+    rng = np.random.default_rng(seed)
+    M = rng.standard_normal((n, n))
+    A = M @ M.T / n + 0.2 * np.eye(n)
+    E = rng.standard_normal((n, n)) * 0.15 / np.sqrt(n)
+    Ahat = A + E + E.T
+    Ahat += max(0.0, 0.05 - np.linalg.eigvalsh(Ahat).min()) * np.eye(n)
+    return A, Ahat, rng.standard_normal(n)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_bi_pqn_reused_secants_fit_current_model(seed):
+    """Inside Alg. 3 every seeded subproblem pair satisfies B^(k) s = y -- the
+    property the secant re-use exists for -- and the solution is the unique LCP solution."""
+    A, Ahat, b = _bifi_lcp(300 + seed, 24)
+    x, rep = pqn.bi_pqn(lambda v: A @ v, lambda v: Ahat @ v, b, np.zeros(b.size), eps_abs=1e-11,
+                        verify_secants=True)
+    assert rep["termination"] == pqn.TERM_KKT_ABS
+    assert len(rep["secant_residuals"]) >= 2
+    assert max(rep["secant_residuals"]) <= 1e-10, rep["secant_residuals"]
+    xm, _, _, _, _ = pqn.mono_pqn(mvp_of(A), b, np.zeros(b.size), eps_abs=1e-12)
+    np.testing.assert_allclose(x, xm, atol=1e-9)
