@@ -7,6 +7,13 @@ Usage: python tests/fixtures/make_fixtures.py [c ...] [--no-lcp]
 low-fidelity A^ likewise) and re-runs the oracle's Mono-/Bi-PQN on them (O14's
 dense route; the matrix-free and dense operators agree to the GMRES tolerance).
 The -m gpu tests then evaluate R26's complementarity residual with the oracle's A.
+       python tests/fixtures/make_fixtures.py --certify 4 LAMBDA.npy
+--certify stores a KKT certificate for a candidate solution lambda of the c4 LCP
+(where the oracle cannot afford its own solve: Nc = 540 columns at ~1 h per oracle
+MVP): the oracle's A lambda (one oracle MVP, GMRES 1e-13) and
+||min(lambda, A lambda + b)||_2 with the oracle's A and b (R26).  lambda is only an
+input to the oracle here; the stored expected values are the oracle's (R35).
+The oracle's operator data are built first; the script then waits for LAMBDA.npy.
 Runs the plain CPU oracle (oracle/) on the seeded synth/ inputs and stores the
 operator outputs and LCP solutions the -m gpu parity tests compare against
 (SURVEY 8(c).4).  Wall time and core count of each piece are recorded.
@@ -140,7 +147,38 @@ def run_dense(c):
     log("wrote", path)
 
 
+def run_certify(c, lam_path):
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "c%d.npz" % c)
+    cfg = make_config(c)
+    t = time.time()
+    d = Disc(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
+    d.near_T_all()
+    d.self_full()
+    t_pre = time.time() - t
+    log("c%d oracle operator data built %.1fs; waiting for %s" % (c, t_pre, lam_path))
+    while not os.path.exists(lam_path):
+        time.sleep(30)
+    time.sleep(5)
+    lam = np.load(lam_path)
+    out = dict(np.load(path, allow_pickle=True))
+    assert lam.shape == (len(out["pairs"]),) and (lam >= 0).all()
+    t = time.time()
+    w, info = lcp.lcp_mvp(d, out["pairs"], out["normals"], lam, tol=GMRES_TOL, return_info=True)
+    t_mvp = time.time() - t
+    kkt = float(np.linalg.norm(np.minimum(lam, w + out["b"])))
+    log("c%d certificate: oracle MVP %.1fs (%d its), ||min(lam, A lam + b)|| = %.3e" % (c, t_mvp, info["iters"], kkt))
+    out.update(lam_cert=lam, A_lam_cert=w, cert_kkt=kkt, cert_times_json=repr(dict(precompute=t_pre, mvp=t_mvp)),
+               cert_cores=os.cpu_count())
+    np.savez_compressed(path, **out)
+    log("wrote", path)
+
+
 if __name__ == "__main__":
+    if "--certify" in sys.argv:
+        native.build()
+        a = [x for x in sys.argv[1:] if not x.startswith("--")]
+        run_certify(int(a[0]), a[1])
+        sys.exit(0)
     if "--dense" in sys.argv:
         native.build()
         for c in [int(a) for a in sys.argv[1:] if not a.startswith("--")]:
