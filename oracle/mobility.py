@@ -59,8 +59,9 @@ def A_op(disc, q):
     return -0.5 * q + disc.apply_all(q=q) + Pi_R(disc, q)
 
 
-def gmres(apply, rhs, tol=1e-13, maxiter=400):
-    """Textbook full GMRES (MGS Arnoldi, Givens), x0 = 0.  Returns (x, iters, relres)."""
+def gmres(apply, rhs, tol=1e-13, maxiter=400, hist=None):
+    """Textbook full GMRES (MGS Arnoldi, Givens), x0 = 0.  Returns (x, iters, relres).
+    hist: optional list that receives the relative residual after every iteration."""
     b = rhs.reshape(-1)
     beta = np.linalg.norm(b)
     if beta == 0.0:
@@ -89,6 +90,8 @@ def gmres(apply, rhs, tol=1e-13, maxiter=400):
         g[k + 1] = -sn[k] * g[k]
         g[k] = cs[k] * g[k]
         relres = abs(g[k + 1]) / beta
+        if hist is not None:
+            hist.append(relres)
         if relres <= tol:
             break
         V.append(w / np.linalg.norm(w)) if np.linalg.norm(w) > 0 else V.append(w)
@@ -103,10 +106,11 @@ def mobility(disc, FT, slip=None, tol=1e-13, maxiter=400, return_info=False):
     f = PT(disc, FT)
     g = disc.apply_all(f=f)
     rhs = -g if slip is None else np.asarray(slip).reshape(-1, 3) - g
-    q, it, rr = gmres(lambda v: A_op(disc, v), rhs, tol=tol, maxiter=maxiter)
+    hist = []
+    q, it, rr = gmres(lambda v: A_op(disc, v), rhs, tol=tol, maxiter=maxiter, hist=hist)
     UO = -rigid_coeffs(disc, q)
     if return_info:
-        return UO, dict(iters=it, relres=rr, q=q.reshape(-1, 3))
+        return UO, dict(iters=it, relres=rr, q=q.reshape(-1, 3), hist=hist)
     return UO
 
 

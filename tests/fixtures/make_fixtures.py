@@ -166,6 +166,9 @@ def run_certify(c, lam_path):
     w, info = lcp.lcp_mvp(d, out["pairs"], out["normals"], lam, tol=GMRES_TOL, return_info=True)
     t_mvp = time.time() - t
     kkt = float(np.linalg.norm(np.minimum(lam, w + out["b"])))
+    h = np.array(info["hist"])
+    out["oracle_kg_1e-8"] = int(np.argmax(h <= 1e-8)) + 1 if (h <= 1e-8).any() else -1
+    out["oracle_gmres_hist"] = h
     log("c%d certificate: oracle MVP %.1fs (%d its), ||min(lam, A lam + b)|| = %.3e" % (c, t_mvp, info["iters"], kkt))
     out.update(lam_cert=lam, A_lam_cert=w, cert_kkt=kkt, cert_times_json=repr(dict(precompute=t_pre, mvp=t_mvp)),
                cert_cores=os.cpu_count())
