@@ -69,8 +69,12 @@ typedef struct {
   int recycle;        /* 1: start from the least-squares combination of this handle's earlier
                          solutions and keep this solve's (rhs, solution) pair (Krylov
                          recycling across the MVPs of one LCP solve).
-                         The store holds up to 256 orthonormalised pairs; it is emptied by
-                         bpqn_gmres_recycle_reset and at the start of bpqn_solve_lcp.  0: off. */
+                         The store holds up to 1024 orthonormalised pairs within min(4 GB, a
+                         quarter of the free device memory) per handle; it is allocated (and
+                         emptied) by bpqn_gmres_recycle_reset and at the start of bpqn_solve_lcp
+                         -- never inside an MVP: without a reserved store recycle = 1 is a no-op.
+                         A solve's pair is kept only if its new direction has norm
+                         > max(1e-8, sqrt(tol)) |rhs|.  0: off. */
 } bpqn_gmres_opts;
 
 typedef struct {
@@ -242,7 +246,8 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
 int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs_recv_dev,
                                   int (*reduce_scatter)(void* user), void* user);
 
-/* Empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
+/* Reserve (first call: allocate; BPQN_OK with recycling left off if the memory is not there)
+ * and empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
 int bpqn_gmres_recycle_reset(bpqn_geom_t g);
 
 /* Thread-local message for the last non-zero return. */

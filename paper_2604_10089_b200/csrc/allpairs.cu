@@ -309,7 +309,10 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
 struct K1SymParams {
   const double* pk;       // packed records [npad][RecS] (targets and sources)
   const double* centers;  // [Np][3]
-  double* out;            // [N][3], zeroed, atomically accumulated
+  // deterministic partial sums (no atomics; k_row_reduce adds them in a fixed order):
+  double* pseg;           // [grid + nb][KS_B][3]: target-side sums of CTA c over block b at segment c + b
+  double* psrc;           // [nb][psrc_ld]: source-side sums of unit (b, t) at psrc[b][3 (64 t + j) + comp]
+  size_t psrc_ld;
   int N, nb, nt, nq, np;  // blocks of KS_B points, tiles of K1_TS points, nodes per sphere, spheres
   double a;
   long long units;        // units this launch processes: [ubeg, ubeg + units) of the block-major list
@@ -522,15 +525,14 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     const int buf = i % NS;
     const unsigned parity = (unsigned)(i / NS) & 1u;
     if (b_cur != loaded_b) {
-      if (loaded_b >= 0) {
+      if (loaded_b >= 0) {  // this CTA's target-side sums over block loaded_b: segment blockIdx.x + loaded_b
+        double* sg = P.pseg + (size_t)(blockIdx.x + loaded_b) * KS_B * 3;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-          const int t = loaded_b * KS_B + warp * 32 * R + r * 32 + lane;
-          if (t < P.N) {
-            atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
-            atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
-            atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
-          }
+          const int tl = warp * 32 * R + r * 32 + lane;
+          sg[3 * tl] = acc[r][0];
+          sg[3 * tl + 1] = acc[r][1];
+          sg[3 * tl + 2] = acc[r][2];
         }
       }
       loaded_b = b_cur;
@@ -606,7 +608,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
         double sum = 0.0;
 #pragma unroll
         for (int w = 0; w < KS_W; ++w) sum += red[par][w][tid];
-        if (t_cur * K1_TS + tid / 3 < P.N) atomicAdd(P.out + 3 * (size_t)t_cur * K1_TS + tid, sum);
+        P.psrc[(size_t)b_cur * P.psrc_ld + 3 * (size_t)t_cur * K1_TS + tid] = sum;
       }
       par ^= 1;
     }
@@ -617,15 +619,94 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     }
     if (++t_cur == P.nt) t_cur = ++b_cur * TPB;
   }
+  {
+    double* sg = P.pseg + (size_t)(blockIdx.x + loaded_b) * KS_B * 3;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int t = loaded_b * KS_B + warp * 32 * R + r * 32 + lane;
-    if (t < P.N) {
-      atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
-      atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
-      atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
+    for (int r = 0; r < R; ++r) {
+      const int tl = warp * 32 * R + r * 32 + lane;
+      sg[3 * tl] = acc[r][0];
+      sg[3 * tl + 1] = acc[r][1];
+      sg[3 * tl + 2] = acc[r][2];
     }
   }
+}
+
+// ---------------------------------------------------------------- row reduction
+// out[3 i + c] = (K1: the CTA segments over i's block in CTA order, then the source-side
+// partials of blocks b' < b in block order -- or far[3 i + c]) + (K2: the near partials of
+// row i in (target, source sphere) order).  A fixed summation order: the operator is
+// bit-reproducible run to run (no floating-point atomics anywhere on the path).
+struct RowRedParams {
+  int N, r0, r1;
+  const double *pseg, *psrc;  // symmetric K1 partials (pseg == nullptr: use far)
+  size_t psrc_ld;
+  int ks_b, tpb, nt, grid;
+  long long ubeg, units;
+  const double* far;
+  const double* pinc;         // K2 partials [n_inc][3] (K2 order) or nullptr
+  const int *row_ptr, *row_pos;
+  double* out;
+};
+
+__device__ __forceinline__ int k1_cta_of(long long u, long long ubeg, long long units, int G) {
+  int lo = 0, hi = G - 1;  // largest c with ubeg + units c / G <= u
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (ubeg + units * mid / G <= u) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
+
+__global__ void k_row_reduce(RowRedParams P) {
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x + 3LL * P.r0;
+  if (e >= 3LL * P.r1) return;
+  const int i = (int)(e / 3), c = (int)(e - 3LL * i);
+  double v = 0.0;
+  if (P.pseg) {
+    const int b = i / P.ks_b, local = i - b * P.ks_b;
+    const long long Ub = (long long)b * P.nt - (long long)P.tpb * b * (b - 1) / 2;  // units before block b
+    const long long lo = max(Ub, P.ubeg), hi = min(Ub + (P.nt - (long long)b * P.tpb), P.ubeg + P.units);
+    if (lo < hi) {
+      const int c0 = k1_cta_of(lo, P.ubeg, P.units, P.grid), c1 = k1_cta_of(hi - 1, P.ubeg, P.units, P.grid);
+      for (int cc = c0; cc <= c1; ++cc) v += P.pseg[((size_t)(cc + b) * P.ks_b + local) * 3 + c];
+    }
+    for (int bb = 0; bb < b; ++bb) v += P.psrc[(size_t)bb * P.psrc_ld + e];
+  } else if (P.far) {
+    v = P.far[e];
+  }
+  if (P.pinc)
+    for (int k = P.row_ptr[i]; k < P.row_ptr[i + 1]; ++k) v += P.pinc[3 * (size_t)P.row_pos[k] + c];
+  P.out[e] = v;
+}
+
+void launch_row_reduce(Geom& g, bool k1_partials, const double* far, bool with_k2, double* out, int r0, int r1,
+                       cudaStream_t st) {
+  RowRedParams P{};
+  P.N = g.n;
+  P.r0 = r0;
+  P.r1 = r1;
+  if (k1_partials) {
+    P.pseg = g.k1_pseg.p;
+    P.psrc = g.k1_psrc.p;
+    P.psrc_ld = g.k1lay.psrc_ld;
+    P.ks_b = g.k1lay.ks_b;
+    P.tpb = g.k1lay.tpb;
+    P.nt = g.k1lay.nt;
+    P.grid = g.k1lay.grid;
+    P.ubeg = g.k1lay.ubeg;
+    P.units = g.k1lay.units;
+  }
+  P.far = far;
+  P.pinc = with_k2 && g.n_inc > 0 ? g.k2_pinc.p : nullptr;
+  P.row_ptr = g.row_ptr.p;
+  P.row_pos = g.row_pos.p;
+  P.out = out;
+  const long long n = 3LL * (r1 - r0);
+  if (n <= 0) return;
+  k_row_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(P);
+  BPQN_CHECK_LAUNCH();
+  g.prof.launches++;
 }
 
 // Algorithmic flops per target-source pair of the fused formulation (DESIGN.md
@@ -655,7 +736,8 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   K1SymParams P;
   P.pk = g.packed.p;
   P.centers = g.centers_d.p;
-  P.out = out;
+  P.pseg = g.k1_pseg.p;
+  P.psrc = g.k1_psrc.p;
   P.N = g.n;
   P.nq = g.nq;
   P.np = g.np;
@@ -692,9 +774,37 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
       occ.emplace_back(smem, grid);
     }
   }
-  if (P.units == 0) return;  // a rank with no share (more ranks than units); out stays zero
-  const int gr = (int)std::min<long long>(grid, P.units);
+  const int gr = (int)std::max<long long>(1, std::min<long long>(grid, P.units));
+  const int npad = P.nb * KS_B;
+  P.psrc_ld = 3 * (size_t)npad;
+  K1Layout& Ly = g.k1lay;
+  Ly.sym = true;
+  Ly.ks_b = KS_B;
+  Ly.tpb = KS_B / K1_TS;
+  Ly.nt = P.nt;
+  Ly.nb = P.nb;
+  Ly.grid = gr;
+  Ly.ubeg = P.ubeg;
+  Ly.units = P.units;
+  Ly.psrc_ld = P.psrc_ld;
+  BPQN_REQUIRE((size_t)(gr + P.nb) * KS_B * 3 <= g.k1_pseg.n && (size_t)P.nb * P.psrc_ld <= g.k1_psrc.n,
+               "K1 partial-sum workspace too small");
+  if (g.shard_world > 1) {  // this rank's share of the units: the other partials read as zero
+    BPQN_CUDA(cudaMemsetAsync(g.k1_pseg.p, 0, sizeof(double) * (size_t)(gr + P.nb) * KS_B * 3, st));
+    BPQN_CUDA(cudaMemsetAsync(g.k1_psrc.p, 0, sizeof(double) * (size_t)P.nb * P.psrc_ld, st));
+  }
+  if (P.units == 0) return;  // a rank with no share (more ranks than units): every partial stays zero
   k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
+}
+
+static int sym_block_points(int c);
+// Workspace of the symmetric kernel's partial sums for one launch shape.
+static void sym_ws(const Geom& g, int cfg, size_t& pseg, size_t& psrc, size_t& packed) {
+  const int kb = sym_block_points(cfg);
+  const size_t nb = (size_t)((g.n + kb - 1) / kb), npad = nb * kb;
+  pseg = std::max(pseg, (size_t)(4 * g.sms + nb) * kb * 3);  // grid <= 4 CTAs per SM
+  psrc = std::max(psrc, nb * 3 * npad);
+  packed = std::max(packed, npad * 14);
 }
 
 // Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps at 1 CTA/SM with
@@ -785,6 +895,17 @@ bool k1_sharded_symmetric(const Geom& g) {
   return g.shard_world > 1 && g.sh_rs_fn != nullptr && k1_symmetric() && k1_sym_eligible(g);
 }
 
+// All K1 workspace, allocated once per handle (geometry init / update): the packed records and
+// the deterministic partial-sum buffers for every mode's launch shape -- the hot calls allocate nothing.
+void k1_reserve(Geom& g) {
+  size_t pseg = 1, psrc = 1, packed = ((g.n + K1_TS - 1) / K1_TS) * (size_t)K1_TS * 14;
+  if (k1_sym_eligible(g))
+    for (int mode = 0; mode < 3; ++mode) sym_ws(g, sym_cfg(g, mode), pseg, psrc, packed);
+  g.k1_pseg.ensure(pseg);
+  g.k1_psrc.ensure(psrc);
+  g.packed.ensure(packed);
+}
+
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
   const bool sym = k1_symmetric();
   // symmetric kernel: a 32-point group spans <= 2 spheres, centres fit smem, all targets on this
@@ -794,7 +915,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   // source tile (one-directional: 64-point tiles); the padding is far away, zero strength
   const int blk = use_sym ? sym_block_points(sym_cfg(g, mode)) : K1_TS;
   const int npad = ((g.n + blk - 1) / blk) * blk;
-  g.packed.ensure((size_t)npad * 14);
+  BPQN_REQUIRE((size_t)npad * 14 <= g.packed.n, "K1 packed workspace too small (k1_reserve)");
   if (use_sym)
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
                                                    1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);
@@ -802,7 +923,8 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
     k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
                                                -3.0 / (4.0 * PI_A), g.packed.p);
   BPQN_CHECK_LAUNCH();
-  BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
+  g.k1lay.sym = use_sym;
+  if (!use_sym) BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
   if (use_sym) {
     if (mode == MODE_D) launch_sym<MODE_D>(g, out, st);
     else if (mode == MODE_S) launch_sym<MODE_S>(g, out, st);

@@ -80,41 +80,37 @@ struct Profile {
   long long allpairs_launches = 0, launches = 0;
 };
 
-// CUDA graphs of the GMRES Arnoldi steps (gmres.cu), one per step index k, valid for one
-// set of buffer addresses / restart length / preconditioner flag.
-struct GraphCache {
-  std::vector<cudaGraphExec_t> exec;
-  std::vector<char> warm;
-  std::vector<long long> launches;
+// One GMRES restart cycle as a CUDA graph (gmres.cu): a conditional WHILE node whose body is
+// one Arnoldi step; valid for one set of buffer addresses / restart length / preconditioner flag.
+struct CycleGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  cudaGraphConditionalHandle h = 0;
   cudaStream_t cap = nullptr;
-  bool ok = true;
-  const void* sig[5] = {};
+  bool ok = true, warm = false, pre = false;
   int m = -1;
-  bool pre = false;
+  const void *V = nullptr, *S = nullptr, *red = nullptr;
+  long long launches = 0, k1 = 0;  // kernel launches / K1 launches per step
   void clear() {
-    for (auto& e : exec)
-      if (e) cudaGraphExecDestroy(e);
-    exec.clear();
-    warm.clear();
-    launches.clear();
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    exec = nullptr;
+    graph = nullptr;
+    m = -1;
+    warm = false;  // the next cycle runs uncaptured first (attribute setup for new sizes)
   }
-  void validate(const void* a, const void* b, const void* c, const void* d, const void* e, int mm, bool pp) {
-    const void* s2[5] = {a, b, c, d, e};
-    bool same = mm == m && pp == pre;
-    for (int i = 0; i < 5; ++i) same = same && s2[i] == sig[i];
-    if (same) return;
-    clear();
-    for (int i = 0; i < 5; ++i) sig[i] = s2[i];
-    m = mm;
-    pre = pp;
-    exec.assign(m, nullptr);
-    warm.assign(m, 0);
-    launches.assign(m, 0);
-  }
-  ~GraphCache() {
+  ~CycleGraph() {
     clear();
     if (cap) cudaStreamDestroy(cap);
   }
+};
+
+// Launch layout of the last symmetric K1 launch: how k_row_reduce finds its partial sums.
+struct K1Layout {
+  bool sym = false;
+  int ks_b = 0, tpb = 0, nt = 0, nb = 0, grid = 0;
+  long long ubeg = 0, units = 0;
+  size_t psrc_ld = 0;
 };
 
 struct Geom {
@@ -152,7 +148,7 @@ struct Geom {
   DBuf<int> chunks;              // [n_chunks][2] position ranges
   int n_chunks = 0;
   DBuf<double> T_S, T_D;         // [n_inc][6][nb'], nb' = nb rounded up to even (zero pad)
-  DBuf<double> coef;             // [2][np][nb'][3] SH coefficients of the densities (K2 workspace)
+  DBuf<double> coef;             // [2][KC_Z][np][nb'][3] SH coefficients of the densities, per node slab (K2)
 
   // contacts
   int nc = 0, nc_cap = 0;
@@ -160,8 +156,14 @@ struct Geom {
   DBuf<double> normals;   // [cap][3]
   DBuf<double> gaps;      // [cap]
 
-  // workspaces
-  DBuf<double> packed;   // K1 packed source records [npad][<=12]
+  // workspaces (all allocated at init / update: the hot calls allocate nothing)
+  DBuf<double> packed;   // K1 packed source records [npad][<=14]
+  DBuf<double> k1_pseg, k1_psrc;  // symmetric K1 partial sums (allpairs.cu, deterministic reduction)
+  K1Layout k1lay;
+  DBuf<double> k2_pinc;  // [n_inc][3] K2 per-incidence sums (K2 order)
+  DBuf<int> row_ptr, row_pos;  // [N+1], [n_inc]: K2 positions of each target row, (target, sphere) order
+  DBuf<double> k3_part;  // K3 split-K partial tiles
+  DBuf<unsigned> k3_cnt; // K3 per-tile arrival counters (self-resetting)
   DBuf<double> far;      // [N][3] all-pairs accumulator
   DBuf<double> nearout;  // [N][3]
   DBuf<double> rhs, sol, tmp, tmp2, tmp3;  // [N][3]
@@ -169,18 +171,16 @@ struct Geom {
   DBuf<double> red;      // reduction scratch
   DBuf<double> scal;     // device scalars
   DBuf<double> ft, uo;   // [np][6]
+  DBuf<int> gm_ctl;      // GMRES device control words (gmres.cu)
+  bool gm_ctl_init = false;
+  DBuf<double> gm_z, gm_vin;  // Arnoldi step operator output / input
   // GMRES recycling store (gmres.cu): W orthonormal past rhs, Z = A_op^-1 W
   DBuf<double> rec_W, rec_Z;
   int rec_k = 0, rec_cap = 0;
-  // GCRO deflation space (gmres.cu, R33b): A~ U = C, C orthonormal, def_k vectors
-  DBuf<double> def_U, def_C;
-  int def_k = 0;
-  bool def_pre = false;
   double* host_scal = nullptr;  // pinned
-  int gm_restart = 0;
 
   Profile prof;
-  GraphCache gm_graphs;
+  CycleGraph gm_cycle;
   cudaStream_t side = nullptr;            // K2 overlapped with K1 (layer.cu)
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool overlap_k2 = false;
@@ -218,14 +218,22 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
 double allpairs_flops_per_pair(int mode);
 void profile_collect(Geom& g);
 void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, double* out, cudaStream_t st);
+void k1_reserve(Geom& g);
+// out rows [r0, r1) = (K1 partials of the last symmetric launch, or far) + (K2 partials if with_k2)
+void launch_row_reduce(Geom& g, bool k1_partials, const double* far, bool with_k2, double* out, int r0, int r1,
+                       cudaStream_t st);
+void layer_reserve(Geom& g);  // K2 / K3 workspace (layer.cu)
 bool k1_sharded_symmetric(const Geom& g);
-void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st);
-void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
-                      double* out, int accumulate, cudaStream_t st, int s0 = 0, int s1 = -1);
+void launch_near(Geom& g, const double* sigS, const double* sigD, cudaStream_t st);  // -> g.k2_pinc
+// out (+)= E X per sphere (columns [s0, s1)), deterministic split-K
+void launch_self_gemm(Geom& g, const double* E, const double* X, double* out, int accumulate, cudaStream_t st,
+                      int s0 = 0, int s1 = -1);
 
 // GMRES on A_op q = rhs (A_op = E_A + coarse + near); returns stats.
 int gmres_solve(Geom& g, const double* rhs, double* x, const bpqn_gmres_opts& o, bpqn_gmres_stats& st,
                 cudaStream_t s);
+void gmres_reserve(Geom& g, int restart);   // basis and scratch for a restart length (init: default 100)
+void gmres_recycle_reserve(Geom& g);        // recycling store (outside the hot calls; may stay off)
 
 // small kernels (contacts.cu)
 void launch_pt(Geom& g, const double* ft, double* f, cudaStream_t st);

@@ -77,8 +77,7 @@ static void shard_ranges(Geom& g) {
 // |x_i - c_m| - a < d_near (R8), sorted by (i, m).
 static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
   Geom* g = &G;
-  g->gm_graphs.clear();  // captured GMRES steps hold the old near data and grid sizes
-  g->gm_graphs.m = -1;
+  g->gm_cycle.clear();  // the captured GMRES cycle holds the old near data and grid sizes
   const double radius = g->a;
   const int n_spheres = g->np;
   g->centers.assign(centers_host, centers_host + 3 * (size_t)n_spheres);
@@ -156,6 +155,18 @@ static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
   upload_i(g->cm_t, ct, st);
   upload_i(g->cm_m, cm, st);
   upload_i(g->chunks, ch, st);
+  // per target row: its K2 positions in source-sphere order (k_row_reduce's fixed summation order)
+  std::vector<int> rp((size_t)N + 1, 0), rpos(ct.size());
+  for (int t : ct) rp[t + 1]++;
+  for (int i = 0; i < N; ++i) rp[i + 1] += rp[i];
+  {
+    std::vector<int> fill(rp.begin(), rp.end() - 1);
+    for (size_t k = 0; k < ct.size(); ++k) rpos[fill[ct[k]]++] = (int)k;
+  }
+  upload_i(g->row_ptr, rp, st);
+  upload_i(g->row_pos, rpos, st);
+  k1_reserve(*g);
+  layer_reserve(*g);
   BPQN_CUDA(cudaStreamSynchronize(st));  // host staging vectors go out of scope
 }
 
@@ -281,6 +292,7 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       g->tmp2.alloc(n3);
       g->ft.alloc(6 * (size_t)g->np);
       g->uo.alloc(6 * (size_t)g->np);
+      gmres_reserve(*g, 100);
       BPQN_CUDA(cudaMallocHost(&g->host_scal, 64 * sizeof(double)));
       precompute(*g, st, true);
     } catch (...) {
@@ -307,7 +319,6 @@ int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream
     precompute(*g, st, false);  // near rows only; grid, SH analysis, self operators and inverse kept
     g->nc = 0;
     g->rec_k = 0;
-    g->def_k = 0;
     return BPQN_OK;
   });
 }
@@ -329,8 +340,7 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
     }
     BPQN_REQUIRE(world <= g->np, "more ranks than spheres");
     BPQN_REQUIRE(send_dev && recv_dev && allgather, "null buffer or callback");
-    g->gm_graphs.clear();
-    g->gm_graphs.m = -1;
+    g->gm_cycle.clear();
     g->shard_rank = rank;
     g->shard_world = world;
     g->sh_send = send_dev;
@@ -346,8 +356,7 @@ int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs
                                   int (*reduce_scatter)(void* user), void* user) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");
-    g->gm_graphs.clear();
-    g->gm_graphs.m = -1;
+    g->gm_cycle.clear();
     if (!reduce_scatter) {  // back to the one-directional K1 over the owned target rows
       g->sh_rs_fn = nullptr;
       g->sh_rs_send = g->sh_rs_recv = nullptr;
@@ -538,8 +547,14 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     BPQN_CUDA(cudaMemcpyAsync(x0.data(), lambda_dev, 8 * nc, cudaMemcpyDeviceToHost, s));
     BPQN_CUDA(cudaStreamSynchronize(s));
     for (double v : x0) BPQN_REQUIRE(v >= 0, "x_init must be >= 0");
-    if (o.gm_hi.recycle) hi->rec_k = hi->def_k = 0;
-    if (bi && o.gm_lo.recycle) lo->rec_k = lo->def_k = 0;
+    if (o.gm_hi.recycle) {  // reserved here, outside the MVPs (no allocation in the hot calls)
+      gmres_recycle_reserve(*hi);
+      hi->rec_k = 0;
+    }
+    if (bi && o.gm_lo.recycle) {
+      gmres_recycle_reserve(*lo);
+      lo->rec_k = 0;
+    }
     DBuf<double> dv, dw;
     dv.alloc(nc);
     dw.alloc(nc);
@@ -743,13 +758,11 @@ int bpqn_dvi_step(bpqn_geom_t hi, bpqn_geom_t lo, double* centers_host, double* 
     precompute(g, s, false);
     g.nc = 0;
     g.rec_k = 0;
-    g.def_k = 0;
     if (lo) {
       set_centers(*lo, cn.data(), s);
       precompute(*lo, s, false);
       lo->nc = 0;
       lo->rec_k = 0;
-      lo->def_k = 0;
     }
     std::copy(cn.begin(), cn.end(), centers_host);
     std::copy(an.begin(), an.end(), axes_host);
@@ -814,8 +827,8 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
 int bpqn_gmres_recycle_reset(bpqn_geom_t g) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");
+    gmres_recycle_reserve(*g);
     g->rec_k = 0;
-    g->def_k = 0;
     return BPQN_OK;
   });
 }

@@ -27,9 +27,10 @@ namespace bpqn {
 // coef[m][b][c] = sum_j A[b][j] sigma[m][j][c] (A row-major [nb][nq]); rows b in [nb, nbp) are zero.
 // A small tiled GEMM: block = 32 rows of A x 8 spheres; its 256 threads form 4 groups that take
 // interleaved slabs of 16 nodes (each thread 4 rows x 1 sphere x 3 components), then add their
-// partial sums through shared memory; gridDim.z blocks split the nodes and add atomically.  A is
-// read once per 8 spheres (L2 traffic nb nq Np bytes).
-constexpr int KC_BM = 32, KC_BS = 8, KC_JT = 16, KC_G = 4;
+// partial sums through shared memory; the KC_Z blocks along gridDim.z split the nodes and write
+// one coefficient slab each (k2_near adds the slabs in a fixed order -- no atomics).  A is read
+// once per 8 spheres (L2 traffic nb nq Np bytes).
+constexpr int KC_BM = 32, KC_BS = 8, KC_JT = 16, KC_G = 4, KC_Z = 4;
 __global__ void __launch_bounds__(256) k2_coef(int nq, int nb, int nbp, int np, const double* __restrict__ A,
                                                const double* __restrict__ sig, double* __restrict__ coef) {
   constexpr int NA = KC_G * KC_BM * (KC_JT + 1), NS = KC_G * KC_BS * KC_JT * 3;
@@ -83,14 +84,13 @@ __global__ void __launch_bounds__(256) k2_coef(int nq, int nb, int nbp, int np, 
   for (int u = 0; u < 4; ++u) {
     const int bb = b0 + 4 * tr + u;
     if (bb >= nbp) continue;
-    double* o = coef + ((size_t)(s0 + ts) * nbp + bb) * 3;
+    double* o = coef + (size_t)blockIdx.z * np * nbp * 3 + ((size_t)(s0 + ts) * nbp + bb) * 3;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
       double v = 0.0;
 #pragma unroll
       for (int g = 0; g < KC_G; ++g) v += red[(g * 64 + t) * 12 + 3 * u + k];
-      if (gridDim.z == 1) o[k] = v;
-      else atomicAdd(o + k, v);  // node ranges split over gridDim.z blocks (coef zeroed)
+      o[k] = v;  // this node slab's coefficient
     }
   }
 }
@@ -101,11 +101,11 @@ struct K2Params {
   const double* centers;         // [np][3]
   double a;
   const double *TS, *TD;         // [n_inc][6][nbp] or null (nbp = nb rounded up to even)
-  const double *coefS, *coefD;   // [np][nbp][3]
+  const double *coefS, *coefD;   // [KC_Z][np][nbp][3] node-slab partial coefficients
   const double *sigS, *sigD;     // [N][3]
-  int nq, nbp, t0, t1;           // targets outside [t0, t1) are skipped (sharding)
+  int np, nq, nbp, t0, t1;       // targets outside [t0, t1) are skipped (sharding)
   double cS, cD;                 // 1/(8 pi mu), -3/(4 pi)
-  double* out;                   // [N][3], zeroed
+  double* pinc;                  // [n_inc][3] per-incidence sums (K2 order), summed per row by k_row_reduce
 };
 
 // u[a] += sum_c T[sym(a,c)] c[c] over the packed symmetric rows, streamed in b pairs
@@ -146,9 +146,16 @@ __global__ void __launch_bounds__(256, 4) k2_near(K2Params P) {
     if (doD) sqD[e] = P.cD * w * P.sigD[3 * j0 + e];
     if (doS) sqS[e] = P.cS * w * P.sigS[3 * j0 + e];
   }
+  const size_t slab = (size_t)P.np * nb * 3;
   for (int e = threadIdx.x; e < 3 * nb; e += blockDim.x) {
-    if (doD) scD[e] = P.coefD[(size_t)m * nb * 3 + e];
-    if (doS) scS[e] = P.coefS[(size_t)m * nb * 3 + e];
+    double cd = 0.0, cs = 0.0;
+#pragma unroll
+    for (int z = 0; z < KC_Z; ++z) {  // node slabs in a fixed order
+      if (doD) cd += P.coefD[z * slab + (size_t)m * nb * 3 + e];
+      if (doS) cs += P.coefS[z * slab + (size_t)m * nb * 3 + e];
+    }
+    if (doD) scD[e] = cd;
+    if (doS) scS[e] = cs;
   }
   const double cm0 = P.centers[3 * m], cm1 = P.centers[3 * m + 1], cm2 = P.centers[3 * m + 2];
   const double inv2a = 0.5 / P.a, a2 = P.a * P.a;
@@ -202,27 +209,25 @@ __global__ void __launch_bounds__(256, 4) k2_near(K2Params P) {
       u2 += __shfl_xor_sync(hmask, u2, o);
     }
     if (hl == 0) {
-      atomicAdd(P.out + 3 * (size_t)i, u0);
-      atomicAdd(P.out + 3 * (size_t)i + 1, u1);
-      atomicAdd(P.out + 3 * (size_t)i + 2, u2);
+      P.pinc[3 * (size_t)pos] = u0;
+      P.pinc[3 * (size_t)pos + 1] = u1;
+      P.pinc[3 * (size_t)pos + 2] = u2;
     }
   }
 }
 
-void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st) {
-  BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
-  g.prof.launches++;
+// K2 into the per-incidence partials g.k2_pinc (summed per target row by k_row_reduce).
+void launch_near(Geom& g, const double* sigS, const double* sigD, cudaStream_t st) {
   if (g.n_inc == 0) return;
   const bool doS = sigS && g.T_S.p, doD = sigD != nullptr;
   if (!doS && !doD) return;
   const int nq = g.nq, nb = g.nb;
   const int nbp = (nb + 1) & ~1;
-  g.coef.ensure((size_t)2 * g.np * nbp * 3);
+  BPQN_REQUIRE(g.coef.n >= (size_t)2 * KC_Z * g.np * nbp * 3, "K2 workspace too small (layer_reserve)");
   double* coefD = g.coef.p;
-  double* coefS = g.coef.p + (size_t)g.np * nbp * 3;
-  // node ranges split over 4 blocks for parallelism (atomic sums into zeroed coefficients)
-  const dim3 cgrid((nbp + KC_BM - 1) / KC_BM, (g.np + KC_BS - 1) / KC_BS, 4);
-  BPQN_CUDA(cudaMemsetAsync(g.coef.p, 0, sizeof(double) * 2 * (size_t)g.np * nbp * 3, st));
+  double* coefS = g.coef.p + (size_t)KC_Z * g.np * nbp * 3;
+  // node ranges split over KC_Z blocks for parallelism, one coefficient slab each
+  const dim3 cgrid((nbp + KC_BM - 1) / KC_BM, (g.np + KC_BS - 1) / KC_BS, KC_Z);
   if (doD) {
     k2_coef<<<cgrid, 256, 0, st>>>(nq, nb, nbp, g.np, g.analysis.p, sigD, coefD);
     BPQN_CHECK_LAUNCH();
@@ -247,13 +252,14 @@ void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, c
   P.coefD = coefD;
   P.sigS = sigS;
   P.sigD = sigD;
+  P.np = g.np;
   P.nq = nq;
   P.nbp = nbp;
   P.t0 = g.shard_world > 1 ? g.sh_t0 : 0;
   P.t1 = g.shard_world > 1 ? g.sh_t1 : g.n;
   P.cS = 1.0 / (8.0 * 3.14159265358979323846 * g.mu);
   P.cD = -3.0 / (4.0 * 3.14159265358979323846);
-  P.out = out;
+  P.pinc = g.k2_pinc.p;
   const int smem = (3 * nq + (doD ? 3 * nq + 3 * nbp : 0) + (doS ? 3 * nq + 3 * nbp : 0)) * 8;
   static std::atomic<int> attr{48 * 1024};  // the opt-in limit only grows
   if (smem > attr.load()) {
@@ -270,8 +276,8 @@ void launch_near(Geom& g, const double* sigS, const double* sigD, double* out, c
 // the same for every sphere (translation invariance of the self rule).  FP64 tensor
 // cores via mma.sync m8n8k4 (DMMA; tcgen05 has no f64 kind).  CTA tile 64 x 72
 // (8 warps, each one 8-row strip x 9 n8 tiles), K in stages of 16 through a 3-deep
-// cp.async ring (zero-filled tails), split-K over gridDim.z with fp64 atomics into an
-// output that k3_prologue initialised with the fused additions (K1 + K2 results).
+// cp.async ring (zero-filled tails), split-K over gridDim.z with a fixed-order reduction of the
+// partial tiles, accumulated into an output that k_row_reduce initialised with the K1 + K2 sums.
 constexpr int K3_BM = 64, K3_BN = 72, K3_BK = 16, K3_ST = 3, K3_LDA = K3_BK + 4;  // LDA 20: conflict-free fragments
 constexpr int K3_SMEM = K3_ST * (K3_BM + K3_BN) * K3_LDA * 8;
 
@@ -287,18 +293,15 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src, bool vali
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src), "r"(sz) : "memory");
 }
 
-__global__ void k3_prologue(size_t n, const double* add1, const double* add2, double* out, int accumulate) {
-  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
-    double v = accumulate ? out[e] : 0.0;
-    if (add1) v += add1[e];
-    if (add2) v += add2[e];
-    out[e] = v;
-  }
-}
-
+// Split-K without atomics: with gridDim.z > 1 every CTA stores its 64 x 72 partial tile in
+// part[z][tile]; the last CTA of a tile to arrive (per-tile counter, reset by that CTA for the
+// next launch or graph replay) adds the ks partials in z order to out -- a fixed summation
+// order, so the result is bit-reproducible.  With one split the CTA writes out directly.
 __global__ void __launch_bounds__(256) k3_self_gemm(int M, int Nn, int kchunk, const double* __restrict__ E,
-                                                    const double* __restrict__ X, double* out) {
+                                                    const double* __restrict__ X, double* out, int accumulate,
+                                                    double* __restrict__ part, unsigned* cnt) {
   extern __shared__ __align__(16) double k3_dyn[];
+  __shared__ unsigned s_last;
   double (*As)[K3_BM][K3_LDA] = reinterpret_cast<double (*)[K3_BM][K3_LDA]>(k3_dyn);
   double (*Bs)[K3_BN][K3_LDA] = reinterpret_cast<double (*)[K3_BN][K3_LDA]>(k3_dyn + K3_ST * K3_BM * K3_LDA);
   const int m0 = blockIdx.x * K3_BM, n0 = blockIdx.y * K3_BN;
@@ -348,19 +351,58 @@ __global__ void __launch_bounds__(256) k3_self_gemm(int M, int Nn, int kchunk, c
   }
   // epilogue: fragment row g, cols 2 t4 + {0, 1} of each n8 tile
   const int row = m0 + warp * 8 + g;
+  const int ks = gridDim.z;
+  if (ks > 1) {
+    const size_t tile = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    const size_t ntile = (size_t)gridDim.x * gridDim.y;
+    double* mine = part + ((size_t)blockIdx.z * ntile + tile) * (K3_BM * K3_BN);
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) mine[(warp * 8 + g) * K3_BN + j * 8 + 2 * t4 + h] = acc[j][h];
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd(cnt + tile, 1u) == (unsigned)(ks - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+#pragma unroll
+    for (int j = 0; j < 9; ++j)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double v = 0.0;
+        for (int z = 0; z < ks; ++z)
+          v += __ldcg(part + ((size_t)z * ntile + tile) * (K3_BM * K3_BN) + (warp * 8 + g) * K3_BN + j * 8 + 2 * t4 + h);
+        acc[j][h] = v;
+      }
+    if (tid == 0) cnt[tile] = 0u;  // ready for the next launch / graph replay
+  }
   if (row < M) {
 #pragma unroll
     for (int j = 0; j < 9; ++j)
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int col = n0 + j * 8 + 2 * t4 + h;
-        if (col < Nn) atomicAdd(out + (size_t)col * M + row, acc[j][h]);
+        if (col < Nn) {
+          double* o = out + (size_t)col * M + row;
+          *o = accumulate ? *o + acc[j][h] : acc[j][h];
+        }
       }
   }
 }
 
-void launch_self_gemm(Geom& g, const double* E, const double* X, const double* add1, const double* add2,
-                      double* out, int accumulate, cudaStream_t st, int s0, int s1) {
+// split-K factor: about two waves of CTAs over the GPU, K chunks of >= 8 stages; one split
+// (a single writer) when sharded
+static int k3_splits(const Geom& g, int mt, int nt, int M) {
+  int ks = std::max(1, std::min((2 * g.sms + mt * nt - 1) / (mt * nt), (M + 8 * K3_BK - 1) / (8 * K3_BK)));
+  if (g.shard_world > 1) ks = 1;
+  int kchunk = (M + ks - 1) / ks;
+  kchunk = ((kchunk + K3_BK - 1) / K3_BK) * K3_BK;
+  return (M + kchunk - 1) / kchunk;
+}
+
+void launch_self_gemm(Geom& g, const double* E, const double* X, double* out, int accumulate, cudaStream_t st,
+                      int s0, int s1) {
   // spheres [s0, s1) only (sharded operator); columns are contiguous per sphere
   if (s1 < 0) s1 = g.np;
   const int M = 3 * g.nq, ncol = s1 - s0;
@@ -368,28 +410,34 @@ void launch_self_gemm(Geom& g, const double* E, const double* X, const double* a
   const size_t off = (size_t)M * s0;
   X += off;
   out += off;
-  if (add1) add1 += off;
-  if (add2) add2 += off;
-  const size_t n = (size_t)M * ncol;
-  k3_prologue<<<(unsigned)std::min<size_t>((n + 255) / 256, 4 * (size_t)g.sms), 256, 0, st>>>(n, add1, add2, out,
-                                                                                            accumulate);
   const int mt = (M + K3_BM - 1) / K3_BM, nt = (ncol + K3_BN - 1) / K3_BN;
-  // split K so that the grid covers the GPU about twice; no split (a single writer per
-  // output, bit-reproducible) when sharded, so that every rank's replicated GMRES agrees
-  int ks = std::max(1, std::min((2 * g.sms + mt * nt - 1) / (mt * nt), (M + 8 * K3_BK - 1) / (8 * K3_BK)));
-  if (g.shard_world > 1) ks = 1;
-  int kchunk = (M + ks - 1) / ks;
-  kchunk = ((kchunk + K3_BK - 1) / K3_BK) * K3_BK;
-  ks = (M + kchunk - 1) / kchunk;
+  const int ks = k3_splits(g, mt, nt, M);
+  const int kchunk = ((((M + ks - 1) / ks) + K3_BK - 1) / K3_BK) * K3_BK;
+  BPQN_REQUIRE(ks == 1 || (g.k3_part.n >= (size_t)ks * mt * nt * K3_BM * K3_BN && g.k3_cnt.n >= (size_t)mt * nt),
+               "K3 workspace too small (layer_reserve)");
   dim3 grid(mt, nt, ks);
   static bool attr = false;
   if (!attr) {
     BPQN_CUDA(cudaFuncSetAttribute(k3_self_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, K3_SMEM));
     attr = true;
   }
-  k3_self_gemm<<<grid, 256, K3_SMEM, st>>>(M, ncol, kchunk, E, X, out);
+  k3_self_gemm<<<grid, 256, K3_SMEM, st>>>(M, ncol, kchunk, E, X, out, accumulate, g.k3_part.p, g.k3_cnt.p);
   BPQN_CHECK_LAUNCH();
-  g.prof.launches += 2;
+  g.prof.launches += 1;
+}
+
+// K2 and K3 workspace, allocated at geometry init / update (no allocation in the hot calls).
+void layer_reserve(Geom& g) {
+  const int nbp = (g.nb + 1) & ~1;
+  g.coef.ensure((size_t)2 * KC_Z * g.np * nbp * 3);
+  g.k2_pinc.ensure(3 * (size_t)std::max<long long>(g.n_inc, 1));
+  const int M = 3 * g.nq, mt = (M + K3_BM - 1) / K3_BM, nt = (g.np + K3_BN - 1) / K3_BN;
+  const int ks = k3_splits(g, mt, nt, M);
+  g.k3_part.ensure((size_t)std::max(ks, 1) * mt * nt * K3_BM * K3_BN);
+  if (g.k3_cnt.n < (size_t)mt * nt) {
+    g.k3_cnt.alloc((size_t)mt * nt);
+    BPQN_CUDA(cudaMemset(g.k3_cnt.p, 0, sizeof(unsigned) * mt * nt));
+  }
 }
 
 // Sharded operator (bpqn_geometry_shard): gather every rank's owned rows into `out`.
@@ -474,7 +522,7 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
     BPQN_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
   }
   if (ev) BPQN_CUDA(cudaEventRecord(ev[2], sk2));
-  launch_near(g, sigS, sigD, g.nearout.p, sk2);
+  launch_near(g, sigS, sigD, sk2);
   if (ev) BPQN_CUDA(cudaEventRecord(ev[3], sk2));
   if (ev) BPQN_CUDA(cudaEventRecord(ev[0], st));
   launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
@@ -491,16 +539,18 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
     BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
   }
   const bool sharded = g.shard_world > 1;
-  if (sharded && k1_sharded_symmetric(g)) shard_reduce_scatter(g, g.far.p, st);
   const int s0 = sharded ? g.sh_s0 : 0, s1 = sharded ? g.sh_s1 : g.np;
-  if (sigS && sigD) {
-    launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st, s0, s1);
-    launch_self_gemm(g, Ed, sigD, nullptr, nullptr, out, 1, st, s0, s1);
-  } else if (sigS) {
-    launch_self_gemm(g, Es, sigS, g.far.p, g.nearout.p, out, 0, st, s0, s1);
+  const int r0 = sharded ? g.sh_t0 : 0, r1 = sharded ? g.sh_t1 : g.n;
+  // out = K1 + K2 (fixed-order row sums), then the self blocks K3 accumulate into it
+  if (sharded && k1_sharded_symmetric(g)) {
+    launch_row_reduce(g, true, nullptr, false, g.far.p, 0, g.n, st);  // this rank's K1 partials, all rows
+    shard_reduce_scatter(g, g.far.p, st);                              // owned rows of far = sum over ranks
+    launch_row_reduce(g, false, g.far.p, true, out, r0, r1, st);
   } else {
-    launch_self_gemm(g, Ed, sigD, g.far.p, g.nearout.p, out, 0, st, s0, s1);
+    launch_row_reduce(g, g.k1lay.sym, g.far.p, true, out, r0, r1, st);
   }
+  if (sigS) launch_self_gemm(g, Es, sigS, out, 1, st, s0, s1);
+  if (sigD) launch_self_gemm(g, Ed, sigD, out, 1, st, s0, s1);
   if (sharded) shard_exchange(g, out, st);
   if (ev) BPQN_CUDA(cudaEventRecord(ev[4], st));
 }

@@ -619,3 +619,53 @@ def test_shard_argument_errors(bp):
     assert L.bpqn_geometry_shard(g.h, 0, 3, buf, buf, cb, None) == 1          # more ranks than spheres
     assert L.bpqn_geometry_shard_symmetric(g.h, buf, buf, cb, None) == 1      # not sharded
     assert L.bpqn_geometry_shard_symmetric(g.h, None, None, bp._bpqn.ALLGATHER_FN(0), None) == 0  # disable: ok
+
+
+# ------------------------------------------------------------------ determinism and the GMRES cycle graph
+def _cfg_geometry(bp, c):
+    from synth import make_config
+    cfg = make_config(c)
+    g = bp.Geometry(cfg["centers"], cfg["p"])
+    bp.contacts(g, cfg["delta"])
+    return g, cfg
+
+
+@pytest.mark.parametrize("c", [1, 2])
+def test_operator_and_mvp_bit_reproducible(bp, c):
+    """No floating-point atomics on the path (fixed-order K1/K2/K3 partial sums, K1-K4):
+    the layer operator and the LCP MVP give bit-identical results run to run.  The first MVP on a
+    handle runs its GMRES steps host-driven, later ones replay the captured cycle graph (conditional
+    WHILE node): identical bits mean the graph runs exactly the same kernels."""
+    import torch
+    from synth import lambda_test
+    g, cfg = _cfg_geometry(bp, c)
+    rng = np.random.default_rng(7)
+    f, q = T(rng.standard_normal((g.N, 3))), T(rng.standard_normal((g.N, 3)))
+    u1 = bp.layer_apply(g, f, q).cpu().numpy()
+    u2 = bp.layer_apply(g, f, q).cpu().numpy()
+    assert np.array_equal(u1, u2)
+    lam = T(lambda_test(c, g.nc, 0))
+    gm = bp.default_gmres_opts(tol=1e-10)
+    ws, its = [], []
+    for _ in range(3):
+        w, st = bp.lcp_mvp(g, lam, gmres=gm)
+        torch.cuda.synchronize()
+        ws.append(w.cpu().numpy())
+        its.append(st.iters)
+    assert len(set(its)) == 1, its
+    assert np.array_equal(ws[0], ws[1]) and np.array_equal(ws[1], ws[2])
+
+
+def test_gmres_restart_cycles_match_unrestarted(bp):
+    """Restarted GMRES(m) with the device-side stopping test: a short restart length (several
+    cycles, each its own graph launch) reaches the same solution as one long cycle."""
+    from synth import lambda_test
+    g, cfg = _cfg_geometry(bp, 1)
+    lam = T(lambda_test(1, g.nc, 1))
+    w_long, st_long = bp.lcp_mvp(g, lam, gmres=bp.default_gmres_opts(tol=1e-12, restart=200))
+    w_short, st_short = bp.lcp_mvp(g, lam, gmres=bp.default_gmres_opts(tol=1e-12, restart=7))
+    w_short2, st_short2 = bp.lcp_mvp(g, lam, gmres=bp.default_gmres_opts(tol=1e-12, restart=7))
+    assert st_short.restarts >= 2 and st_long.restarts == 0
+    assert rel(w_short.cpu().numpy(), w_long.cpu().numpy()) < 1e-10
+    assert np.array_equal(w_short.cpu().numpy(), w_short2.cpu().numpy())
+    assert st_short.iters == st_short2.iters
