@@ -73,8 +73,8 @@ typedef struct {
                          quarter of the free device memory) per handle; it is allocated (and
                          emptied) by bpqn_gmres_recycle_reset and at the start of bpqn_solve_lcp
                          -- never inside an MVP: without a reserved store recycle = 1 is a no-op.
-                         A solve's pair is kept only if its new direction has norm
-                         > max(1e-8, sqrt(tol)) |rhs|.  0: off. */
+                         A solve's pair is kept if its new direction has norm > 1e-8 |rhs|.
+                         0: off. */
 } bpqn_gmres_opts;
 
 typedef struct {
