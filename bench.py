@@ -12,8 +12,11 @@ launching stream, L2 flushed (256 MiB write) between steps outside the events;
 W untimed warm-up steps; max over ranks.  The c5 line (one all-pairs S+D layer
 apply with near and self parts, 259 200 points) gives pair-interactions/s.
 
-N > 1 (torchrun): "replicas only" -- every rank runs its own independent LCP MVP
-(weak scaling, no data-path collective).
+N > 1 (torchrun): the MVP is sharded over the ranks (strong scaling):
+rank r owns Np/N spheres' operator rows, K1 runs an equal share of the symmetric kernel's units,
+and each operator application does one NCCL reduce-scatter and one all-gather on the library's
+own communicator, enqueued on its stream.  --replicas: N independent MVPs instead (weak scaling,
+no data-path collective).
 
 --impl reference times the CPU oracle (oracle/, the only other place bench.py
 executes it) on a bounded sample of the same workload; rank 0 only.
@@ -50,7 +53,8 @@ def parse():
     ap.add_argument("--recycle", type=int, default=1)   # GMRES recycling inside the LCP solve (NEXT-3)
     ap.add_argument("--solvers", default="bi")          # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
-    ap.add_argument("--shard", action="store_true")     # N > 1: shard one MVP over the ranks (NCCL all-gather)
+    ap.add_argument("--replicas", action="store_true")  # N > 1: independent replicas instead of the sharded MVP
+    ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
     ap.add_argument("--shard-asym", action="store_true")  # sharded K1 as the one-directional kernel (no reduce-scatter)
     ap.add_argument("--sub-forcing", type=float, default=0.0)   # Bi-PQN inexact subproblems (off = R22)
     ap.add_argument("--c5-steps", type=int, default=3)
@@ -291,9 +295,15 @@ def run_ours(args, ws, rank, local):
     t_init = time.time() - t0
     pairs, nrm, gaps = bp.contacts(g, cfg["delta"])
     nc = g.nc
-    shard = args.shard and ws > 1
+    shard = ws > 1 and not args.replicas
     if shard:   # strong scaling of one MVP: each rank owns Np/N spheres' rows
-        bp.geometry_shard(g, rank, ws, symmetric=not args.shard_asym)
+        if args.shard_callback:
+            bp.geometry_shard(g, rank, ws, symmetric=not args.shard_asym)
+        else:
+            import torch.distributed as dist
+            uid = [bp.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            bp.geometry_shard_nccl(g, rank, ws, uid[0], symmetric=not args.shard_asym)
     rng = np.random.default_rng(20260000 + args.config + 2000)     # synth.lambda_test recipe
     lam_h = rng.uniform(0.0, 1.0, size=nc)
     lam = torch.tensor(lam_h, dtype=torch.float64, device=dev)
@@ -370,10 +380,11 @@ def run_ours(args, ws, rank, local):
                    "contacts": nc, "gmres_tol": args.gmres_tol, "gmres_restart": gm.restart,
                    "gmres_iters_per_mvp": k_g, "near_incidences": g.n_incidences,
                    "l2": "flushed between steps (256 MiB write outside the per-step events)",
-                   "parallelism": (("shard-targets (one-directional K1, NCCL all-gather per operator application)"
+                   "parallelism": (("shard-targets (one-directional K1, all-gather per operator application)"
                                     if args.shard_asym else
-                                    "shard (symmetric K1 units split, NCCL reduce-scatter + all-gather per operator "
-                                    "application)") if shard
+                                    "shard (symmetric K1 units split, reduce-scatter + all-gather per operator "
+                                    "application)") + (" via torch.distributed callbacks" if args.shard_callback
+                                                       else " on the library's NCCL communicator") if shard
                                    else ("replicas" if ws > 1 else "single GPU")),
                    "geometry_init_s": round(t_init, 3)},
         "pair_interactions_per_s": n_pairs_step * (1 if shard else ws) / (ms_per_step * 1e-3),
@@ -397,9 +408,9 @@ def run_ours(args, ws, rank, local):
     del g
     torch.cuda.empty_cache()
 
-    if not args.no_c5:
+    if not args.no_c5 and ws == 1:
         line["layer_apply_c5"] = run_c5(args, dev, stream)
-    if not args.no_paper:
+    if not args.no_paper and ws == 1:
         line["paper_setting_6x6x6"] = run_paper_setting(args, dev, stream)
 
     if rank == 0 and ws == 1:

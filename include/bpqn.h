@@ -246,6 +246,21 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
 int bpqn_geometry_shard_symmetric(bpqn_geom_t g, double* rs_send_dev, double* rs_recv_dev,
                                   int (*reduce_scatter)(void* user), void* user);
 
+/* Multi-GPU with the library's own NCCL communicator: the same
+ * target-side sharding as bpqn_geometry_shard (rank r of `world` owns spheres [Np r/world,
+ * Np (r+1)/world)), but the collectives of every operator application -- the reduce-scatter of the
+ * symmetric K1 partial sums (symmetric != 0; K1 then runs an equal share of the symmetric kernel's
+ * units on every rank) and the all-gather of the owned rows -- are NCCL calls enqueued on the
+ * handle's stream: no host synchronisation and no callback; the reduce-scatter overlaps K2.
+ * bpqn_nccl_unique_id fills 128 bytes on one rank; the caller distributes them (e.g. a
+ * torch.distributed broadcast) and every rank calls bpqn_geometry_shard_nccl with them (collective).
+ * world = 1 is allowed (a one-rank communicator: the sharded code path on one GPU).  The library
+ * owns the communicator and the exchange buffers (freed by bpqn_geometry_destroy or a later
+ * bpqn_geometry_shard call).  NCCL is loaded at run time (libnccl.so.2; the copy the process already
+ * has, e.g. torch's); BPQN_ERR_CUDA if it is missing. */
+int bpqn_nccl_unique_id(void* uid128);
+int bpqn_geometry_shard_nccl(bpqn_geom_t g, int rank, int world, const void* uid128, int symmetric);
+
 /* Reserve (first call: allocate; BPQN_OK with recycling left off if the memory is not there)
  * and empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
 int bpqn_gmres_recycle_reset(bpqn_geom_t g);

@@ -77,6 +77,8 @@ SYMBOLS = {
     "bpqn_gmres_recycle_reset": (c_int, [c_void_p]),
     "bpqn_geometry_shard": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_geometry_shard_symmetric": (c_int, [c_void_p, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
+    "bpqn_nccl_unique_id": (c_int, [c_void_p]),
+    "bpqn_geometry_shard_nccl": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
     "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
     "bpqn_dvi_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
                               P(SolveOpts), c_void_p, P(StepReport), c_void_p]),
@@ -402,6 +404,22 @@ def geometry_shard(g, rank, world, allgather=None, symmetric=False, reduce_scatt
         rfun = _callback(reduce_scatter or _torch_reduce_scatter, rs_send, rs_recv)
         g._shard = g._shard + (rs_send, rs_recv, rfun)
         _check(lib().bpqn_geometry_shard_symmetric(g.h, _ptr(rs_send), _ptr(rs_recv), rfun, None))
+
+
+def nccl_unique_id():
+    """128 bytes for bpqn_geometry_shard_nccl (call on one rank, distribute to all)."""
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().bpqn_nccl_unique_id(buf))
+    return buf.raw
+
+
+def geometry_shard_nccl(g, rank, world, uid, symmetric=True):
+    """Shard the operator over `world` ranks with the library's own NCCL communicator
+    (bpqn_geometry_shard_nccl; collective: every rank calls it with the same 128-byte uid)."""
+    assert isinstance(uid, (bytes, bytearray)) and len(uid) == 128
+    buf = ctypes.create_string_buffer(bytes(uid), 128)
+    _check(lib().bpqn_geometry_shard_nccl(g.h, rank, world, buf, 1 if symmetric else 0))
+    g._shard = None
 
 
 def gmres_recycle_reset(g):

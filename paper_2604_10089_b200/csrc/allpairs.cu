@@ -747,8 +747,8 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   long long tot = 0;
   for (int b = 0; b < P.nb; ++b) tot += P.nt - b * (KS_B / K1_TS);
   // sharded symmetric K1: this rank's equal share of the unordered (block, tile) units
-  P.ubeg = g.shard_world > 1 ? tot * g.shard_rank / g.shard_world : 0;
-  P.units = g.shard_world > 1 ? tot * (g.shard_rank + 1) / g.shard_world - P.ubeg : tot;
+  P.ubeg = g.sharded() ? tot * g.shard_rank / g.shard_world : 0;
+  P.units = g.sharded() ? tot * (g.shard_rank + 1) / g.shard_world - P.ubeg : tot;
   const int nslot_max = KS_B / g.nq + 2;
   const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
                     (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * 2 * K1_TS)) * 8;
@@ -789,7 +789,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   Ly.psrc_ld = P.psrc_ld;
   BPQN_REQUIRE((size_t)(gr + P.nb) * KS_B * 3 <= g.k1_pseg.n && (size_t)P.nb * P.psrc_ld <= g.k1_psrc.n,
                "K1 partial-sum workspace too small");
-  if (g.shard_world > 1) {  // this rank's share of the units: the other partials read as zero
+  if (g.sharded()) {  // this rank's share of the units: the other partials read as zero
     BPQN_CUDA(cudaMemsetAsync(g.k1_pseg.p, 0, sizeof(double) * (size_t)(gr + P.nb) * KS_B * 3, st));
     BPQN_CUDA(cudaMemsetAsync(g.k1_psrc.p, 0, sizeof(double) * (size_t)P.nb * P.psrc_ld, st));
   }
@@ -892,7 +892,7 @@ static bool k1_sym_eligible(const Geom& g) { return g.nq >= 32 && g.np <= 4096; 
 // Sharded handle whose K1 runs the symmetric kernel over this rank's share of the units: the
 // partial sums cover every target row and must be reduce-scattered (layer.cu).
 bool k1_sharded_symmetric(const Geom& g) {
-  return g.shard_world > 1 && g.sh_rs_fn != nullptr && k1_symmetric() && k1_sym_eligible(g);
+  return g.sharded() && (g.sh_rs_fn != nullptr || g.sh_sym_nccl) && k1_symmetric() && k1_sym_eligible(g);
 }
 
 // All K1 workspace, allocated once per handle (geometry init / update): the packed records and
@@ -910,7 +910,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   const bool sym = k1_symmetric();
   // symmetric kernel: a 32-point group spans <= 2 spheres, centres fit smem, all targets on this
   // GPU (or the sharded symmetric split with its reduce-scatter)
-  const bool use_sym = sym && k1_sym_eligible(g) && (g.shard_world == 1 || g.sh_rs_fn != nullptr);
+  const bool use_sym = sym && k1_sym_eligible(g) && (!g.sharded() || g.sh_rs_fn != nullptr || g.sh_sym_nccl);
   // packed records cover every target block (symmetric: nb blocks of the launch shape) and
   // source tile (one-directional: 64-point tiles); the padding is far away, zero strength
   const int blk = use_sym ? sym_block_points(sym_cfg(g, mode)) : K1_TS;
@@ -931,7 +931,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
     else launch_sym<MODE_SD>(g, out, st);
   } else {
     // sharded (bpqn_geometry_shard): this rank's target rows against all sources
-    const int t0 = g.shard_world > 1 ? g.sh_t0 : 0, t1 = g.shard_world > 1 ? g.sh_t1 : g.n;
+    const int t0 = g.sharded() ? g.sh_t0 : 0, t1 = g.sharded() ? g.sh_t1 : g.n;
     if (mode == MODE_D) launch_asym<MODE_D>(g, out, st, t0, t1);
     else if (mode == MODE_S) launch_asym<MODE_S>(g, out, st, t0, t1);
     else launch_asym<MODE_SD>(g, out, st, t0, t1);

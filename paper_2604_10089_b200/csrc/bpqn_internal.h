@@ -200,6 +200,12 @@ struct Geom {
   int (*sh_rs_fn)(void* user) = nullptr;
   void* sh_rs_user = nullptr;
   std::vector<int> nt_list_h;  // host copy of the near-target list (shard ranges)
+  // NCCL sharding (bpqn_geometry_shard_nccl, comm.cu): the library's own communicator and exchange
+  // buffers; collectives are enqueued on the handle's stream (no host sync, no callback)
+  void* nccl_comm = nullptr;
+  bool sh_sym_nccl = false;  // symmetric K1 split with the NCCL reduce-scatter
+  DBuf<double> sh_own_send, sh_own_recv, sh_own_rs_send, sh_own_rs_recv;
+  bool sharded() const { return shard_world > 1 || nccl_comm != nullptr; }
   ~Geom();
 };
 
@@ -234,6 +240,13 @@ int gmres_solve(Geom& g, const double* rhs, double* x, const bpqn_gmres_opts& o,
                 cudaStream_t s);
 void gmres_reserve(Geom& g, int restart);   // basis and scratch for a restart length (init: default 100)
 void gmres_recycle_reserve(Geom& g);        // recycling store (outside the hot calls; may stay off)
+
+// NCCL (comm.cu)
+void comm_unique_id(void* out128);
+void comm_init(Geom& g, int rank, int world, const void* uid128);
+void comm_destroy(Geom& g);
+void comm_allgather(Geom& g, const double* send, double* recv, size_t count, cudaStream_t st);
+void comm_reduce_scatter(Geom& g, const double* send, double* recv, size_t count, cudaStream_t st);
 
 // small kernels (contacts.cu)
 void launch_pt(Geom& g, const double* ft, double* f, cudaStream_t st);

@@ -18,6 +18,10 @@ static thread_local std::string g_err;
 void set_error(const std::string& msg) { g_err = msg; }
 
 Geom::~Geom() {
+  try {
+    comm_destroy(*this);
+  } catch (...) {
+  }
   if (host_scal) cudaFreeHost(host_scal);
   for (auto& e : prof.pool)
     if (e) cudaEventDestroy(e);
@@ -62,7 +66,7 @@ static bpqn_gmres_opts gm_or_default(const bpqn_gmres_opts* gm) {
 
 // Owned spheres / nodes / near-target entries of this rank (bpqn_geometry_shard).
 static void shard_ranges(Geom& g) {
-  if (g.shard_world <= 1) return;
+  if (!g.sharded()) return;
   g.sh_s0 = (int)((long long)g.np * g.shard_rank / g.shard_world);
   g.sh_s1 = (int)((long long)g.np * (g.shard_rank + 1) / g.shard_world);
   g.sh_t0 = g.sh_s0 * g.nq;
@@ -333,6 +337,9 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
     g->sh_rs_fn = nullptr;
     g->sh_rs_send = g->sh_rs_recv = nullptr;
     g->sh_rs_user = nullptr;
+    comm_destroy(*g);  // callback sharding replaces an NCCL sharding
+    g->sh_sym_nccl = false;
+    g->gm_cycle.clear();
     if (world == 1) {
       g->shard_world = 1;
       g->shard_rank = 0;
@@ -347,6 +354,37 @@ int bpqn_geometry_shard(bpqn_geom_t g, int rank, int world, double* send_dev, do
     g->sh_recv = recv_dev;
     g->sh_fn = allgather;
     g->sh_user = user;
+    shard_ranges(*g);
+    return BPQN_OK;
+  });
+}
+
+int bpqn_nccl_unique_id(void* uid128) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(uid128, "null pointer");
+    comm_unique_id(uid128);
+    return BPQN_OK;
+  });
+}
+
+int bpqn_geometry_shard_nccl(bpqn_geom_t g, int rank, int world, const void* uid128, int symmetric) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && uid128, "null pointer");
+    BPQN_REQUIRE(world >= 1 && rank >= 0 && rank < world, "bad rank / world");
+    BPQN_REQUIRE(world <= g->np, "more ranks than spheres");
+    g->sh_fn = nullptr;
+    g->sh_send = g->sh_recv = nullptr;
+    g->sh_user = nullptr;
+    g->sh_rs_fn = nullptr;
+    g->sh_rs_send = g->sh_rs_recv = nullptr;
+    g->sh_rs_user = nullptr;
+    g->gm_cycle.clear();
+    g->shard_world = 1;
+    g->shard_rank = 0;
+    comm_init(*g, rank, world, uid128);  // collective over the world ranks
+    g->shard_rank = rank;
+    g->shard_world = world;
+    g->sh_sym_nccl = symmetric != 0 && g->nq >= 32 && g->np <= 4096;
     shard_ranges(*g);
     return BPQN_OK;
   });

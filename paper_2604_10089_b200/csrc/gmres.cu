@@ -563,7 +563,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   // handle and restart length; not when profiling events, sharding or BPQN_GRAPHS=0 make the step
   // non-capturable)
   CycleGraph& CG = g.gm_cycle;
-  const bool use_graphs = graphs_enabled() && !g.prof.events && g.shard_world == 1 && !g.overlap_k2 && CG.ok;
+  const bool use_graphs = graphs_enabled() && !g.prof.events && !g.sharded() && !g.overlap_k2 && CG.ok;
   if (CG.exec && (CG.m != m || CG.pre != pre || CG.V != g.V.p || CG.S != g.scal.p || CG.red != g.red.p))
     CG.clear();
   auto build_graph = [&]() -> bool {

@@ -255,8 +255,8 @@ void launch_near(Geom& g, const double* sigS, const double* sigD, cudaStream_t s
   P.np = g.np;
   P.nq = nq;
   P.nbp = nbp;
-  P.t0 = g.shard_world > 1 ? g.sh_t0 : 0;
-  P.t1 = g.shard_world > 1 ? g.sh_t1 : g.n;
+  P.t0 = g.sharded() ? g.sh_t0 : 0;
+  P.t1 = g.sharded() ? g.sh_t1 : g.n;
   P.cS = 1.0 / (8.0 * 3.14159265358979323846 * g.mu);
   P.cD = -3.0 / (4.0 * 3.14159265358979323846);
   P.pinc = g.k2_pinc.p;
@@ -395,7 +395,7 @@ __global__ void __launch_bounds__(256) k3_self_gemm(int M, int Nn, int kchunk, c
 // (a single writer) when sharded
 static int k3_splits(const Geom& g, int mt, int nt, int M) {
   int ks = std::max(1, std::min((2 * g.sms + mt * nt - 1) / (mt * nt), (M + 8 * K3_BK - 1) / (8 * K3_BK)));
-  if (g.shard_world > 1) ks = 1;
+  if (g.sharded()) ks = 1;
   int kchunk = (M + ks - 1) / ks;
   kchunk = ((kchunk + K3_BK - 1) / K3_BK) * K3_BK;
   return (M + kchunk - 1) / kchunk;
@@ -466,26 +466,40 @@ __global__ void k_rs_pack(const double* __restrict__ far, int world, int rows, i
   send[e] = k < 3 * (s1 - s0) * nq ? far[3 * (size_t)s0 * nq + k] : 0.0;
 }
 
+// reduce-scatter of the sharded symmetric K1 partial sums into the owned rows of far: NCCL on the
+// given stream (library communicator), or the caller's callback after a stream sync
 static void shard_reduce_scatter(Geom& g, double* far, cudaStream_t st) {
   const long long tot = 3LL * g.sh_rows * g.shard_world;
-  k_rs_pack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(far, g.shard_world, g.sh_rows, g.np, g.nq, g.sh_rs_send);
+  double* send = g.nccl_comm ? g.sh_own_rs_send.p : g.sh_rs_send;
+  double* recv = g.nccl_comm ? g.sh_own_rs_recv.p : g.sh_rs_recv;
+  k_rs_pack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(far, g.shard_world, g.sh_rows, g.np, g.nq, send);
   BPQN_CHECK_LAUNCH();
-  BPQN_CUDA(cudaStreamSynchronize(st));
-  if (g.sh_rs_fn(g.sh_rs_user) != 0) throw Error{BPQN_ERR_CUDA, "shard reduce-scatter callback failed"};
+  if (g.nccl_comm) {
+    comm_reduce_scatter(g, send, recv, 3 * (size_t)g.sh_rows, st);
+  } else {
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    if (g.sh_rs_fn(g.sh_rs_user) != 0) throw Error{BPQN_ERR_CUDA, "shard reduce-scatter callback failed"};
+  }
   // the owned rows of far <- the sum over ranks
-  BPQN_CUDA(cudaMemcpyAsync(far + 3 * (size_t)g.sh_t0, g.sh_rs_recv, sizeof(double) * 3 * (size_t)(g.sh_t1 - g.sh_t0),
+  BPQN_CUDA(cudaMemcpyAsync(far + 3 * (size_t)g.sh_t0, recv, sizeof(double) * 3 * (size_t)(g.sh_t1 - g.sh_t0),
                             cudaMemcpyDeviceToDevice, st));
   g.prof.launches += 1;
 }
 
 static void shard_exchange(Geom& g, double* out, cudaStream_t st) {
   const int nrow = g.sh_t1 - g.sh_t0;
-  k_shard_pack<<<(3 * g.sh_rows + 255) / 256, 256, 0, st>>>(out, g.sh_t0, nrow, g.sh_send, g.sh_rows);
+  double* send = g.nccl_comm ? g.sh_own_send.p : g.sh_send;
+  double* recv = g.nccl_comm ? g.sh_own_recv.p : g.sh_recv;
+  k_shard_pack<<<(3 * g.sh_rows + 255) / 256, 256, 0, st>>>(out, g.sh_t0, nrow, send, g.sh_rows);
   BPQN_CHECK_LAUNCH();
-  BPQN_CUDA(cudaStreamSynchronize(st));
-  if (g.sh_fn(g.sh_user) != 0) throw Error{BPQN_ERR_CUDA, "shard all-gather callback failed"};
+  if (g.nccl_comm) {
+    comm_allgather(g, send, recv, 3 * (size_t)g.sh_rows, st);
+  } else {
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    if (g.sh_fn(g.sh_user) != 0) throw Error{BPQN_ERR_CUDA, "shard all-gather callback failed"};
+  }
   const long long tot = 3LL * g.sh_rows * g.shard_world;
-  k_shard_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(g.sh_recv, g.shard_world, g.sh_rows, g.np, g.nq, out);
+  k_shard_unpack<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(recv, g.shard_world, g.sh_rows, g.np, g.nq, out);
   BPQN_CHECK_LAUNCH();
   g.prof.launches += 2;
 }
@@ -517,6 +531,34 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
     ev = P.pool.data() + P.used;
     P.used += 5;
   }
+  const bool sharded = g.sharded();
+  const int s0 = sharded ? g.sh_s0 : 0, s1 = sharded ? g.sh_s1 : g.np;
+  const int r0 = sharded ? g.sh_t0 : 0, r1 = sharded ? g.sh_t1 : g.n;
+  if (sharded && g.nccl_comm && k1_sharded_symmetric(g)) {
+    // K1 over this rank's units -> far (all rows); its NCCL reduce-scatter on the side stream
+    // overlaps K2 on the main stream; then out = far(owned) + K2, K3, all-gather
+    if (ev) BPQN_CUDA(cudaEventRecord(ev[0], st));
+    launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
+    if (ev) {
+      BPQN_CUDA(cudaEventRecord(ev[1], st));
+      P.allpairs_flop += (double)g.n * ((double)g.n / g.shard_world) * allpairs_flops_per_pair(mode);
+    }
+    launch_row_reduce(g, true, nullptr, false, g.far.p, 0, g.n, st);
+    BPQN_CUDA(cudaEventRecord(g.ev_fork, st));
+    BPQN_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
+    shard_reduce_scatter(g, g.far.p, g.side);
+    BPQN_CUDA(cudaEventRecord(g.ev_join, g.side));
+    if (ev) BPQN_CUDA(cudaEventRecord(ev[2], st));
+    launch_near(g, sigS, sigD, st);
+    if (ev) BPQN_CUDA(cudaEventRecord(ev[3], st));
+    BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
+    launch_row_reduce(g, false, g.far.p, true, out, r0, r1, st);
+    if (sigS) launch_self_gemm(g, Es, sigS, out, 1, st, s0, s1);
+    if (sigD) launch_self_gemm(g, Ed, sigD, out, 1, st, s0, s1);
+    shard_exchange(g, out, st);
+    if (ev) BPQN_CUDA(cudaEventRecord(ev[4], st));
+    return;
+  }
   if (overlap) {
     BPQN_CUDA(cudaEventRecord(g.ev_fork, st));
     BPQN_CUDA(cudaStreamWaitEvent(g.side, g.ev_fork, 0));
@@ -529,18 +571,15 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   if (ev) {
     BPQN_CUDA(cudaEventRecord(ev[1], st));
     // this rank's share of the nominal N^2 pairs
-    const double ntg = g.shard_world > 1 ? (k1_sharded_symmetric(g) ? (double)g.n / g.shard_world
-                                                                     : (double)(g.sh_t1 - g.sh_t0))
-                                         : (double)g.n;
+    const double ntg = sharded ? (k1_sharded_symmetric(g) ? (double)g.n / g.shard_world
+                                                          : (double)(g.sh_t1 - g.sh_t0))
+                               : (double)g.n;
     P.allpairs_flop += (double)g.n * ntg * allpairs_flops_per_pair(mode);
   }
   if (overlap) {
     BPQN_CUDA(cudaEventRecord(g.ev_join, g.side));
     BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
   }
-  const bool sharded = g.shard_world > 1;
-  const int s0 = sharded ? g.sh_s0 : 0, s1 = sharded ? g.sh_s1 : g.np;
-  const int r0 = sharded ? g.sh_t0 : 0, r1 = sharded ? g.sh_t1 : g.n;
   // out = K1 + K2 (fixed-order row sums), then the self blocks K3 accumulate into it
   if (sharded && k1_sharded_symmetric(g)) {
     launch_row_reduce(g, true, nullptr, false, g.far.p, 0, g.n, st);  // this rank's K1 partials, all rows

@@ -81,3 +81,37 @@ def test_sharded_mvp_two_ranks(c, world, sym, tmp_path):
     assert np.linalg.norm(w0 - w_ref) / np.linalg.norm(w_ref) <= 1e-9
     uo = np.array(res[0]["uo"])
     assert np.linalg.norm(uo - uo_ref) / np.linalg.norm(uo_ref) <= 1e-9
+
+
+@pytest.mark.parametrize("c,sym", [(1, True), (2, True), (2, False)])
+def test_nccl_sharding_one_rank_equals_single_gpu(c, sym):
+    """bpqn_geometry_shard_nccl with a one-rank NCCL communicator (the one GPU of the test box):
+    the sharded code path -- K1 over the rank's units, NCCL reduce-scatter on the side stream
+    overlapping K2, K3 on the owned spheres, NCCL all-gather, all enqueued on the handle's stream
+    without host syncs -- gives the single-GPU operator and MVP.  (NCCL refuses two ranks on one
+    GPU; the multi-rank split itself is covered by the callback tests above.)"""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2604_10089_b200 as bp
+    from synth import lambda_test, make_config
+    cfg = make_config(c)
+    g = bp.Geometry(cfg["centers"], cfg["p"])
+    bp.contacts(g, 0.1)
+    gm = bp.default_gmres_opts(tol=1e-12)
+    lam = torch.tensor(lambda_test(c, g.nc, 0), device="cuda")
+    rng = np.random.default_rng(3)
+    q = torch.tensor(rng.standard_normal((g.N, 3)), device="cuda")
+    u_ref = bp.layer_apply(g, None, q).cpu().numpy()
+    w_ref, _ = bp.lcp_mvp(g, lam, gmres=gm)
+    w_ref = w_ref.cpu().numpy()
+    bp.geometry_shard_nccl(g, 0, 1, bp.nccl_unique_id(), symmetric=sym)
+    u = bp.layer_apply(g, None, q).cpu().numpy()
+    w, _ = bp.lcp_mvp(g, lam, gmres=gm)
+    w2, _ = bp.lcp_mvp(g, lam, gmres=gm)
+    assert np.linalg.norm(u - u_ref) / np.linalg.norm(u_ref) <= 1e-13
+    assert np.linalg.norm(w.cpu().numpy() - w_ref) / np.linalg.norm(w_ref) <= 1e-10
+    assert np.array_equal(w.cpu().numpy(), w2.cpu().numpy())
+    bp.geometry_shard(g, 0, 1)                # back to the single-GPU operator (frees the communicator)
+    w3, _ = bp.lcp_mvp(g, lam, gmres=gm)
+    assert np.array_equal(w3.cpu().numpy(), w_ref)
