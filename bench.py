@@ -466,7 +466,7 @@ def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
            "rc": rc, "lo_geometry_init_s": round(t_lo_init, 3),
            "negative_b_fraction": float((b < 0).double().mean().item()),
            "active_contacts": int((lam > 0).sum().item())}
-    out.update({k: r[k] for k in ("iterations", "hi_mvps", "lo_mvps", "e_mvps", "cost_ratio", "kkt_abs",
+    out.update({k: r[k] for k in ("iterations", "hi_mvps", "lo_mvps", "lo_mvps_init", "e_mvps", "cost_ratio", "kkt_abs",
                                   "gmres_iters_hi", "gmres_iters_lo", "ms_hi", "ms_lo", "termination")})
     if lo is not None:
         lo.close()

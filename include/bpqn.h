@@ -114,6 +114,7 @@ typedef struct {
   double e_mvps, cost_ratio, kkt_abs, kkt_rel, objective, ms_total, ms_hi, ms_lo;
   int termination;            /* 0 KKT_ABS, 1 KKT_REL, 2 MAX_ITER, 3 STALLED */
   double secant_residual;     /* see bpqn_solve_opts.verify_secants (0 otherwise) */
+  int lo_mvps_init;           /* Bi-PQN: lo MVPs of the low-fidelity initialisation (Alg. 3 line 1) */
 } bpqn_report;
 
 /* Defaults for the option structs above. */

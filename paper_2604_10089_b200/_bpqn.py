@@ -43,7 +43,7 @@ class Report(ctypes.Structure):
                 ("gmres_iters_lo", c_int), ("e_mvps", c_double), ("cost_ratio", c_double),
                 ("kkt_abs", c_double), ("kkt_rel", c_double), ("objective", c_double),
                 ("ms_total", c_double), ("ms_hi", c_double), ("ms_lo", c_double), ("termination", c_int),
-                ("secant_residual", c_double)]
+                ("secant_residual", c_double), ("lo_mvps_init", c_int)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -148,7 +148,7 @@ __device__ __forceinline__ double seed_or_zero(double rr) {
 struct K1Params {
   const double* X;     // [N][3] node positions (targets t0 .. t0 + nt - 1)
   const double* pk;    // packed sources [npad][REC]
-  double* out;         // [N][3], zeroed, atomically accumulated (target rows only)
+  double* pseg;        // [grid + n_tb][K1_TB][3]: CTA c's sums over target block tb at segment c + tb
   int t0, nt, n_tb, n_st;
   long long units;     // n_tb * n_st
 };
@@ -189,16 +189,14 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
     const unsigned parity = (unsigned)(i / K1_STAGES) & 1u;
     const int tb = (int)(u / P.n_st);
     if (tb != cur_tb) {
-      if (cur_tb >= 0) {
+      if (cur_tb >= 0) {  // segment blockIdx.x + cur_tb (fixed-order sum in k_row_reduce)
+        double* sg = P.pseg + (size_t)(blockIdx.x + cur_tb) * K1_TB * 3;
 #pragma unroll
         for (int r = 0; r < K1_R; ++r) {
-          const int tl = cur_tb * K1_TB + r * K1_THREADS + tid;
-          const int t = P.t0 + tl;
-          if (tl < P.nt) {
-            atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
-            atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
-            atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
-          }
+          const int lr = r * K1_THREADS + tid;
+          sg[3 * lr] = acc[r][0];
+          sg[3 * lr + 1] = acc[r][1];
+          sg[3 * lr + 2] = acc[r][2];
         }
       }
       cur_tb = tb;
@@ -275,14 +273,14 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
       bulk_g2s(ring[buf], P.pk + (size_t)st * TILE_DBL, TILE_BYTES, &full[buf]);
     }
   }
+  {
+    double* sg = P.pseg + (size_t)(blockIdx.x + cur_tb) * K1_TB * 3;
 #pragma unroll
-  for (int r = 0; r < K1_R; ++r) {
-    const int tl = cur_tb * K1_TB + r * K1_THREADS + tid;
-    const int t = P.t0 + tl;
-    if (tl < P.nt) {
-      atomicAdd(P.out + 3 * (size_t)t, acc[r][0]);
-      atomicAdd(P.out + 3 * (size_t)t + 1, acc[r][1]);
-      atomicAdd(P.out + 3 * (size_t)t + 2, acc[r][2]);
+    for (int r = 0; r < K1_R; ++r) {
+      const int lr = r * K1_THREADS + tid;
+      sg[3 * lr] = acc[r][0];
+      sg[3 * lr + 1] = acc[r][1];
+      sg[3 * lr + 2] = acc[r][2];
     }
   }
 }
@@ -638,9 +636,11 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
 // bit-reproducible run to run (no floating-point atomics anywhere on the path).
 struct RowRedParams {
   int N, r0, r1;
-  const double *pseg, *psrc;  // symmetric K1 partials (pseg == nullptr: use far)
+  const double *pseg, *psrc;  // K1 partials (pseg == nullptr: use far); psrc: symmetric kernel only
   size_t psrc_ld;
   int ks_b, tpb, nt, grid;
+  int tri;                    // 1: symmetric kernel (block b has nt - b tpb units); 0: one-directional
+  int t0;                     // one-directional: first target row of the launch (blocks from t0)
   long long ubeg, units;
   const double* far;
   const double* pinc;         // K2 partials [n_inc][3] (K2 order) or nullptr
@@ -664,14 +664,18 @@ __global__ void k_row_reduce(RowRedParams P) {
   const int i = (int)(e / 3), c = (int)(e - 3LL * i);
   double v = 0.0;
   if (P.pseg) {
-    const int b = i / P.ks_b, local = i - b * P.ks_b;
-    const long long Ub = (long long)b * P.nt - (long long)P.tpb * b * (b - 1) / 2;  // units before block b
-    const long long lo = max(Ub, P.ubeg), hi = min(Ub + (P.nt - (long long)b * P.tpb), P.ubeg + P.units);
+    const int il = i - P.t0;
+    const int b = il / P.ks_b, local = il - b * P.ks_b;
+    // units of block b: symmetric kernel nt - b tpb (tiles from the block's first on), else nt
+    const long long Ub = P.tri ? (long long)b * P.nt - (long long)P.tpb * b * (b - 1) / 2 : (long long)b * P.nt;
+    const long long nu = P.tri ? (P.nt - (long long)b * P.tpb) : (long long)P.nt;
+    const long long lo = max(Ub, P.ubeg), hi = min(Ub + nu, P.ubeg + P.units);
     if (lo < hi) {
       const int c0 = k1_cta_of(lo, P.ubeg, P.units, P.grid), c1 = k1_cta_of(hi - 1, P.ubeg, P.units, P.grid);
       for (int cc = c0; cc <= c1; ++cc) v += P.pseg[((size_t)(cc + b) * P.ks_b + local) * 3 + c];
     }
-    for (int bb = 0; bb < b; ++bb) v += P.psrc[(size_t)bb * P.psrc_ld + e];
+    if (P.tri)
+      for (int bb = 0; bb < b; ++bb) v += P.psrc[(size_t)bb * P.psrc_ld + e];
   } else if (P.far) {
     v = P.far[e];
   }
@@ -694,6 +698,8 @@ void launch_row_reduce(Geom& g, bool k1_partials, const double* far, bool with_k
     P.tpb = g.k1lay.tpb;
     P.nt = g.k1lay.nt;
     P.grid = g.k1lay.grid;
+    P.tri = g.k1lay.sym ? 1 : 0;
+    P.t0 = g.k1lay.t0;
     P.ubeg = g.k1lay.ubeg;
     P.units = g.k1lay.units;
   }
@@ -879,10 +885,23 @@ static void launch_asym(Geom& g, double* out, cudaStream_t st, int t0, int t1) {
   P.units = (long long)P.n_tb * P.n_st;
   P.X = g.X.p;
   P.pk = g.packed.p;
-  P.out = out;
+  P.pseg = g.k1_pseg.p;
   static int grid = 0;
   if (!grid) grid = k1_grid(g, k1_allpairs<MODE>, K1_THREADS);
-  const int gr = (int)std::min<long long>(grid, P.units);
+  const int gr = (int)std::max<long long>(1, std::min<long long>(grid, P.units));
+  K1Layout& Ly = g.k1lay;
+  Ly.sym = false;
+  Ly.ks_b = K1_TB;
+  Ly.tpb = 0;
+  Ly.nt = P.n_st;
+  Ly.nb = P.n_tb;
+  Ly.grid = gr;
+  Ly.t0 = t0;
+  Ly.ubeg = 0;
+  Ly.units = P.units;
+  Ly.psrc_ld = 0;
+  BPQN_REQUIRE((size_t)(gr + P.n_tb) * K1_TB * 3 <= g.k1_pseg.n, "K1 partial-sum workspace too small");
+  if (P.units == 0) return;
   k1_allpairs<MODE><<<gr, K1_THREADS, 0, st>>>(P);
 }
 
@@ -898,7 +917,9 @@ bool k1_sharded_symmetric(const Geom& g) {
 // All K1 workspace, allocated once per handle (geometry init / update): the packed records and
 // the deterministic partial-sum buffers for every mode's launch shape -- the hot calls allocate nothing.
 void k1_reserve(Geom& g) {
-  size_t pseg = 1, psrc = 1, packed = ((g.n + K1_TS - 1) / K1_TS) * (size_t)K1_TS * 14;
+  // one-directional kernel: (grid + target blocks) segments of K1_TB rows (grid <= 4 CTAs per SM)
+  size_t pseg = (size_t)(4 * g.sms + (g.n + K1_TB - 1) / K1_TB) * K1_TB * 3, psrc = 1,
+         packed = ((g.n + K1_TS - 1) / K1_TS) * (size_t)K1_TS * 14;
   if (k1_sym_eligible(g))
     for (int mode = 0; mode < 3; ++mode) sym_ws(g, sym_cfg(g, mode), pseg, psrc, packed);
   g.k1_pseg.ensure(pseg);
@@ -924,7 +945,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
                                                -3.0 / (4.0 * PI_A), g.packed.p);
   BPQN_CHECK_LAUNCH();
   g.k1lay.sym = use_sym;
-  if (!use_sym) BPQN_CUDA(cudaMemsetAsync(out, 0, sizeof(double) * 3 * (size_t)g.n, st));
+  g.k1lay.t0 = 0;
   if (use_sym) {
     if (mode == MODE_D) launch_sym<MODE_D>(g, out, st);
     else if (mode == MODE_S) launch_sym<MODE_S>(g, out, st);

@@ -107,8 +107,8 @@ struct CycleGraph {
 
 // Launch layout of the last symmetric K1 launch: how k_row_reduce finds its partial sums.
 struct K1Layout {
-  bool sym = false;
-  int ks_b = 0, tpb = 0, nt = 0, nb = 0, grid = 0;
+  bool sym = false;  // symmetric kernel (else the one-directional kernel over rows t0..)
+  int ks_b = 0, tpb = 0, nt = 0, nb = 0, grid = 0, t0 = 0;
   long long ubeg = 0, units = 0;
   size_t psrc_ld = 0;
 };

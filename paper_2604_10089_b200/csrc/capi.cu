@@ -627,6 +627,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     std::vector<double> x;
     int iters = 0, term = 2, hi_mvps = 0, lo_mvps = 0;
     double kkt = 0, kkt_rel = 0, secant_res = 0;
+    int lo_init = 0;
     if (bi) {
       MvpFn flo = make(lo, glo, ms_lo, it_lo, n_lo);
       BiResult r = bi_pqn(fhi, flo, b, x0, q);
@@ -639,6 +640,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       kkt = r.kkt;
       kkt_rel = r.kkt_rel;
       secant_res = r.secant_residual;
+      lo_init = r.init_lo_mvps;
     } else {
       MonoResult r = o.method == 2 ? bb_pgd(fhi, b, x0, q) : mono_pqn(fhi, b, x0, q, nullptr, nullptr, nullptr);
       prox_profile_flush();
@@ -670,6 +672,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       rep->ms_lo = ms_lo;
       rep->termination = term;
       rep->secant_residual = secant_res;
+      rep->lo_mvps_init = lo_init;
     }
     if (gm_fail) {
       set_error("an inner GMRES solve did not converge");
@@ -843,6 +846,7 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
         rep->kkt_abs = r.kkt;
         rep->termination = term;
         rep->secant_residual = r.secant_residual;
+        rep->lo_mvps_init = r.init_lo_mvps;
       }
     } else {
       MonoResult r = o.method == 2 ? bb_pgd(dense(A), b, x0, q) : mono_pqn(dense(A), b, x0, q, nullptr, nullptr, nullptr);

@@ -586,7 +586,7 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
     shard_reduce_scatter(g, g.far.p, st);                              // owned rows of far = sum over ranks
     launch_row_reduce(g, false, g.far.p, true, out, r0, r1, st);
   } else {
-    launch_row_reduce(g, g.k1lay.sym, g.far.p, true, out, r0, r1, st);
+    launch_row_reduce(g, true, nullptr, true, out, r0, r1, st);  // K1 segment partials (either kernel)
   }
   if (sigS) launch_self_gemm(g, Es, sigS, out, 1, st, s0, s1);
   if (sigD) launch_self_gemm(g, Ed, sigD, out, 1, st, s0, s1);

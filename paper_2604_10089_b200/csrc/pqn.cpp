@@ -732,6 +732,7 @@ BiResult bi_pqn(const MvpFn& hi, const MvpFn& lo, const Vec& b, const Vec& x_ini
   };
   MonoResult r0 = mono_pqn(lo_aux, b, x_init, o, nullptr, nullptr, nullptr);
   R.lo_mvps += r0.mvps;
+  R.init_lo_mvps = r0.mvps;
   Vec x = r0.x, Ahat_x = r0.aux;
   std::vector<std::pair<Vec, Vec>> low = r0.pairs;
   Vec g(n);

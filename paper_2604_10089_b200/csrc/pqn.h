@@ -52,7 +52,7 @@ struct MonoResult {
 
 struct BiResult {
   std::vector<double> x, g;
-  int iterations = 0, hi_mvps = 0, lo_mvps = 0, termination = 2, init_iterations = 0;
+  int iterations = 0, hi_mvps = 0, lo_mvps = 0, termination = 2, init_iterations = 0, init_lo_mvps = 0;
   std::vector<int> sub_iterations;
   double kkt = 0, kkt_rel = 0;
   double secant_residual = 0;  // with verify_secants: max over subproblems and seeded pairs
