@@ -219,6 +219,10 @@ int bpqn_geometry_update(bpqn_geom_t g, const double* centers_host, void* stream
  * A_host, Ahat_host [n][n] row-major (Ahat NULL -> Mono-PQN), b_host, x_host [n]. */
 int bpqn_solve_lcp_dense(const double* A_host, const double* Ahat_host, int n, const double* b_host,
                          double* x_host, const bpqn_solve_opts* o, bpqn_report* rep);
+/* The same with device arrays (SURVEY 8(b) signature): A_dev, Ahat_dev [n][n] (Ahat NULL -> Mono-PQN),
+ * b_dev, x_dev [n] (x: in = x_init, out = solution); all copies on `stream`, which is synchronised. */
+int bpqn_solve_lcp_dense_dev(const double* A_dev, const double* Ahat_dev, int n, const double* b_dev, double* x_dev,
+                             const bpqn_solve_opts* o, bpqn_report* rep, void* stream);
 
 /* Multi-GPU (one process per GPU): shard the target side of the layer
  * operator.  Rank r of `world` owns spheres [Np r/world, Np (r+1)/world); every operator
@@ -265,6 +269,13 @@ int bpqn_geometry_shard_nccl(bpqn_geom_t g, int rank, int world, const void* uid
 /* Reserve (first call: allocate; BPQN_OK with recycling left off if the memory is not there)
  * and empty the GMRES recycling store of a handle (see bpqn_gmres_opts.recycle). */
 int bpqn_gmres_recycle_reset(bpqn_geom_t g);
+
+/* Diagnostic (tests; not on the hot path): exhaustive sweep of the MUFU.RSQ64H seed y of
+ * rsqrt.approx.ftz.f64 that K1 / K2 refine with a truncated series: for every
+ * input rr = 2^e (1 + m) with e in [exp_lo, exp_hi] and every 20-bit high mantissa pattern (the
+ * seed reads the high word; the low word's extremes bound e = 1 - rr y^2 monotonically) writes
+ * max |1 - rr y^2| to *max_abs_e (host).  Allocates and synchronises the default stream. */
+int bpqn_diag_rsqrt_seed(int exp_lo, int exp_hi, double* max_abs_e);
 
 /* Thread-local message for the last non-zero return. */
 const char* bpqn_last_error(void);

@@ -4,7 +4,8 @@ Reading R10 / O1: the paper only states that order-p spherical
 harmonics with N = 6 Np p(p+1) dof are used.  Per sphere we use
 (p+1) Gauss-Legendre nodes in t = cos(theta) (k = 0 nearest the north pole) times
 2p equispaced phi_l = pi l / p, weight w_kl = a^2 omega_k pi / p, local index
-i = k*2p + l.  Pinned by tests/test_oracle_grid.py (sphere moments, sum w = 4 pi a^2).
+i = k*2p + l.  Pinned by tests/test_oracle_geometry.py::test_grid_moments (sphere moments to degree 2p,
+sum w = 4 pi a^2).
 """
 import numpy as np
 

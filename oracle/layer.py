@@ -13,7 +13,8 @@ x_i of sphere n
 - S_self / D_self: rotated-grid singular quadrature of order p_s = 2p (R5, R6).
 
 The paper treats this operator as a black box.
-Pins: tests/test_oracle_layer.py.
+Pins: tests/test_oracle_operator.py (test_direct_sum_vs_longdouble,
+test_layer_far_field_and_gauss, test_layer_targets_subset_matches_all).
 """
 import numpy as np
 

@@ -7,7 +7,8 @@ lexicographic i < j), O8-O10.
 
 Column l of D: -n_l in sphere i's force rows, +n_l in sphere j's force rows, zero
 torque rows, n_l = (c_j - c_i)/|c_j - c_i|.
-Pins (tests/test_oracle_lcp.py): D column = finite difference of Phi; D^T of a
+Pins (tests/test_oracle_operator.py::test_contacts_and_D, test_lcp_matrix_pd_near_contact;
+tests/test_oracle_pqn.py brute-force LCPs): D column = finite difference of Phi; D^T of a
 common translation = 0; A = D^T M D symmetric / PSD to a p-dependent tolerance
 (R27); brute-force active-set enumeration (O14) agrees with the PQN solvers.
 """

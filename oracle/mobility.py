@@ -13,7 +13,8 @@ the BIE.  Readings R1-R4, O7:
 
 GMRES here is the textbook full (unrestarted) Arnoldi + modified Gram-Schmidt +
 Givens iteration from q0 = 0 to relative residual <= tol (default 1e-13).
-Pins (tests/test_oracle_mobility.py): single sphere U = F/(6 pi mu a),
+Pins (tests/test_oracle_operator.py: test_single_sphere_mobility, test_single_janus_sphere,
+test_gmres_vs_dense_solve, test_rotation_covariance, test_far_spheres_rpy): single sphere U = F/(6 pi mu a),
 Omega = T/(8 pi mu a^3); single Janus sphere U = -<u_s>; GMRES vs dense LU on a
 tiny scene; exact discrete covariance under z-rotation by pi/p and z-reflection;
 two far spheres vs Rotne-Prager-Yamakawa.

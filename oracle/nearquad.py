@@ -17,7 +17,8 @@ evaluation only as O(p^4) / FFT-accelerated.  Definition:
   the density there is the Pi_p interpolant of sphere m's nodal density.
 * the refined rule REPLACES the coarse nodal sum over sphere m for that target.
 
-Accuracy (tests/test_oracle_near.py): the exterior closed forms (translating /
+Accuracy (tests/test_oracle_geometry.py: test_near_rule_exterior_closed_forms,
+test_near_rule_converged_random_density): the exterior closed forms (translating /
 rotating sphere field for S, D[const] = 0 outside) hold to <= 1e-12 for
 h in [1e-4, d_near], and a random V_p density agrees with a 4x finer rule.
 """

@@ -12,7 +12,8 @@ with a dense solve -- it does NOT use the closed-form "halve the cos(p phi)
 coefficient" shortcut the CUDA path uses (App. A.3), so agreement of the two is a
 check of that derivation.
 
-Pins (tests/test_oracle_sh.py): the Legendre recurrence against
+Pins (tests/test_oracle_geometry.py: test_legendre_vs_scipy,
+test_legendre_recurrence_small_closed_forms, test_sh_orthonormal_and_nyquist, test_projection): the Legendre recurrence against
 scipy.special.sph_harm_y; orthonormality under exact (high-order) quadrature;
 Pi reproduces V_p and is idempotent; Pi annihilates sin(p phi) P_p^p.
 """

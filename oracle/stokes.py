@@ -14,7 +14,7 @@ kernel * (Pi_p interpolant of the density) there:
     S_self[i, j] = sum_s w'_s G(x_i - y'_s) Pi_j(y'_s),
     w'_s = a^2 sin(theta'_k) (pi/2) omega'_k (pi/p_s).
 
-Pins (tests/test_oracle_stokes.py): closed forms on a sphere (App. A.1):
+Pins (tests/test_oracle_geometry.py: test_self_closed_forms, test_self_converged_in_ps): closed forms on a sphere (App. A.1):
 S[const] = 2a/(3 mu) const (Stokes drag), S[rotation traction] = Omega x x,
 S[xi] = 0; Gauss identity D[const] = const/2, rigid motions eigenvalue +1/2, the
 normal field eigenvalue -1/2; both to <= 1e-10 at the configs' p.

@@ -73,11 +73,14 @@ SYMBOLS = {
     "bpqn_lcp_b": (c_int, [c_void_p, c_void_p, c_void_p, c_double, c_void_p, P(GmresOpts), P(GmresStats), c_void_p]),
     "bpqn_solve_lcp": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, P(SolveOpts), P(Report), c_void_p]),
     "bpqn_solve_lcp_dense": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, P(SolveOpts), P(Report)]),
+    "bpqn_solve_lcp_dense_dev": (c_int, [c_void_p, c_void_p, c_int, c_void_p, c_void_p, P(SolveOpts), P(Report),
+                                         c_void_p]),
     "bpqn_last_error": (ctypes.c_char_p, []),
     "bpqn_gmres_recycle_reset": (c_int, [c_void_p]),
     "bpqn_geometry_shard": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_geometry_shard_symmetric": (c_int, [c_void_p, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_nccl_unique_id": (c_int, [c_void_p]),
+    "bpqn_diag_rsqrt_seed": (c_int, [c_int, c_int, P(c_double)]),
     "bpqn_geometry_shard_nccl": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
     "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
     "bpqn_dvi_step": (c_int, [c_void_p, c_void_p, c_void_p, c_void_p, c_void_p, c_double, c_double, c_double,
@@ -300,6 +303,17 @@ def solve_lcp_dense(A, b, x0=None, Ahat=None, opts=None):
     return x, rep, rc
 
 
+def solve_lcp_dense_dev(A, b, x, Ahat=None, opts=None, stream=None):
+    """Dense LCP solve with CUDA tensors (x: initial guess in, solution out)."""
+    rep = Report()
+    rc = lib().bpqn_solve_lcp_dense_dev(_ptr(A), _ptr(Ahat), int(b.shape[0]), _ptr(b), _ptr(x),
+                                        ctypes.byref(opts) if opts is not None else None, ctypes.byref(rep),
+                                        _stream(stream))
+    if rc not in (0, 4, 5):
+        _check(rc)
+    return x, rep, rc
+
+
 def geometry_update(g, centers, stream=None):
     """Move the handle to new centres (same spheres, p); clears its contact set."""
     import numpy as np
@@ -404,6 +418,13 @@ def geometry_shard(g, rank, world, allgather=None, symmetric=False, reduce_scatt
         rfun = _callback(reduce_scatter or _torch_reduce_scatter, rs_send, rs_recv)
         g._shard = g._shard + (rs_send, rs_recv, rfun)
         _check(lib().bpqn_geometry_shard_symmetric(g.h, _ptr(rs_send), _ptr(rs_recv), rfun, None))
+
+
+def diag_rsqrt_seed(exp_lo, exp_hi):
+    """max |1 - rr y^2| of the MUFU.RSQ64H seed over every high-word pattern with exponents in range."""
+    v = c_double()
+    _check(lib().bpqn_diag_rsqrt_seed(exp_lo, exp_hi, ctypes.byref(v)))
+    return v.value
 
 
 def nccl_unique_id():

@@ -366,11 +366,16 @@ __global__ void k1_pack_sym(int mode, int N, int npad, const double* __restrict_
 // needs no zero mask: padded targets occur only in the last block, whose tiles are all
 // diagonal).  MIXED: the group straddles the tile's sphere boundary (per-pair select of h);
 // otherwise h is chosen once per group (always so at p = 16, where Nq = 17 x 32).
-template <int MODE, int R, bool SYM, bool MIXED, int UNR>
+// TQ: the targets' own densities (record entries >= 3, used by the reverse direction only) live in
+// shared memory (tq[c - 3][tq_stride], this lane's entry of target r at tq[(c - 3) tq_stride + 32 r])
+// instead of registers -- fewer live registers per target, more room to interleave pair chains.
+#define K1_TGV(r, c) (TQ ? tq[((c) - 3) * tq_stride + (r) * 32] : tg[r][c])
+template <int MODE, int R, bool SYM, bool MIXED, int UNR, bool TQ>
 __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const double (&tg)[R][TgtN<MODE>::n],
                                          const double (&h)[R][2], int jl0, int jb, double inv2a,
                                          const double* __restrict__ Hg, const int (&slot)[R], double (&acc)[R][3],
-                                         int lane, double& as0, double& as1, double& as2) {
+                                         int lane, double& as0, double& as1, double& as2, const double* tq,
+                                         int tq_stride) {
   constexpr int REC = RecS<MODE>::n;
   constexpr int QO = MODE == MODE_D ? 3 : 6;  // offset of q~ in a source record
   double hu[R];
@@ -409,11 +414,11 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
         acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
         acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
         if (SYM) {  // G(-r) = G(r)
-          const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+          const double rf2 = fma(r2, K1_TGV(r, 5), fma(r1, K1_TGV(r, 4), r0 * K1_TGV(r, 3)));
           const double tb = rf2 * s3;
-          as0 = fma(tg[r][3], s, fma(r0, tb, as0));
-          as1 = fma(tg[r][4], s, fma(r1, tb, as1));
-          as2 = fma(tg[r][5], s, fma(r2, tb, as2));
+          as0 = fma(K1_TGV(r, 3), s, fma(r0, tb, as0));
+          as1 = fma(K1_TGV(r, 4), s, fma(r1, tb, as1));
+          as2 = fma(K1_TGV(r, 5), s, fma(r2, tb, as2));
         }
       } else {
         const double hm = MIXED ? (second ? h[r][1] : h[r][0]) : hu[r];
@@ -436,7 +441,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           acc[r][2] = fma(r2, tf, acc[r][2]);
           if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5, r.n_i = (rho^2 - H)/(2a)
             const double rn2 = fma(rr, inv2a, -lds_f64(hb[r] + 8 * k));
-            const double rq2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
+            const double rq2 = fma(r2, K1_TGV(r, 5), fma(r1, K1_TGV(r, 4), r0 * K1_TGV(r, 3)));
             const double tb = (rn2 * rq2) * s5;
             as0 = fma(-r0, tb, as0);
             as1 = fma(-r1, tb, as1);
@@ -450,12 +455,12 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
           if (SYM) {
             const double rn2 = fma(rr, inv2a, -lds_f64(hb[r] + 8 * k));
-            const double rf2 = fma(r2, tg[r][5], fma(r1, tg[r][4], r0 * tg[r][3]));
-            const double rq2 = fma(r2, tg[r][8], fma(r1, tg[r][7], r0 * tg[r][6]));
+            const double rf2 = fma(r2, K1_TGV(r, 5), fma(r1, K1_TGV(r, 4), r0 * K1_TGV(r, 3)));
+            const double rq2 = fma(r2, K1_TGV(r, 8), fma(r1, K1_TGV(r, 7), r0 * K1_TGV(r, 6)));
             const double tb = fma(rf2, s3, -((rn2 * rq2) * s5));
-            as0 = fma(tg[r][3], s, fma(r0, tb, as0));
-            as1 = fma(tg[r][4], s, fma(r1, tb, as1));
-            as2 = fma(tg[r][5], s, fma(r2, tb, as2));
+            as0 = fma(K1_TGV(r, 3), s, fma(r0, tb, as0));
+            as1 = fma(K1_TGV(r, 4), s, fma(r1, tb, as1));
+            as2 = fma(K1_TGV(r, 5), s, fma(r2, tb, as2));
           }
         }
       }
@@ -469,7 +474,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
   }
 }
 
-template <int MODE, int KS_W, int R, int MINB, int UNR>
+template <int MODE, int KS_W, int R, int MINB, int UNR, bool TQ = false>
 __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   constexpr int REC = RecS<MODE>::n;
   constexpr int TN = TgtN<MODE>::n;
@@ -482,7 +487,8 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
   double (*ring)[TILE_DBL] = reinterpret_cast<double (*)[TILE_DBL]>(k1_dyn);            // [NS][TILE_DBL]
   double (*red)[KS_W][K1_TS * 3] =
       reinterpret_cast<double (*)[KS_W][K1_TS * 3]>(k1_dyn + NS * TILE_DBL);             // [2][W][192]
-  double* cs = k1_dyn + NS * TILE_DBL + 2 * KS_W * K1_TS * 3;                             // centres [Np][3]
+  double* tqs = k1_dyn + NS * TILE_DBL + 2 * KS_W * K1_TS * 3;                            // TQ: [TN-3][KS_B]
+  double* cs = tqs + (TQ ? (TN - 3) * KS_B : 0);                                          // centres [Np][3]
   double* Hs = cs + (MODE == MODE_S ? 0 : 3 * P.np);                                      // [slots][2 K1_TS]
   __shared__ __align__(8) uint64_t full[NS];
 
@@ -541,7 +547,10 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
         const int t = b_cur * KS_B + warp * 32 * R + r * 32 + lane;  // < npad
         const double* rec = P.pk + (size_t)REC * t;
 #pragma unroll
-        for (int c = 0; c < TN; ++c) tg[r][c] = rec[c];
+        for (int c = 0; c < TN; ++c) {
+          if (TQ && c >= 3) tqs[(c - 3) * KS_B + warp * 32 * R + r * 32 + lane] = rec[c];
+          else tg[r][c] = rec[c];
+        }
         slot[r] = min(t / P.nq, P.np - 1) - fs;
         acc[r][0] = acc[r][1] = acc[r][2] = 0.0;
       }
@@ -587,13 +596,17 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       const double* gr = ring[buf] + grp * 32 * REC;
       double as0 = 0.0, as1 = 0.0, as2 = 0.0;
       const bool mixed = jb < grp * 32 + 32;
+      const double* tql = tqs + warp * 32 * R + lane;
       if (diag) {
-        k1_group<MODE, R, false, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
+        k1_group<MODE, R, false, true, UNR, TQ>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2,
+                                                tql, KS_B);
       } else {
         if (mixed)
-          k1_group<MODE, R, true, true, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
+          k1_group<MODE, R, true, true, UNR, TQ>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1,
+                                                 as2, tql, KS_B);
         else
-          k1_group<MODE, R, true, false, UNR>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1, as2);
+          k1_group<MODE, R, true, false, UNR, TQ>(gr, tg, hs, grp * 32, jb, inv2a, Hs, slot, acc, lane, as0, as1,
+                                                  as2, tql, KS_B);
         double* rw = red[par][warp] + (grp * 32 + lane) * 3;
         rw[0] = as0;
         rw[1] = as1;
@@ -736,7 +749,7 @@ static bool k1_symmetric() {
   return v == 1;
 }
 
-template <int MODE, int W, int R, int MINB, int UNR = 2>
+template <int MODE, int W, int R, int MINB, int UNR = 2, bool TQ = false>
 static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   constexpr int KS_B = 32 * R * W;
   K1SymParams P;
@@ -756,7 +769,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   P.ubeg = g.sharded() ? tot * g.shard_rank / g.shard_world : 0;
   P.units = g.sharded() ? tot * (g.shard_rank + 1) / g.shard_world - P.ubeg : tot;
   const int nslot_max = KS_B / g.nq + 2;
-  const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 +
+  const int smem = (K1_STAGES * K1_TS * RecS<MODE>::n + 2 * W * K1_TS * 3 + (TQ ? (TgtN<MODE>::n - 3) * KS_B : 0) +
                     (MODE == MODE_S ? 0 : 3 * g.np + nslot_max * 2 * K1_TS)) * 8;
   // per instantiation: the opt-in smem limit only grows; occupancy cached per smem size
   // (hi and lo fidelity handles alternate in Bi-PQN with different table sizes)
@@ -767,7 +780,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
   {
     std::lock_guard<std::mutex> lock(mu);
     if (smem > attr_smem) {
-      BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      BPQN_CUDA(cudaFuncSetAttribute(k1_sym<MODE, W, R, MINB, UNR, TQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      smem));
       attr_smem = smem;
     }
@@ -775,7 +788,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
       if (e.first == smem) grid = e.second;
     if (!grid) {
       int b = 0;
-      BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB, UNR>, 32 * W, smem));
+      BPQN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, k1_sym<MODE, W, R, MINB, UNR, TQ>, 32 * W, smem));
       grid = std::max(1, b) * g.sms;
       occ.emplace_back(smem, grid);
     }
@@ -800,7 +813,7 @@ static void launch_sym_cfg(Geom& g, double* out, cudaStream_t st) {
     BPQN_CUDA(cudaMemsetAsync(g.k1_psrc.p, 0, sizeof(double) * (size_t)P.nb * P.psrc_ld, st));
   }
   if (P.units == 0) return;  // a rank with no share (more ranks than units): every partial stays zero
-  k1_sym<MODE, W, R, MINB, UNR><<<gr, 32 * W, smem, st>>>(P);
+  k1_sym<MODE, W, R, MINB, UNR, TQ><<<gr, 32 * W, smem, st>>>(P);
 }
 
 static int sym_block_points(int c);
@@ -847,6 +860,12 @@ static int sym_block_points(int c) {
     case 14: return 32 * 8 * 5;
     case 15: return 32 * 8 * 6;
     case 16: return 32 * 4 * 6;
+    case 17: return 32 * 8 * 5;
+    case 18: return 32 * 8 * 6;
+    case 19: return 32 * 12 * 4;
+    case 20: return 32 * 12 * 3;
+    case 21: return 32 * 16 * 3;
+    case 22: return 32 * 8 * 4;
     default: return 32 * 8 * 2;
   }
 }
@@ -871,6 +890,12 @@ static void launch_sym(Geom& g, double* out, cudaStream_t st) {
     case 14: launch_sym_cfg<MODE, 8, 5, 1>(g, out, st); break;
     case 15: launch_sym_cfg<MODE, 8, 6, 1>(g, out, st); break;
     case 16: launch_sym_cfg<MODE, 4, 6, 2>(g, out, st); break;
+    case 17: launch_sym_cfg<MODE, 8, 5, 1, 2, true>(g, out, st); break;
+    case 18: launch_sym_cfg<MODE, 8, 6, 1, 2, true>(g, out, st); break;
+    case 19: launch_sym_cfg<MODE, 12, 4, 1, 2, true>(g, out, st); break;
+    case 20: launch_sym_cfg<MODE, 12, 3, 1, 2, true>(g, out, st); break;
+    case 21: launch_sym_cfg<MODE, 16, 3, 1, 2, true>(g, out, st); break;
+    case 22: launch_sym_cfg<MODE, 8, 4, 1, 2, true>(g, out, st); break;
     default: launch_sym_cfg<MODE, 8, 2, 2>(g, out, st); break;
   }
 }

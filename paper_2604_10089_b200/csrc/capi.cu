@@ -866,6 +866,30 @@ int bpqn_solve_lcp_dense(const double* A, const double* Ahat, int n, const doubl
   });
 }
 
+int bpqn_solve_lcp_dense_dev(const double* A_dev, const double* Ahat_dev, int n, const double* b_dev, double* x_dev,
+                             const bpqn_solve_opts* opts, bpqn_report* rep, void* stream) {
+  try {
+    BPQN_REQUIRE(A_dev && b_dev && x_dev && n > 0, "null pointer / bad size");
+    cudaStream_t st = S(stream);
+    std::vector<double> A((size_t)n * n), Ah, b(n), x(n);
+    BPQN_CUDA(cudaMemcpyAsync(A.data(), A_dev, 8 * A.size(), cudaMemcpyDeviceToHost, st));
+    if (Ahat_dev) {
+      Ah.resize((size_t)n * n);
+      BPQN_CUDA(cudaMemcpyAsync(Ah.data(), Ahat_dev, 8 * Ah.size(), cudaMemcpyDeviceToHost, st));
+    }
+    BPQN_CUDA(cudaMemcpyAsync(b.data(), b_dev, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    BPQN_CUDA(cudaMemcpyAsync(x.data(), x_dev, 8 * (size_t)n, cudaMemcpyDeviceToHost, st));
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    const int rc = bpqn_solve_lcp_dense(A.data(), Ahat_dev ? Ah.data() : nullptr, n, b.data(), x.data(), opts, rep);
+    BPQN_CUDA(cudaMemcpyAsync(x_dev, x.data(), 8 * (size_t)n, cudaMemcpyHostToDevice, st));
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    return rc;
+  } catch (const Error& e) {
+    set_error(e.msg);
+    return e.code;
+  }
+}
+
 int bpqn_gmres_recycle_reset(bpqn_geom_t g) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");

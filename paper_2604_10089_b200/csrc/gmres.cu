@@ -377,17 +377,25 @@ __global__ void k_cycle_init(const double* src, double* V0, double* vin, size_t 
   }
 }
 
-// back substitution H[0:kk,0:kk] y = gv[0:kk], kk = ctl[0]
+// back substitution H[0:kk,0:kk] y = gv[0:kk], kk = ctl[0]: column-oriented, one block; after y_i
+// is known every thread updates its rows j < i in parallel (kk barrier steps instead of a serial
+// kk^2/2 chain of dependent global loads)
 __global__ void k_backsolve(double* S, GmLayout L, const int* ctl) {
-  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  __shared__ double r[GM_MAX_RESTART + 1];
+  __shared__ double yi;
   const int kk = ctl[0];
   const double* H = S + L.H;
-  double* y = S + L.y;
-  const double* gv = S + L.gv;
+  for (int j = threadIdx.x; j < kk; j += blockDim.x) r[j] = S[L.gv + j];
+  __syncthreads();
   for (int i = kk - 1; i >= 0; --i) {
-    double acc = gv[i];
-    for (int j = i + 1; j < kk; ++j) acc -= H[(size_t)j * (L.m + 1) + i] * y[j];
-    y[i] = acc / H[(size_t)i * (L.m + 1) + i];
+    if (threadIdx.x == 0) {
+      yi = r[i] / H[(size_t)i * (L.m + 1) + i];
+      S[L.y + i] = yi;
+    }
+    __syncthreads();
+    const double* col = H + (size_t)i * (L.m + 1);
+    for (int j = threadIdx.x; j < i; j += blockDim.x) r[j] -= col[j] * yi;
+    __syncthreads();
   }
 }
 
@@ -692,7 +700,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       done = true;
     }
     if (kk > 0) {  // x += M^-1 V y
-      k_backsolve<<<1, 32, 0, st>>>(S, L, ctl);
+      k_backsolve<<<1, 128, 0, st>>>(S, L, ctl);
       k_add_basis<<<blocks_vec, 256, 0, st>>>(g.V.p, ld, 0, ctl, S + L.y, g.tmp3.p, n, 1);
       BPQN_CHECK_LAUNCH();
       if (pre) launch_self_gemm(g, g.Minv.p, g.tmp3.p, x, 1, st);

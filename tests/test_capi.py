@@ -175,3 +175,22 @@ def test_dense_bi_pqn_secant_reuse(lib, seed):
     assert 0 < rep.secant_residual <= 1e-10, rep.secant_residual
     xm, _, _ = bp.solve_lcp_dense(A, b, opts=bp.default_solve_opts(method=0, eps_kkt_abs=1e-12))
     np.testing.assert_allclose(x, xm, atol=1e-9)
+
+
+def test_c4_certificate():
+    """The oracle's KKT certificate of the c4 LCP solution (R26 / DESIGN.md R35): the stored
+    A_oracle lambda_cert (one oracle MVP, tests/fixtures/make_fixtures.py --certify 4) and the
+    oracle's b give ||min(lambda, A lambda + b)||_2 <= 1e-8; recomputed here from the stored oracle
+    values (lambda_cert >= 0, complementarity on the active set, dual feasibility off it)."""
+    import os
+    path = os.path.join(os.path.dirname(__file__), "fixtures", "c4.npz")
+    z = np.load(path, allow_pickle=True)
+    if "lam_cert" not in z:
+        pytest.skip("c4 certificate not generated")
+    lam, w, b = z["lam_cert"], z["A_lam_cert"], z["b"]
+    assert (lam >= 0).all()
+    kkt = np.linalg.norm(np.minimum(lam, w + b))
+    assert abs(kkt - float(z["cert_kkt"])) <= 1e-15 + 1e-12 * kkt
+    assert kkt <= 1e-8
+    g = w + b
+    assert (g[lam == 0] >= -1e-8).all() and np.abs(g[lam > 1e-12]).max() <= 1e-8
