@@ -155,8 +155,36 @@ class Disc:
             out += np.einsum("iajb,njb->nia", D, q.reshape(self.np, self.nq, 3)).reshape(-1, 3)
         return out
 
-    def near_T_all(self):
+    def near_T_all(self, workers=1):
+        """All incidences' near tensors [n_inc, 2, 3, 3, nb].  workers > 1 computes the same
+        per-incidence tensors (near_T) in forked worker processes writing disjoint slices of one
+        shared array -- a wall-time convenience for the large fixtures, no change of arithmetic."""
         if not hasattr(self, "_Tall"):
-            self._Tall = np.stack([self.near_T(k) for k in range(len(self.inc))]) if self.inc else None
+            if not self.inc:
+                self._Tall = None
+            elif workers <= 1:
+                self._Tall = np.stack([self.near_T(k) for k in range(len(self.inc))])
+            else:
+                import multiprocessing as mp
+                shape = (len(self.inc),) + self.near_T(0).shape
+                buf = mp.RawArray("d", int(np.prod(shape)))
+                out = np.frombuffer(buf, dtype=np.float64).reshape(shape)
+                bounds = np.linspace(0, shape[0], workers + 1).astype(int)
+
+                def work(k0, k1):
+                    dst = np.frombuffer(buf, dtype=np.float64).reshape(shape)
+                    for k in range(k0, k1):
+                        i, m = self.inc[k]
+                        dst[k] = near_tensor(self.X[i], self.centers[m], self.a, self.mu, self.p, self.rule)
+
+                ctx = mp.get_context("fork")
+                procs = [ctx.Process(target=work, args=(bounds[w], bounds[w + 1])) for w in range(workers)]
+                for pr in procs:
+                    pr.start()
+                for pr in procs:
+                    pr.join()
+                    if pr.exitcode != 0:
+                        raise RuntimeError("near tensor worker failed")
+                self._Tall = out
             self._T = {}
         return self._Tall

@@ -152,7 +152,7 @@ def run_certify(c, lam_path):
     cfg = make_config(c)
     t = time.time()
     d = Disc(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"])
-    d.near_T_all()
+    d.near_T_all(workers=os.cpu_count() or 1)
     d.self_full()
     t_pre = time.time() - t
     log("c%d oracle operator data built %.1fs; waiting for %s" % (c, t_pre, lam_path))
