@@ -46,12 +46,12 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--gmres-tol", type=float, default=1e-8)   # paper's hi-fidelity eps_gmres (R9)
-    ap.add_argument("--gmres-tol-lo", type=float, default=1e-8)  # low fidelity: 1e-8 online, <= 1e-6 offline
+    ap.add_argument("--gmres-tol-lo", type=float, default=1e-6)  # low fidelity of a standalone LCP: <= 1e-6 (offline, R36); online runs 1e-8
     ap.add_argument("--gmres-restart", type=int, default=100)
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--recycle", type=int, default=1)   # GMRES recycling inside the LCP solve (NEXT-3)
-    ap.add_argument("--solvers", default="bi")          # comma list of bi, mono, bb (BB-PGD)
+    ap.add_argument("--solvers", default="bi,mono")     # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--replicas", action="store_true")  # N > 1: independent replicas instead of the sharded MVP
     ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
