@@ -255,6 +255,103 @@ static bool lu_solve_par(std::vector<double>& A, int n, Vec& b) {
   return true;
 }
 
+// Blocked right-looking LU with partial pivoting (panel width 32) and one right-hand side: the
+// panel is factored by one thread, the U12 block row and the trailing update A22 -= L21 U12 run
+// in an OpenMP team with the column loop vectorised (the rank-1-per-column version spent 1.19 s
+// of a c4 Bi-PQN solve in 564 factorisations of mean order 371).
+static bool lu_solve_blocked(std::vector<double>& A, int n, Vec& b) {
+  constexpr int NB = 32;
+  if (n <= 2 * NB) return lu_solve_par(A, n, b);
+  std::vector<int> piv(n);
+  bool ok = true;
+  for (int k0 = 0; k0 < n && ok; k0 += NB) {
+    const int kb = std::min(NB, n - k0), k1 = k0 + kb;
+    for (int k = k0; k < k1; ++k) {  // panel (rows k..n-1, columns k..k1-1)
+      int pm = k;
+      for (int i = k + 1; i < n; ++i)
+        if (std::fabs(A[(size_t)i * n + k]) > std::fabs(A[(size_t)pm * n + k])) pm = i;
+      piv[k] = pm;
+      if (A[(size_t)pm * n + k] == 0.0) {
+        ok = false;
+        break;
+      }
+      if (pm != k)
+        for (int j = 0; j < n; ++j) std::swap(A[(size_t)k * n + j], A[(size_t)pm * n + j]);
+      const double inv = 1.0 / A[(size_t)k * n + k];
+      const double* rk = &A[(size_t)k * n];
+      for (int i = k + 1; i < n; ++i) {
+        double* ri = &A[(size_t)i * n];
+        const double f = (ri[k] *= inv);
+        if (f != 0.0)
+          for (int j = k + 1; j < k1; ++j) ri[j] -= f * rk[j];
+      }
+    }
+    if (!ok || k1 >= n) break;
+    // U12 = L11^-1 A12 (unit lower) and A22 -= L21 U12
+#pragma omp parallel
+    {
+#pragma omp for schedule(static)
+      for (int jb = k1; jb < n; jb += 64) {
+        const int je = std::min(n, jb + 64);
+        for (int k = k0; k < k1; ++k)
+          for (int i = k + 1; i < k1; ++i) {
+            const double f = A[(size_t)i * n + k];
+            double* ri = &A[(size_t)i * n];
+            const double* rk = &A[(size_t)k * n];
+#pragma omp simd
+            for (int j = jb; j < je; ++j) ri[j] -= f * rk[j];
+          }
+      }
+      // trailing update, four rows at a time (each U12 row is loaded once per four updated rows)
+#pragma omp for schedule(static)
+      for (int i0 = k1; i0 < n; i0 += 4) {
+        const int ni = std::min(4, n - i0);
+        double* r0 = &A[(size_t)i0 * n];
+        double* r1 = ni > 1 ? r0 + n : r0;
+        double* r2 = ni > 2 ? r0 + 2 * (size_t)n : r0;
+        double* r3 = ni > 3 ? r0 + 3 * (size_t)n : r0;
+        for (int k = k0; k < k1; ++k) {
+          const double f0 = r0[k], f1 = ni > 1 ? r1[k] : 0.0, f2 = ni > 2 ? r2[k] : 0.0, f3 = ni > 3 ? r3[k] : 0.0;
+          const double* rk = &A[(size_t)k * n];
+          if (ni == 4) {
+#pragma omp simd
+            for (int j = k1; j < n; ++j) {
+              const double u = rk[j];
+              r0[j] -= f0 * u;
+              r1[j] -= f1 * u;
+              r2[j] -= f2 * u;
+              r3[j] -= f3 * u;
+            }
+          } else {
+            for (int q = 0; q < ni; ++q) {
+              double* rq = r0 + (size_t)q * n;
+              const double f = rq[k];
+#pragma omp simd
+              for (int j = k1; j < n; ++j) rq[j] -= f * rk[j];
+            }
+          }
+        }
+      }
+    }
+  }
+  if (!ok) return false;
+  for (int k = 0; k < n; ++k)
+    if (piv[k] != k) std::swap(b[k], b[piv[k]]);
+  for (int i = 1; i < n; ++i) {  // unit lower
+    double s = b[i];
+    const double* ri = &A[(size_t)i * n];
+    for (int j = 0; j < i; ++j) s -= ri[j] * b[j];
+    b[i] = s;
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double s = b[i];
+    const double* ri = &A[(size_t)i * n];
+    for (int j = i + 1; j < n; ++j) s -= ri[j] * b[j];
+    b[i] = s / ri[i];
+  }
+  return true;
+}
+
 // ------------------------------------------------------------------ weighted prox
 // prox^B_{x>=0}(x~), B = I + UU^T - VV^T (D = I in both solvers, R19), by the dual
 // root of Prop. 1 with Alg. 4's semi-smooth Newton on the
@@ -502,7 +599,7 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
       g_pt.jac += t_2 - t_1;
       Vec step = L;
       std::vector<double> Jc = J;
-      const bool lu_ok = lu_solve_par(Jc, d, step);
+      const bool lu_ok = lu_solve_blocked(Jc, d, step);
       g_pt.lu += now_s() - t_2;
       t_2 = now_s();
       if (!lu_ok) {
@@ -510,7 +607,7 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
         for (double v : J) jn = std::max(jn, std::fabs(v));
         for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1e-10 * jn * d;
         step = L;
-        if (!lu_solve_par(J, d, step)) break;
+        if (!lu_solve_blocked(J, d, step)) break;
       }
       double t = 1.0;
       bool ok = false;
