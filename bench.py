@@ -57,6 +57,7 @@ def parse():
     ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
     ap.add_argument("--shard-asym", action="store_true")  # sharded K1 as the one-directional kernel (no reduce-scatter)
     ap.add_argument("--sub-forcing", type=float, default=0.0)   # Bi-PQN inexact subproblems (off = R22)
+    ap.add_argument("--lo-dense", type=int, default=1)  # Bi-PQN: form the low-fidelity A^ once (R38); 0 = matrix-free
     ap.add_argument("--c5-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-targets", type=int, default=0)
     return ap.parse_args()
@@ -449,7 +450,8 @@ def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
     torch.cuda.synchronize()
     ms_b = e0.elapsed_time(e1)
     o = bp.default_solve_opts(method=1 if lo is not None else (2 if meth == "bb" else 0), eps_kkt_abs=1e-8,
-                              eps_kkt_rel=1e-8, k_max=500, sub_forcing=args.sub_forcing)
+                              eps_kkt_rel=1e-8, k_max=500, sub_forcing=args.sub_forcing,
+                              lo_dense=int(args.lo_dense) if meth == "bi" else 0)
     o.gm_hi = gmo
     o.gm_lo = bp.default_gmres_opts(tol=args.gmres_tol_lo, restart=args.gmres_restart, recycle=int(args.recycle))
     lam = torch.zeros(g.nc, dtype=torch.float64, device=dev)
@@ -466,7 +468,8 @@ def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
            "rc": rc, "lo_geometry_init_s": round(t_lo_init, 3),
            "negative_b_fraction": float((b < 0).double().mean().item()),
            "active_contacts": int((lam > 0).sum().item())}
-    out.update({k: r[k] for k in ("iterations", "hi_mvps", "lo_mvps", "lo_mvps_init", "e_mvps", "cost_ratio", "kkt_abs",
+    out.update({k: r[k] for k in ("iterations", "hi_mvps", "lo_mvps", "lo_mvps_init", "lo_dense_columns",
+                                  "lo_dense_gmres_iters", "ms_lo_dense", "e_mvps", "cost_ratio", "kkt_abs",
                                   "gmres_iters_hi", "gmres_iters_lo", "ms_hi", "ms_lo", "termination")})
     if lo is not None:
         lo.close()
@@ -506,7 +509,8 @@ def run_paper_setting(args, dev, stream):
     b, _ = bp.lcp_b(hi, torch.tensor(cfg["F_nc"], device=dev), slip=slip, gmres=gmo)
     solves = {}
     for meth, code in (("Bi-PQN", 1), ("Mono-PQN", 0), ("BB-PGD", 2)):
-        o = bp.default_solve_opts(method=code, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500)
+        o = bp.default_solve_opts(method=code, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500,
+                                  lo_dense=int(args.lo_dense) if code == 1 else 0)
         o.gm_hi = gmo
         o.gm_lo = gmo
         t0 = time.perf_counter()
@@ -515,11 +519,11 @@ def run_paper_setting(args, dev, stream):
         torch.cuda.synchronize()
         solves[meth] = {"ms": (time.perf_counter() - t0) * 1e3, "rc": rc, "iterations": rep.iterations,
                         "hi_mvps": rep.hi_mvps, "lo_mvps": rep.lo_mvps, "e_mvps": rep.e_mvps,
-                        "kkt_abs": rep.kkt_abs}
+                        "kkt_abs": rep.kkt_abs, "ms_lo_dense": rep.ms_lo_dense}
     # one full DVI step (contacts, U_nc with slip, b, Bi-PQN, M D lambda, Euler, geometry update)
     C = np.ascontiguousarray(cfg["centers"].copy())
     A = np.ascontiguousarray(cfg["axes"].copy())
-    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=int(args.lo_dense))
     o.gm_hi = gmo
     o.gm_lo = gmo
     steps = []

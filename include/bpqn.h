@@ -107,6 +107,12 @@ typedef struct {
                                  max_j |B^(k) s_j - y_j|_inf / max(1, |y_j|_inf) over the re-used
                                  secant pairs (reading R34) with extra, uncounted lo MVPs;
                                  reported in bpqn_report.secant_residual */
+  int lo_dense;               /* Bi-PQN: 1 = form the low-fidelity LCP matrix A^ = D^T M_lo D once per solve
+                                 (all Nc mobility solves as one batched GMRES on the dense completed
+                                 double-layer operator of `lo`, FP64 GEMMs on the tensor cores; gm_lo's
+                                 tolerance per column; R38) and apply it as an Nc x Nc product for
+                                 every low-fidelity MVP; falls back to matrix-free lo MVPs if the dense
+                                 operator (8 (3 N_lo)^2 bytes) does not fit.  0 (default): matrix-free */
 } bpqn_solve_opts;
 
 typedef struct {
@@ -115,6 +121,9 @@ typedef struct {
   int termination;            /* 0 KKT_ABS, 1 KKT_REL, 2 MAX_ITER, 3 STALLED */
   double secant_residual;     /* see bpqn_solve_opts.verify_secants (0 otherwise) */
   int lo_mvps_init;           /* Bi-PQN: lo MVPs of the low-fidelity initialisation (Alg. 3 line 1) */
+  int lo_dense_columns;       /* lo_dense: columns formed (= Nc; 0 when matrix-free) */
+  int lo_dense_gmres_iters;   /* lo_dense: iterations of the batched GMRES */
+  double ms_lo_dense;         /* lo_dense: wall time of forming A^ (included in ms_lo and ms_total) */
 } bpqn_report;
 
 /* Defaults for the option structs above. */
@@ -181,6 +190,15 @@ int bpqn_lcp_b(bpqn_geom_t g, const double* fnc_dev, const double* slip_dev, dou
  * (>= 0), out = solution.  rep may be NULL. */
 int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* lambda_dev,
                    const bpqn_solve_opts* o, bpqn_report* rep, void* stream);
+
+/* The whole LCP matrix A = D^T M D of the handle's contact set, row-major [Nc][Nc] into A_host:
+ * all Nc mobility solves as one batched right-preconditioned GMRES on the dense completed double-layer
+ * operator (8 (3N)^2 bytes of device memory, FP64 GEMMs; gm's tolerance per column).  This is how
+ * bpqn_solve_opts.lo_dense forms the low-fidelity A^ (R38); the paper analyses dense A / A^ offline
+ * (Fig. 3).  BPQN_ERR_OOM if the dense operator does not fit; N <= 65535 nodes.  st: iters =
+ * batched GMRES iterations, ms = wall time.  Synchronises the stream. */
+int bpqn_lcp_matrix_dense(bpqn_geom_t g, const bpqn_gmres_opts* gm, double* A_host, bpqn_gmres_stats* st,
+                          void* stream);
 
 /* Report of one DVI time step (bpqn_dvi_step). */
 typedef struct {

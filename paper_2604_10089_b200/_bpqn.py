@@ -35,7 +35,7 @@ class SolveOpts(ctypes.Structure):
                 ("tau", c_double), ("refresh_period", c_int), ("sub_eps_factor", c_double),
                 ("sub_k_max", c_int), ("prox_tol", c_double), ("prox_jmax", c_int), ("curv_skip", c_double),
                 ("gm_hi", GmresOpts), ("gm_lo", GmresOpts), ("cost_ratio", c_double), ("sub_forcing", c_double),
-                ("verify_secants", c_int)]
+                ("verify_secants", c_int), ("lo_dense", c_int)]
 
 
 class Report(ctypes.Structure):
@@ -43,7 +43,8 @@ class Report(ctypes.Structure):
                 ("gmres_iters_lo", c_int), ("e_mvps", c_double), ("cost_ratio", c_double),
                 ("kkt_abs", c_double), ("kkt_rel", c_double), ("objective", c_double),
                 ("ms_total", c_double), ("ms_hi", c_double), ("ms_lo", c_double), ("termination", c_int),
-                ("secant_residual", c_double), ("lo_mvps_init", c_int)]
+                ("secant_residual", c_double), ("lo_mvps_init", c_int), ("lo_dense_columns", c_int),
+                ("lo_dense_gmres_iters", c_int), ("ms_lo_dense", c_double)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -80,6 +81,7 @@ SYMBOLS = {
     "bpqn_geometry_shard": (c_int, [c_void_p, c_int, c_int, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_geometry_shard_symmetric": (c_int, [c_void_p, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_nccl_unique_id": (c_int, [c_void_p]),
+    "bpqn_lcp_matrix_dense": (c_int, [c_void_p, P(GmresOpts), c_void_p, P(GmresStats), c_void_p]),
     "bpqn_diag_rsqrt_seed": (c_int, [c_int, c_int, P(c_double)]),
     "bpqn_geometry_shard_nccl": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
     "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
@@ -425,6 +427,16 @@ def diag_rsqrt_seed(exp_lo, exp_hi):
     v = c_double()
     _check(lib().bpqn_diag_rsqrt_seed(exp_lo, exp_hi, ctypes.byref(v)))
     return v.value
+
+
+def lcp_matrix_dense(g, gmres=None, stream=None):
+    """A = D^T M D of the handle's contact set as a numpy [Nc, Nc] array (bpqn_lcp_matrix_dense)."""
+    import numpy as np
+    A = np.zeros((g.nc, g.nc))
+    st = GmresStats()
+    _check(lib().bpqn_lcp_matrix_dense(g.h, ctypes.byref(gmres) if gmres is not None else None,
+                                       A.ctypes.data_as(c_void_p), ctypes.byref(st), _stream(stream)))
+    return A, st
 
 
 def nccl_unique_id():

@@ -241,6 +241,18 @@ int gmres_solve(Geom& g, const double* rhs, double* x, const bpqn_gmres_opts& o,
 void gmres_reserve(Geom& g, int restart);   // basis and scratch for a restart length (init: default 100)
 void gmres_recycle_reserve(Geom& g);        // recycling store (outside the hot calls; may stay off)
 
+// Low-fidelity LCP matrix densified in HBM (dense_lo.cu, reading R38)
+constexpr int GM_BATCH_MAX_M = 128;
+struct DenseLoStats {
+  int columns = 0, iters = 0, restart = 0;
+  double ms_rhs = 0, ms_total = 0;
+  size_t bytes = 0;
+};
+size_t dense_lo_bytes(const Geom& g, int restart);
+// A^ = D^T M D of the handle's contact set (row-major Nc x Nc, host) by one batched GMRES over all
+// Nc unit vectors with a dense operator; throws BPQN_ERR_OOM if it does not fit
+int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, DenseLoStats& st, cudaStream_t s);
+
 // NCCL (comm.cu)
 void comm_unique_id(void* out128);
 void comm_init(Geom& g, int rank, int world, const void* uid128);

@@ -243,6 +243,7 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o) {
   o->cost_ratio = 0.0;
   o->sub_forcing = 0.0;
   o->verify_secants = 0;
+  o->lo_dense = 0;
 }
 
 int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius, double mu,
@@ -628,8 +629,34 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     int iters = 0, term = 2, hi_mvps = 0, lo_mvps = 0;
     double kkt = 0, kkt_rel = 0, secant_res = 0;
     int lo_init = 0;
+    DenseLoStats dls;
+    std::vector<double> Ahat;
+    bool dense_lo = false;
+    if (bi && o.lo_dense) {
+      try {
+        densify_lcp(*lo, glo, Ahat, dls, s);
+        dense_lo = true;
+        ms_lo += dls.ms_total;
+      } catch (const Error& e) {
+        if (e.code != BPQN_ERR_OOM) throw;
+        cudaGetLastError();  // does not fit: matrix-free low fidelity
+      }
+    }
     if (bi) {
       MvpFn flo = make(lo, glo, ms_lo, it_lo, n_lo);
+      if (dense_lo)  // every low-fidelity MVP is the Nc x Nc product with the formed A^
+        flo = [&](const std::vector<double>& v, std::vector<double>& out, std::vector<double>*) {
+          auto ta = std::chrono::steady_clock::now();
+          out.assign(nc, 0.0);
+          for (int i = 0; i < nc; ++i) {
+            double acc = 0.0;
+            const double* row = Ahat.data() + (size_t)i * nc;
+            for (int j = 0; j < nc; ++j) acc += row[j] * v[j];
+            out[i] = acc;
+          }
+          n_lo++;
+          ms_lo += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - ta).count();
+        };
       BiResult r = bi_pqn(fhi, flo, b, x0, q);
       prox_profile_flush();
       x = r.x;
@@ -673,6 +700,14 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       rep->termination = term;
       rep->secant_residual = secant_res;
       rep->lo_mvps_init = lo_init;
+      rep->lo_dense_columns = dense_lo ? dls.columns : 0;
+      rep->lo_dense_gmres_iters = dense_lo ? dls.iters : 0;
+      rep->ms_lo_dense = dense_lo ? dls.ms_total : 0.0;
+      if (dense_lo) {  // E-MVPs from measured time: the forming of A^ dominates the low-fidelity cost
+        const double t_hi = n_hi ? ms_hi / n_hi : 0;
+        rep->cost_ratio = o.cost_ratio > 0 ? o.cost_ratio : (t_hi > 0 && n_lo ? (ms_lo / n_lo) / t_hi : 0);
+        rep->e_mvps = hi_mvps + (t_hi > 0 ? ms_lo / t_hi : 0);
+      }
     }
     if (gm_fail) {
       set_error("an inner GMRES solve did not converge");
@@ -888,6 +923,26 @@ int bpqn_solve_lcp_dense_dev(const double* A_dev, const double* Ahat_dev, int n,
     set_error(e.msg);
     return e.code;
   }
+}
+
+int bpqn_lcp_matrix_dense(bpqn_geom_t g, const bpqn_gmres_opts* gm, double* A_host, bpqn_gmres_stats* st,
+                          void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && A_host, "null pointer");
+    BPQN_REQUIRE(g->nc > 0, "no contacts installed");
+    DenseLoStats d;
+    std::vector<double> A;
+    densify_lcp(*g, gm_or_default(gm), A, d, S(stream));
+    std::copy(A.begin(), A.end(), A_host);
+    if (st) {
+      st->iters = d.iters;
+      st->restarts = 0;
+      st->rel_resid = 0.0;
+      st->ms = d.ms_total;
+      st->applies = d.iters;
+    }
+    return BPQN_OK;
+  });
 }
 
 int bpqn_gmres_recycle_reset(bpqn_geom_t g) {

@@ -1,0 +1,402 @@
+// The low-fidelity LCP matrix densified in HBM (reading R38).
+//
+// Bi-PQN (Alg. 3) applies the low-fidelity operator A^ = D^T M_lo D hundreds of times
+// (c4: ~390 lo MVPs, each a GMRES solve of ~32 iterations at p_lo = 8).  A^ is a fixed Nc x Nc matrix
+// for the whole LCP solve, so it can instead be formed once, column by column, with all Nc mobility
+// solves running as ONE batched GMRES whose operator application is a dense FP64 GEMM on the tensor
+// cores:
+//   * the completed double-layer operator A_op = -I/2 + D_full + Pi_R of the handle (K1's coarse
+//     stresslet pairs, the refined near rows of K2, the self blocks E_A of K3 -- the same discrete
+//     operator, O6/O7) is assembled once as a dense row-major [3N][3N] matrix (c4 at
+//     p_lo = 8: 93 312^2 doubles = 69.7 GB of the 180 GB HBM);
+//   * right hand sides b_l = -S_full[P^T D e_l] (one single-layer apply per contact);
+//   * Nc independent right-preconditioned GMRES(m) processes advance together: per iteration one
+//     block-Jacobi GEMM (Minv on every sphere of every column) and one [3N x 3N] x [3N x Nc] GEMM
+//     (cuBLAS DGEMM, 35 TFLOP/s measured), then one CTA per column runs its CGS2, Givens rotations
+//     and residual; each column stops at its own relative residual tolerance;
+//   * A^ e_l = D^T (-Pi[q_l]) (the rigid read-out and D^T gather of every MVP).
+// Every later low-fidelity MVP of the solve is the 540 x 540 product A^ v on the host.  cuBLAS is
+// resolved at run time (dlopen; the copy torch loaded when there is one).
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "bpqn_internal.h"
+
+namespace bpqn {
+
+// ---------------------------------------------------------------- cuBLAS (run-time bound)
+typedef int (*cublasCreate_t)(void**);
+typedef int (*cublasSetStream_t)(void*, cudaStream_t);
+typedef int (*cublasDgemm_t)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int,
+                             const double*, double*, int);
+struct Cublas {
+  cublasCreate_t create = nullptr;
+  cublasSetStream_t setStream = nullptr;
+  cublasDgemm_t dgemm = nullptr;
+  void* handle = nullptr;
+  std::string why;
+};
+static Cublas& cublas() {
+  static Cublas c;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libcublas.so.12", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libcublas.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) {
+      c.why = "cuBLAS not found";
+      return;
+    }
+    c.create = reinterpret_cast<cublasCreate_t>(dlsym(h, "cublasCreate_v2"));
+    c.setStream = reinterpret_cast<cublasSetStream_t>(dlsym(h, "cublasSetStream_v2"));
+    c.dgemm = reinterpret_cast<cublasDgemm_t>(dlsym(h, "cublasDgemm_v2"));
+    if (!c.create || !c.setStream || !c.dgemm || c.create(&c.handle) != 0) c.why = "cuBLAS initialisation failed";
+  });
+  if (!c.why.empty()) throw Error{BPQN_ERR_CUDA, c.why};
+  return c;
+}
+constexpr int CUBLAS_OP_N_ = 0, CUBLAS_OP_T_ = 1;
+
+// C[m x n] (col-major, ldc) = op(A) B with A given row-major [m][k] (i.e. col-major A^T, lda = k)
+static void gemm_rowA(cudaStream_t st, int m, int n, int k, const double* A_row, const double* B, int ldb, double* C,
+                      int ldc, double beta = 0.0) {
+  Cublas& cb = cublas();
+  const double one = 1.0;
+  if (cb.setStream(cb.handle, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
+  if (cb.dgemm(cb.handle, CUBLAS_OP_T_, CUBLAS_OP_N_, m, n, k, &one, A_row, k, B, ldb, &beta, C, ldc) != 0)
+    throw Error{BPQN_ERR_CUDA, "cublasDgemm failed"};
+}
+
+// ---------------------------------------------------------------- dense operator assembly
+// coarse stresslet for every node pair (i, j), i != j:  A[3i+a][3j+b] = -3/(4 pi) w_j (r.n_j) r_a r_b / rho^5
+__global__ void k_dense_coarse(int N, const double* __restrict__ src, double* __restrict__ A) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= N) return;
+  const double* yi = src + 8 * (size_t)i;
+  const double* yj = src + 8 * (size_t)j;
+  const double r0 = yi[0] - yj[0], r1 = yi[1] - yj[1], r2 = yi[2] - yj[2];
+  const double rr = r0 * r0 + r1 * r1 + r2 * r2;
+  double t = 0.0;
+  if (i != j) {
+    const double rn = r0 * yj[4] + r1 * yj[5] + r2 * yj[6];
+    const double ir = 1.0 / sqrt(rr);
+    const double ir2 = ir * ir;
+    t = -3.0 / (4.0 * 3.14159265358979323846) * yj[3] * rn * ir2 * ir2 * ir;
+  }
+  const size_t L = 3 * (size_t)N;
+  double* row = A + (3 * (size_t)i) * L + 3 * (size_t)j;
+  const double r[3] = {r0, r1, r2};
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) row[a * L + b] = t * r[a] * r[b];
+}
+
+// near incidences (K2 order pos -> target i, sphere m): the refined rule REPLACES the coarse block:
+// A[3i+a][3(m Nq + j)+c] = sum_b T[pos][sym(a,c)][b] analysis[b][j]
+__global__ void k_dense_near(int N, int nq, int nb, int nbp, const int* __restrict__ cm_t, const int* __restrict__ cm_m,
+                             const double* __restrict__ T, const double* __restrict__ analysis, double* A) {
+  const int pos = blockIdx.x;
+  const int i = cm_t[pos], m = cm_m[pos];
+  extern __shared__ double tr[];  // [6][nb]
+  for (int e = threadIdx.x; e < 6 * nb; e += blockDim.x) tr[e] = T[((size_t)pos * 6 + e / nb) * nbp + e % nb];
+  __syncthreads();
+  const size_t L = 3 * (size_t)N;
+  const int sym[3][3] = {{0, 1, 2}, {1, 3, 4}, {2, 4, 5}};
+  for (int j = threadIdx.x; j < nq; j += blockDim.x) {
+    double s[6] = {0, 0, 0, 0, 0, 0};
+    for (int b = 0; b < nb; ++b) {
+      const double an = analysis[(size_t)b * nq + j];
+#pragma unroll
+      for (int q = 0; q < 6; ++q) s[q] = fma(tr[q * nb + b], an, s[q]);
+    }
+    double* blk = A + (3 * (size_t)i) * L + 3 * ((size_t)m * nq + j);
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) blk[a * L + c] = s[sym[a][c]];
+  }
+}
+
+// same-sphere blocks: A[3i+a][3(n Nq + j)+c] += E_A[3 il + a][3 j + c]  (E_A = self - naive same-sphere
+// stresslet - I/2 + Pi_R, so coarse + E_A = D_self - I/2 + Pi_R)
+__global__ void k_dense_self(int N, int nq, const double* __restrict__ EA, double* A) {
+  const int i = blockIdx.x;
+  const int n = i / nq, il = i - n * nq;
+  const size_t L = 3 * (size_t)N;
+  const int M = 3 * nq;
+  for (int e = threadIdx.x; e < 3 * M; e += blockDim.x) {
+    const int a = e / M, col = e - a * M;
+    A[(3 * (size_t)i + a) * L + 3 * (size_t)n * nq + col] += EA[(size_t)(3 * il + a) * M + col];
+  }
+}
+
+// ---------------------------------------------------------------- batched GMRES, one CTA per column
+struct BgmParams {
+  double* V;        // [(m+1)][R][n]
+  const double* W;  // [R][n] operator output A M^-1 v_k
+  int n, R, m, k;
+  double* H;        // [R][(m+1) m]
+  double *cs, *sn, *gv;  // [R][m], [R][m], [R][m+1]
+  const double* beta;    // [R] |r0|
+  double* resid;         // [R]
+};
+
+__device__ __forceinline__ double block_sum(double v, double* sred) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sred[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(512) k_bgm_step(BgmParams P) {
+  __shared__ double sred[16];
+  __shared__ double h[2][GM_BATCH_MAX_M + 1];
+  const int col = blockIdx.x, k = P.k, n = P.n;
+  double* w = P.V + ((size_t)(k + 1) * P.R + col) * n;  // z lands in V_{k+1}
+  const double* z = P.W + (size_t)col * n;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) w[e] = z[e];
+  for (int pass = 0; pass < 2; ++pass) {  // CGS2
+    for (int i = 0; i <= k; ++i) {
+      const double* v = P.V + ((size_t)i * P.R + col) * n;
+      double s = 0.0;
+      for (int e = threadIdx.x; e < n; e += blockDim.x) s = fma(v[e], w[e], s);
+      s = block_sum(s, sred);
+      if (threadIdx.x == 0) h[pass][i] = s;
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < n; e += blockDim.x) {
+      double acc = w[e];
+      for (int i = 0; i <= k; ++i) acc = fma(-P.V[((size_t)i * P.R + col) * n + e], h[pass][i], acc);
+      w[e] = acc;
+    }
+    __syncthreads();
+  }
+  double s = 0.0;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) s = fma(w[e], w[e], s);
+  const double nrm = sqrt(block_sum(s, sred));
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) w[e] *= inv;
+  if (threadIdx.x != 0) return;
+  const int m = P.m;
+  double* H = P.H + (size_t)col * (m + 1) * m + (size_t)k * (m + 1);
+  double* cs = P.cs + (size_t)col * m;
+  double* sn = P.sn + (size_t)col * m;
+  double* gv = P.gv + (size_t)col * (m + 1);
+  for (int i = 0; i <= k; ++i) H[i] = h[0][i] + h[1][i];
+  H[k + 1] = nrm;
+  for (int i = 0; i < k; ++i) {
+    const double t = cs[i] * H[i] + sn[i] * H[i + 1];
+    H[i + 1] = -sn[i] * H[i] + cs[i] * H[i + 1];
+    H[i] = t;
+  }
+  const double den = hypot(H[k], H[k + 1]);
+  const double c = den > 0 ? H[k] / den : 1.0, sv = den > 0 ? H[k + 1] / den : 0.0;
+  cs[k] = c;
+  sn[k] = sv;
+  H[k] = den;
+  H[k + 1] = 0.0;
+  gv[k + 1] = -sv * gv[k];
+  gv[k] = c * gv[k];
+  P.resid[col] = P.beta[col] > 0.0 ? fabs(gv[k + 1]) / P.beta[col] : 0.0;
+}
+
+// V_0 = r / |r| per column; gv = |r| e_1; beta = |r| (relative to the column's |b|: bnorm)
+__global__ void k_bgm_start(double* V, const double* r, int n, int m, double* gv, double* beta, double* resid,
+                            const double* bnorm) {
+  __shared__ double sred[16];
+  const int col = blockIdx.x;
+  const double* rc = r + (size_t)col * n;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) s = fma(rc[e], rc[e], s);
+  const double nr = sqrt(block_sum(s, sred));
+  const double inv = nr > 0.0 ? 1.0 / nr : 0.0;
+  double* v = V + (size_t)col * n;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) v[e] = rc[e] * inv;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i <= m; ++i) gv[(size_t)col * (m + 1) + i] = 0.0;
+    gv[(size_t)col * (m + 1)] = nr;
+    const double bn = bnorm ? bnorm[col] : nr;
+    beta[col] = bn;  // residuals are relative to |b| (bnorm), as in gmres_solve
+    resid[col] = bn > 0.0 ? nr / bn : 0.0;
+  }
+}
+
+// y = H^-1 gv per column (back substitution, one thread per column); X[:, col] = sum_i y_i V_i
+__global__ void k_bgm_backsolve(const double* H, const double* gv, int m, int kk, int R, double* y) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= R) return;
+  const double* Hc = H + (size_t)col * (m + 1) * m;
+  double* yc = y + (size_t)col * m;
+  for (int i = kk - 1; i >= 0; --i) {
+    double acc = gv[(size_t)col * (m + 1) + i];
+    for (int j = i + 1; j < kk; ++j) acc -= Hc[(size_t)j * (m + 1) + i] * yc[j];
+    yc[i] = Hc[(size_t)i * (m + 1) + i] != 0.0 ? acc / Hc[(size_t)i * (m + 1) + i] : 0.0;
+  }
+}
+
+__global__ void k_bgm_combine(const double* V, const double* y, int n, int R, int m, int kk, double* X) {
+  const int col = blockIdx.y;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int i = 0; i < kk; ++i) acc = fma(V[((size_t)i * R + col) * n + e], y[(size_t)col * m + i], acc);
+    X[(size_t)col * n + e] = acc;
+  }
+}
+
+__global__ void k_sub_cols(double* r, const double* b, const double* ax, size_t tot) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (size_t)gridDim.x * blockDim.x)
+    r[e] = b[e] - ax[e];
+}
+
+__global__ void k_col_norms(const double* b, int n, double* out) {
+  __shared__ double sred[16];
+  const double* bc = b + (size_t)blockIdx.x * n;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) s = fma(bc[e], bc[e], s);
+  s = sqrt(block_sum(s, sred));
+  if (threadIdx.x == 0) out[blockIdx.x] = s;
+}
+
+// ---------------------------------------------------------------- driver
+size_t dense_lo_bytes(const Geom& g, int m) {
+  const size_t n = 3 * (size_t)g.n, R = (size_t)std::max(g.nc, 1);
+  return 8 * (n * n + (size_t)(m + 1) * R * n + 4 * R * n);
+}
+
+int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, DenseLoStats& stt, cudaStream_t st) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const int N = g.n, R = g.nc, nq = g.nq;
+  const size_t n = 3 * (size_t)N;
+  BPQN_REQUIRE(R > 0, "no contacts installed");
+  BPQN_REQUIRE(N <= 65535 && !g.sharded(), "dense low fidelity: N <= 65535 nodes, unsharded handle");
+  BPQN_REQUIRE(g.Minv.p && g.E_A.p, "geometry has no self operators");
+  int m = std::max(4, std::min(o.restart, GM_BATCH_MAX_M));
+  size_t fr = 0, tot = 0;
+  BPQN_CUDA(cudaMemGetInfo(&fr, &tot));
+  while (m > 8 && dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr) m /= 2;
+  if (dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr)
+    throw Error{BPQN_ERR_OOM, "dense low-fidelity operator does not fit in device memory"};
+  cublas();  // fail early if cuBLAS is missing
+  DBuf<double> A, V, B, Wb, X, Z, sm;
+  A.alloc(n * n);
+  V.alloc((size_t)(m + 1) * R * n);
+  B.alloc((size_t)R * n);
+  Wb.alloc((size_t)R * n);
+  X.alloc((size_t)R * n);
+  Z.alloc((size_t)R * n);
+  const size_t hs = (size_t)R * (m + 1) * m, cs = (size_t)R * m, gs = (size_t)R * (m + 1);
+  sm.alloc(hs + 3 * cs + gs + 4 * (size_t)R);
+  double *H = sm.p, *CS = H + hs, *SN = CS + cs, *Y = SN + cs, *GV = Y + cs, *BETA = GV + gs, *RES = BETA + R,
+         *BN = RES + R;
+  // 1. assemble A_op (coarse -> near rows replace -> self blocks add)
+  k_dense_coarse<<<dim3((N + 255) / 256, N), 256, 0, st>>>(N, g.src.p, A.p);
+  BPQN_CHECK_LAUNCH();
+  if (g.n_inc > 0) {
+    const int nbp = (g.nb + 1) & ~1;
+    k_dense_near<<<(unsigned)g.n_inc, 128, 6 * g.nb * sizeof(double), st>>>(N, nq, g.nb, nbp, g.cm_t.p, g.cm_m.p,
+                                                                             g.T_D.p, g.analysis.p, A.p);
+    BPQN_CHECK_LAUNCH();
+  }
+  k_dense_self<<<N, 256, 0, st>>>(N, nq, g.E_A.p, A.p);
+  BPQN_CHECK_LAUNCH();
+  // 2. right-hand sides b_l = -S[P^T D e_l]
+  BPQN_REQUIRE(g.E_S.p, "geometry built without single-layer data");
+  DBuf<double> eye;
+  {
+    std::vector<double> I((size_t)R * R, 0.0);
+    for (int l = 0; l < R; ++l) I[(size_t)l * R + l] = 1.0;
+    eye.alloc(I.size());
+    BPQN_CUDA(cudaMemcpyAsync(eye.p, I.data(), 8 * I.size(), cudaMemcpyHostToDevice, st));
+    BPQN_CUDA(cudaStreamSynchronize(st));
+  }
+  for (int l = 0; l < R; ++l) {
+    launch_d_scatter(g, eye.p + (size_t)l * R, g.ft.p, st);
+    launch_pt(g, g.ft.p, g.tmp.p, st);
+    apply_operator(g, g.tmp.p, nullptr, g.E_S.p, nullptr, B.p + (size_t)l * n, st);
+  }
+  launch_axpby(B.p, 0.0, B.p, -1.0, (size_t)R * n, st);
+  k_col_norms<<<R, 512, 0, st>>>(B.p, (int)n, BN);
+  BPQN_CHECK_LAUNCH();
+  const auto t1 = std::chrono::steady_clock::now();
+  // 3. batched right-preconditioned GMRES(m), x0 = 0
+  BPQN_CUDA(cudaMemsetAsync(X.p, 0, 8 * (size_t)R * n, st));
+  const int M3 = 3 * nq;
+  auto apply_op = [&](const double* in, double* out) {  // out = A_op Minv in (all columns)
+    gemm_rowA(st, M3, g.np * R, M3, g.Minv.p, in, M3, Z.p, M3);
+    gemm_rowA(st, (int)n, R, (int)n, A.p, Z.p, (int)n, out, (int)n);
+  };
+  std::vector<double> res(R);
+  int iters = 0;
+  bool first = true, done = false;
+  while (!done) {
+    const double* r0 = B.p;
+    if (!first) {  // restart: r = b - A x  (x holds the solution so far, already M^-1 applied)
+      gemm_rowA(st, (int)n, R, (int)n, A.p, X.p, (int)n, Wb.p, (int)n);
+      k_sub_cols<<<std::min<int>((int)(((size_t)R * n + 255) / 256), g.sms * 16), 256, 0, st>>>(Wb.p, B.p, Wb.p,
+                                                                                            (size_t)R * n);
+      r0 = Wb.p;
+    }
+    first = false;
+    k_bgm_start<<<R, 512, 0, st>>>(V.p, r0, (int)n, m, GV, BETA, RES, BN);
+    BPQN_CHECK_LAUNCH();
+    int kk = 0;
+    for (int k = 0; k < m; ++k) {
+      apply_op(V.p + (size_t)k * R * n, Wb.p);
+      BgmParams P{V.p, Wb.p, (int)n, R, m, k, H, CS, SN, GV, BETA, RES};
+      k_bgm_step<<<R, 512, 0, st>>>(P);
+      BPQN_CHECK_LAUNCH();
+      kk = k + 1;
+      ++iters;
+      BPQN_CUDA(cudaMemcpyAsync(res.data(), RES, 8 * (size_t)R, cudaMemcpyDeviceToHost, st));
+      BPQN_CUDA(cudaStreamSynchronize(st));
+      const double worst = *std::max_element(res.begin(), res.end());
+      if (!std::isfinite(worst)) throw Error{BPQN_ERR_NAN, "NaN in the batched low-fidelity GMRES"};
+      if (worst <= o.tol) {
+        done = true;
+        break;
+      }
+      if (iters >= o.max_iters) throw Error{BPQN_ERR_NOCONV, "batched low-fidelity GMRES did not converge"};
+    }
+    // x += M^-1 V y
+    k_bgm_backsolve<<<(R + 127) / 128, 128, 0, st>>>(H, GV, m, kk, R, Y);
+    k_bgm_combine<<<dim3(std::max(1, std::min<int>((int)((n + 255) / 256), 64)), R), 256, 0, st>>>(V.p, Y, (int)n, R,
+                                                                                                   m, kk, Wb.p);
+    BPQN_CHECK_LAUNCH();
+    gemm_rowA(st, M3, g.np * R, M3, g.Minv.p, Wb.p, M3, X.p, M3, 1.0);
+  }
+  // 4. A^ e_l = D^T (-Pi[q_l])
+  DBuf<double> Ad;
+  Ad.alloc((size_t)R * R);
+  for (int l = 0; l < R; ++l) {
+    launch_rigid_readout(g, X.p + (size_t)l * n, g.uo.p, st);
+    launch_dt_gather(g, g.uo.p, Ad.p + (size_t)l * R, 1.0, nullptr, st);
+  }
+  std::vector<double> colmajor((size_t)R * R);
+  BPQN_CUDA(cudaMemcpyAsync(colmajor.data(), Ad.p, 8 * (size_t)R * R, cudaMemcpyDeviceToHost, st));
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  Ahat.assign((size_t)R * R, 0.0);  // row-major A^[i][l] = column l, entry i
+  for (int l = 0; l < R; ++l)
+    for (int i = 0; i < R; ++i) Ahat[(size_t)i * R + l] = colmajor[(size_t)l * R + i];
+  const auto t2 = std::chrono::steady_clock::now();
+  stt.columns = R;
+  stt.iters = iters;
+  stt.restart = m;
+  stt.ms_rhs = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  stt.ms_total = std::chrono::duration<double, std::milli>(t2 - t0).count();
+  stt.bytes = dense_lo_bytes(g, m);
+  return BPQN_OK;
+}
+
+}  // namespace bpqn

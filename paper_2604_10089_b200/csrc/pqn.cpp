@@ -302,36 +302,23 @@ static bool lu_solve_blocked(std::vector<double>& A, int n, Vec& b) {
             for (int j = jb; j < je; ++j) ri[j] -= f * rk[j];
           }
       }
-      // trailing update, four rows at a time (each U12 row is loaded once per four updated rows)
-#pragma omp for schedule(static)
-      for (int i0 = k1; i0 < n; i0 += 4) {
-        const int ni = std::min(4, n - i0);
-        double* r0 = &A[(size_t)i0 * n];
-        double* r1 = ni > 1 ? r0 + n : r0;
-        double* r2 = ni > 2 ? r0 + 2 * (size_t)n : r0;
-        double* r3 = ni > 3 ? r0 + 3 * (size_t)n : r0;
-        for (int k = k0; k < k1; ++k) {
-          const double f0 = r0[k], f1 = ni > 1 ? r1[k] : 0.0, f2 = ni > 2 ? r2[k] : 0.0, f3 = ni > 3 ? r3[k] : 0.0;
-          const double* rk = &A[(size_t)k * n];
-          if (ni == 4) {
-#pragma omp simd
-            for (int j = k1; j < n; ++j) {
-              const double u = rk[j];
-              r0[j] -= f0 * u;
-              r1[j] -= f1 * u;
-              r2[j] -= f2 * u;
-              r3[j] -= f3 * u;
-            }
-          } else {
-            for (int q = 0; q < ni; ++q) {
-              double* rq = r0 + (size_t)q * n;
-              const double f = rq[k];
-#pragma omp simd
-              for (int j = k1; j < n; ++j) rq[j] -= f * rk[j];
-            }
-          }
-        }
+    }
+    // trailing update A22 -= L21 U12 as one register-blocked GEMM (gemm_nt: C = A B^T with
+    // contiguous k = kb rows): L21 and U12^T are copied to contiguous panels first
+    const int m = n - k1;
+    std::vector<double> Lp((size_t)m * kb), Up((size_t)m * kb), Cp((size_t)m * m);
+    for (int i = 0; i < m; ++i)
+      for (int k = 0; k < kb; ++k) {
+        Lp[(size_t)i * kb + k] = A[(size_t)(k1 + i) * n + k0 + k];
+        Up[(size_t)i * kb + k] = A[(size_t)(k0 + k) * n + k1 + i];
       }
+    gemm_nt(Lp.data(), Up.data(), Cp.data(), m, m, kb, false);
+#pragma omp parallel for schedule(static) if (par((long long)m * m))
+    for (int i = 0; i < m; ++i) {
+      double* ri = &A[(size_t)(k1 + i) * n + k1];
+      const double* ci = &Cp[(size_t)i * m];
+#pragma omp simd
+      for (int j = 0; j < m; ++j) ri[j] -= ci[j];
     }
   }
   if (!ok) return false;

@@ -731,3 +731,48 @@ def test_solve_lcp_dense_dev_c1(bp):
                                                   opts=bp.default_solve_opts(method=method, eps_kkt_abs=1e-12))
         assert rc == 0
         assert rel(x.cpu().numpy(), z["lam_brute"]) <= TOL_LAM
+
+
+# ------------------------------------------------------------------ dense LCP matrix / densified low fidelity (R38)
+@pytest.mark.parametrize("c,p", [(1, 8), (2, 6)])
+def test_lcp_matrix_dense_equals_mvps(bp, c, p):
+    """bpqn_lcp_matrix_dense (all Nc mobility solves as one batched GMRES on the assembled dense
+    operator, cuBLAS DGEMM) equals the matrix-free LCP MVP on every unit vector (c1 at p = 8, the c2
+    low fidelity p = 6) to the GMRES tolerance, and at c1 the oracle's densified A."""
+    import torch
+    from synth import make_config
+    cfg = make_config(c)
+    g = bp.Geometry(cfg["centers"], p)
+    bp.contacts(g, cfg["delta"])
+    gm = bp.default_gmres_opts(tol=1e-12)
+    A, st = bp.lcp_matrix_dense(g, gmres=gm)
+    cols = []
+    for l in range(g.nc):
+        e = torch.zeros(g.nc, dtype=torch.float64, device="cuda")
+        e[l] = 1.0
+        w, _ = bp.lcp_mvp(g, e, gmres=gm)
+        cols.append(w.cpu().numpy())
+    Amf = np.stack(cols, axis=1)
+    assert rel(A, Amf) <= 1e-10, rel(A, Amf)
+    if c == 1:
+        assert rel(A, fixture(1)["A_dense"]) <= TOL_VEL
+
+
+def test_solve_lcp_bi_dense_lo_c2(bp):
+    """Bi-PQN with the low-fidelity LCP matrix formed once (lo_dense = 1, R38) reaches the oracle's
+    lambda* at c2 (<= 1e-7) with the oracle-A complementarity (R26) <= 1e-8; every low-fidelity MVP
+    is then an Nc x Nc product."""
+    z = fixture(2)
+    g = bp.Geometry(z["centers"], int(z["p"]))
+    pr, nr, gp = bp.contacts(g, 0.1)
+    lo = bp.Geometry(z["centers"], int(z["p_lo"]))
+    bp.set_contacts(lo, pr, nr, gp)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-10, lo_dense=1)
+    o.gm_hi.tol = 1e-12
+    o.gm_lo.tol = 1e-12
+    lam, rep, rc = bp.solve_lcp(g, lo, T(z["b"]), T(np.zeros(g.nc)), opts=o)
+    assert rc == 0
+    assert rep.lo_dense_columns == g.nc and rep.lo_mvps > 0
+    assert rel(lam.cpu().numpy(), z["lam_bi"]) <= TOL_LAM
+    if "A_dense" in z:
+        assert _kkt(lam.cpu().numpy(), z["A_dense"], z["b"]) <= TOL_KKT
