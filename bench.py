@@ -523,7 +523,9 @@ def run_paper_setting(args, dev, stream):
     # one full DVI step (contacts, U_nc with slip, b, Bi-PQN, M D lambda, Euler, geometry update)
     C = np.ascontiguousarray(cfg["centers"].copy())
     A = np.ascontiguousarray(cfg["axes"].copy())
-    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=int(args.lo_dense))
+    # online steps: each LCP is warm and needs few low-fidelity MVPs, so they stay matrix-free
+    # (forming A^ costs ~Nc lo solves; it pays for the hard standalone LCPs above, R38)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=0)
     o.gm_hi = gmo
     o.gm_lo = gmo
     steps = []
