@@ -39,9 +39,10 @@ struct Cublas {
   cublasCreate_t create = nullptr;
   cublasSetStream_t setStream = nullptr;
   cublasDgemm_t dgemm = nullptr;
-  void* handle = nullptr;
   std::string why;
 };
+// one cuBLAS handle per calling thread (distinct geometry handles may be used from different threads)
+static void* cublas_handle();
 static Cublas& cublas() {
   static Cublas c;
   static std::once_flag once;
@@ -56,10 +57,15 @@ static Cublas& cublas() {
     c.create = reinterpret_cast<cublasCreate_t>(dlsym(h, "cublasCreate_v2"));
     c.setStream = reinterpret_cast<cublasSetStream_t>(dlsym(h, "cublasSetStream_v2"));
     c.dgemm = reinterpret_cast<cublasDgemm_t>(dlsym(h, "cublasDgemm_v2"));
-    if (!c.create || !c.setStream || !c.dgemm || c.create(&c.handle) != 0) c.why = "cuBLAS initialisation failed";
+    if (!c.create || !c.setStream || !c.dgemm) c.why = "cuBLAS lacks a required symbol";
   });
   if (!c.why.empty()) throw Error{BPQN_ERR_CUDA, c.why};
   return c;
+}
+static void* cublas_handle() {
+  thread_local void* h = nullptr;
+  if (!h && cublas().create(&h) != 0) throw Error{BPQN_ERR_CUDA, "cublasCreate failed"};
+  return h;
 }
 constexpr int CUBLAS_OP_N_ = 0, CUBLAS_OP_T_ = 1;
 
@@ -67,9 +73,10 @@ constexpr int CUBLAS_OP_N_ = 0, CUBLAS_OP_T_ = 1;
 static void gemm_rowA(cudaStream_t st, int m, int n, int k, const double* A_row, const double* B, int ldb, double* C,
                       int ldc, double beta = 0.0) {
   Cublas& cb = cublas();
+  void* h = cublas_handle();
   const double one = 1.0;
-  if (cb.setStream(cb.handle, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
-  if (cb.dgemm(cb.handle, CUBLAS_OP_T_, CUBLAS_OP_N_, m, n, k, &one, A_row, k, B, ldb, &beta, C, ldc) != 0)
+  if (cb.setStream(h, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
+  if (cb.dgemm(h, CUBLAS_OP_T_, CUBLAS_OP_N_, m, n, k, &one, A_row, k, B, ldb, &beta, C, ldc) != 0)
     throw Error{BPQN_ERR_CUDA, "cublasDgemm failed"};
 }
 
@@ -288,7 +295,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   while (m > 8 && dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr) m /= 2;
   if (dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr)
     throw Error{BPQN_ERR_OOM, "dense low-fidelity operator does not fit in device memory"};
-  cublas();  // fail early if cuBLAS is missing
+  cublas_handle();  // fail early if cuBLAS is missing
   DBuf<double> A, V, B, Wb, X, Z, sm;
   A.alloc(n * n);
   V.alloc((size_t)(m + 1) * R * n);
