@@ -245,6 +245,7 @@ void gmres_recycle_reserve(Geom& g);        // recycling store (outside the hot 
 constexpr int GM_BATCH_MAX_M = 128;
 struct DenseLoStats {
   int columns = 0, iters = 0, restart = 0;
+  long long col_iters = 0;  // sum over columns of their iterations (the GEMM work with compaction)
   double ms_rhs = 0, ms_total = 0;
   size_t bytes = 0;
 };

@@ -11,9 +11,10 @@
 //     p_lo = 8: 93 312^2 doubles = 69.7 GB of the 180 GB HBM);
 //   * right hand sides b_l = -S_full[P^T D e_l] (one single-layer apply per contact);
 //   * Nc independent right-preconditioned GMRES(m) processes advance together: per iteration one
-//     block-Jacobi GEMM (Minv on every sphere of every column) and one [3N x 3N] x [3N x Nc] GEMM
-//     (cuBLAS DGEMM, 35 TFLOP/s measured), then one CTA per column runs its CGS2, Givens rotations
-//     and residual; each column stops at its own relative residual tolerance;
+//     block-Jacobi GEMM (Minv on every sphere of every column) and one [3N x 3N] x [3N x Nc_active]
+//     GEMM (cuBLAS DGEMM, 35 TFLOP/s measured) over the columns not yet converged (gathered
+//     contiguously), then one CTA per active column runs its CGS2, Givens rotations and residual;
+//     each column stops at its own relative residual tolerance and leaves the GEMMs;
 //   * A^ e_l = D^T (-Pi[q_l]) (the rigid read-out and D^T gather of every MVP).
 // Every later low-fidelity MVP of the solve is the 540 x 540 product A^ v on the host.  cuBLAS is
 // resolved at run time (dlopen; the copy torch loaded when there is one).
@@ -148,7 +149,8 @@ __global__ void k_dense_self(int N, int nq, const double* __restrict__ EA, doubl
 // ---------------------------------------------------------------- batched GMRES, one CTA per column
 struct BgmParams {
   double* V;        // [(m+1)][R][n]
-  const double* W;  // [R][n] operator output A M^-1 v_k
+  const double* W;  // [Ra][n] operator output A M^-1 v_k of the active columns (compacted)
+  const int* idx;   // [Ra] active column of each CTA
   int n, R, m, k;
   double* H;        // [R][(m+1) m]
   double *cs, *sn, *gv;  // [R][m], [R][m], [R][m+1]
@@ -170,9 +172,9 @@ __device__ __forceinline__ double block_sum(double v, double* sred) {
 __global__ void __launch_bounds__(512) k_bgm_step(BgmParams P) {
   __shared__ double sred[16];
   __shared__ double h[2][GM_BATCH_MAX_M + 1];
-  const int col = blockIdx.x, k = P.k, n = P.n;
+  const int col = P.idx[blockIdx.x], k = P.k, n = P.n;
   double* w = P.V + ((size_t)(k + 1) * P.R + col) * n;  // z lands in V_{k+1}
-  const double* z = P.W + (size_t)col * n;
+  const double* z = P.W + (size_t)blockIdx.x * n;
   for (int e = threadIdx.x; e < n; e += blockDim.x) w[e] = z[e];
   for (int pass = 0; pass < 2; ++pass) {  // CGS2
     for (int i = 0; i <= k; ++i) {
@@ -241,9 +243,10 @@ __global__ void k_bgm_start(double* V, const double* r, int n, int m, double* gv
 }
 
 // y = H^-1 gv per column (back substitution, one thread per column); X[:, col] = sum_i y_i V_i
-__global__ void k_bgm_backsolve(const double* H, const double* gv, int m, int kk, int R, double* y) {
+__global__ void k_bgm_backsolve(const double* H, const double* gv, int m, const int* kkv, int R, double* y) {
   const int col = blockIdx.x * blockDim.x + threadIdx.x;
   if (col >= R) return;
+  const int kk = kkv[col];
   const double* Hc = H + (size_t)col * (m + 1) * m;
   double* yc = y + (size_t)col * m;
   for (int i = kk - 1; i >= 0; --i) {
@@ -253,13 +256,20 @@ __global__ void k_bgm_backsolve(const double* H, const double* gv, int m, int kk
   }
 }
 
-__global__ void k_bgm_combine(const double* V, const double* y, int n, int R, int m, int kk, double* X) {
-  const int col = blockIdx.y;
+__global__ void k_bgm_combine(const double* V, const double* y, int n, int R, int m, const int* kkv, double* X) {
+  const int col = blockIdx.y, kk = kkv[col];
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) {
     double acc = 0.0;
     for (int i = 0; i < kk; ++i) acc = fma(V[((size_t)i * R + col) * n + e], y[(size_t)col * m + i], acc);
     X[(size_t)col * n + e] = acc;
   }
+}
+
+// out[:, a] = V[:, idx[a]] (the active columns, contiguous for the GEMMs)
+__global__ void k_gather_cols(const double* __restrict__ V, const int* __restrict__ idx, int n, double* __restrict__ out) {
+  const double* src = V + (size_t)idx[blockIdx.y] * n;
+  double* dst = out + (size_t)blockIdx.y * n;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n; e += gridDim.x * blockDim.x) dst[e] = src[e];
 }
 
 __global__ void k_sub_cols(double* r, const double* b, const double* ax, size_t tot) {
@@ -296,8 +306,12 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   if (dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr)
     throw Error{BPQN_ERR_OOM, "dense low-fidelity operator does not fit in device memory"};
   cublas_handle();  // fail early if cuBLAS is missing
-  DBuf<double> A, V, B, Wb, X, Z, sm;
+  DBuf<double> A, V, B, Wb, X, Z, G, sm;
+  DBuf<int> didx, dkk;
   A.alloc(n * n);
+  G.alloc((size_t)R * n);
+  didx.alloc(R);
+  dkk.alloc(R);
   V.alloc((size_t)(m + 1) * R * n);
   B.alloc((size_t)R * n);
   Wb.alloc((size_t)R * n);
@@ -340,13 +354,15 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   // 3. batched right-preconditioned GMRES(m), x0 = 0
   BPQN_CUDA(cudaMemsetAsync(X.p, 0, 8 * (size_t)R * n, st));
   const int M3 = 3 * nq;
-  auto apply_op = [&](const double* in, double* out) {  // out = A_op Minv in (all columns)
-    gemm_rowA(st, M3, g.np * R, M3, g.Minv.p, in, M3, Z.p, M3);
-    gemm_rowA(st, (int)n, R, (int)n, A.p, Z.p, (int)n, out, (int)n);
+  auto apply_op = [&](const double* in, int ncol, double* out) {  // out = A_op Minv in (ncol columns)
+    gemm_rowA(st, M3, g.np * ncol, M3, g.Minv.p, in, M3, Z.p, M3);
+    gemm_rowA(st, (int)n, ncol, (int)n, A.p, Z.p, (int)n, out, (int)n);
   };
   std::vector<double> res(R);
+  std::vector<int> active, kkc(R);
   int iters = 0;
   bool first = true, done = false;
+  long long col_iters = 0;
   while (!done) {
     const double* r0 = B.p;
     if (!first) {  // restart: r = b - A x  (x holds the solution so far, already M^-1 applied)
@@ -358,28 +374,43 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
     first = false;
     k_bgm_start<<<R, 512, 0, st>>>(V.p, r0, (int)n, m, GV, BETA, RES, BN);
     BPQN_CHECK_LAUNCH();
-    int kk = 0;
-    for (int k = 0; k < m; ++k) {
-      apply_op(V.p + (size_t)k * R * n, Wb.p);
-      BgmParams P{V.p, Wb.p, (int)n, R, m, k, H, CS, SN, GV, BETA, RES};
-      k_bgm_step<<<R, 512, 0, st>>>(P);
+    // columns already at tolerance (a restart) take no step; the others are compacted for the GEMMs
+    BPQN_CUDA(cudaMemcpyAsync(res.data(), RES, 8 * (size_t)R, cudaMemcpyDeviceToHost, st));
+    BPQN_CUDA(cudaStreamSynchronize(st));
+    active.clear();
+    for (int c = 0; c < R; ++c) {
+      kkc[c] = 0;
+      if (!(res[c] <= o.tol)) active.push_back(c);
+    }
+    for (int k = 0; k < m && !active.empty(); ++k) {
+      const int Ra = (int)active.size();
+      BPQN_CUDA(cudaMemcpyAsync(didx.p, active.data(), 4 * (size_t)Ra, cudaMemcpyHostToDevice, st));
+      k_gather_cols<<<dim3(std::max(1, std::min<int>((int)((n + 255) / 256), 32)), Ra), 256, 0, st>>>(
+          V.p + (size_t)k * R * n, didx.p, (int)n, G.p);
+      apply_op(G.p, Ra, Wb.p);
+      BgmParams P{V.p, Wb.p, didx.p, (int)n, R, m, k, H, CS, SN, GV, BETA, RES};
+      k_bgm_step<<<Ra, 512, 0, st>>>(P);
       BPQN_CHECK_LAUNCH();
-      kk = k + 1;
       ++iters;
+      col_iters += Ra;
       BPQN_CUDA(cudaMemcpyAsync(res.data(), RES, 8 * (size_t)R, cudaMemcpyDeviceToHost, st));
       BPQN_CUDA(cudaStreamSynchronize(st));
-      const double worst = *std::max_element(res.begin(), res.end());
-      if (!std::isfinite(worst)) throw Error{BPQN_ERR_NAN, "NaN in the batched low-fidelity GMRES"};
-      if (worst <= o.tol) {
-        done = true;
-        break;
+      std::vector<int> still;
+      for (int c : active) {
+        if (!std::isfinite(res[c])) throw Error{BPQN_ERR_NAN, "NaN in the batched low-fidelity GMRES"};
+        kkc[c] = k + 1;
+        if (res[c] > o.tol) still.push_back(c);
       }
-      if (iters >= o.max_iters) throw Error{BPQN_ERR_NOCONV, "batched low-fidelity GMRES did not converge"};
+      active.swap(still);
+      if (active.empty()) done = true;
+      else if (iters >= o.max_iters) throw Error{BPQN_ERR_NOCONV, "batched low-fidelity GMRES did not converge"};
     }
-    // x += M^-1 V y
-    k_bgm_backsolve<<<(R + 127) / 128, 128, 0, st>>>(H, GV, m, kk, R, Y);
+    if (active.empty()) done = true;
+    // x += M^-1 V y, each column with its own step count
+    BPQN_CUDA(cudaMemcpyAsync(dkk.p, kkc.data(), 4 * (size_t)R, cudaMemcpyHostToDevice, st));
+    k_bgm_backsolve<<<(R + 127) / 128, 128, 0, st>>>(H, GV, m, dkk.p, R, Y);
     k_bgm_combine<<<dim3(std::max(1, std::min<int>((int)((n + 255) / 256), 64)), R), 256, 0, st>>>(V.p, Y, (int)n, R,
-                                                                                                   m, kk, Wb.p);
+                                                                                                   m, dkk.p, Wb.p);
     BPQN_CHECK_LAUNCH();
     gemm_rowA(st, M3, g.np * R, M3, g.Minv.p, Wb.p, M3, X.p, M3, 1.0);
   }
@@ -399,6 +430,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   const auto t2 = std::chrono::steady_clock::now();
   stt.columns = R;
   stt.iters = iters;
+  stt.col_iters = col_iters;
   stt.restart = m;
   stt.ms_rhs = std::chrono::duration<double, std::milli>(t1 - t0).count();
   stt.ms_total = std::chrono::duration<double, std::milli>(t2 - t0).count();
