@@ -55,6 +55,7 @@ def parse():
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--replicas", action="store_true")  # N > 1: independent replicas instead of the sharded MVP
     ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
+    ap.add_argument("--shard-world1", action="store_true")    # N = 1: the sharded NCCL code path on a one-rank communicator
     ap.add_argument("--shard-asym", action="store_true")  # sharded K1 as the one-directional kernel (no reduce-scatter)
     ap.add_argument("--sub-forcing", type=float, default=0.0)   # Bi-PQN inexact subproblems (off = R22)
     ap.add_argument("--lo-dense", type=int, default=1)  # Bi-PQN: form the low-fidelity A^ once (R38); 0 = matrix-free
@@ -296,8 +297,10 @@ def run_ours(args, ws, rank, local):
     t_init = time.time() - t0
     pairs, nrm, gaps = bp.contacts(g, cfg["delta"])
     nc = g.nc
-    shard = ws > 1 and not args.replicas
-    if shard:   # strong scaling of one MVP: each rank owns Np/N spheres' rows
+    shard = (ws > 1 and not args.replicas) or args.shard_world1
+    if shard and ws == 1:   # self-test of the sharded path: one-rank NCCL communicator
+        bp.geometry_shard_nccl(g, 0, 1, bp.nccl_unique_id(), symmetric=not args.shard_asym)
+    elif shard:   # strong scaling of one MVP: each rank owns Np/N spheres' rows
         if args.shard_callback:
             bp.geometry_shard(g, rank, ws, symmetric=not args.shard_asym)
         else:
