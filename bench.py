@@ -58,7 +58,7 @@ def parse():
     ap.add_argument("--shard-world1", action="store_true")    # N = 1: the sharded NCCL code path on a one-rank communicator
     ap.add_argument("--shard-asym", action="store_true")  # sharded K1 as the one-directional kernel (no reduce-scatter)
     ap.add_argument("--sub-forcing", type=float, default=0.0)   # Bi-PQN inexact subproblems (off = R22)
-    ap.add_argument("--lo-dense", type=int, default=1)  # Bi-PQN: form the low-fidelity A^ once (R38); 0 = matrix-free
+    ap.add_argument("--lo-dense", type=int, default=2)  # Bi-PQN: A^ formed once (1), matrix-free (0), auto (2; R38)
     ap.add_argument("--c5-steps", type=int, default=3)
     ap.add_argument("--cpu-sample-targets", type=int, default=0)
     return ap.parse_args()
@@ -526,9 +526,9 @@ def run_paper_setting(args, dev, stream):
     # one full DVI step (contacts, U_nc with slip, b, Bi-PQN, M D lambda, Euler, geometry update)
     C = np.ascontiguousarray(cfg["centers"].copy())
     A = np.ascontiguousarray(cfg["axes"].copy())
-    # online steps: each LCP is warm and needs few low-fidelity MVPs, so they stay matrix-free
-    # (forming A^ costs ~Nc lo solves; it pays for the hard standalone LCPs above, R38)
-    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=0)
+    # online steps: warm LCPs with few approaching contacts need few low-fidelity MVPs; the auto
+    # mode (R38) keeps those matrix-free (forming A^ costs ~Nc lo solves)
+    o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=int(args.lo_dense))
     o.gm_hi = gmo
     o.gm_lo = gmo
     steps = []

@@ -112,7 +112,9 @@ typedef struct {
                                  double-layer operator of `lo`, FP64 GEMMs on the tensor cores; gm_lo's
                                  tolerance per column; R38) and apply it as an Nc x Nc product for
                                  every low-fidelity MVP; falls back to matrix-free lo MVPs if the dense
-                                 operator (8 (3 N_lo)^2 bytes) does not fit.  0 (default): matrix-free */
+                                 operator (8 (3 N_lo)^2 bytes) does not fit.  2: auto -- form A^ when at least
+                                 a quarter of the b_l are negative (a hard LCP with hundreds of lo MVPs).
+                                 0 (default): matrix-free */
 } bpqn_solve_opts;
 
 typedef struct {

@@ -632,7 +632,13 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     DenseLoStats dls;
     std::vector<double> Ahat;
     bool dense_lo = false;
-    if (bi && o.lo_dense) {
+    // lo_dense = 2 (auto): form A^ when the LCP looks hard -- at least a quarter of the contacts start
+    // approaching (b_l < 0), where Bi-PQN needs hundreds of lo MVPs (c4: 41 % negative, 386 lo MVPs);
+    // warm online steps with a few approaching contacts need tens and stay matrix-free
+    int n_neg = 0;
+    for (double v : b) n_neg += v < 0.0;
+    const bool want_dense = o.lo_dense == 1 || (o.lo_dense == 2 && 4 * n_neg >= nc);
+    if (bi && want_dense) {
       try {
         densify_lcp(*lo, glo, Ahat, dls, s);
         dense_lo = true;
