@@ -1,7 +1,7 @@
 """GMRES recycling / deflation study (development aid): a sequence of MVPs on one
 geometry with recycle=1, iterations per solve and agreement with cold solves.
 
-  BPQN_DEFLATE=16 python tools/recycle_study.py --config 2 --n 6
+  python tools/recycle_study.py --config 2 --n 6
 """
 import argparse
 import json
