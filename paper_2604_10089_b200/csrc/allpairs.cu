@@ -828,7 +828,8 @@ static void sym_ws(const Geom& g, int cfg, size_t& pseg, size_t& psrc, size_t& p
 
 // Launch shape, measured on B200 (profiles/r01_k1_sym_shapes.md): 8 warps at 1 CTA/SM with
 // 5 (D, S) or 4 (S+D) targets/lane for N >= 6e4 (c4: D 14.81, S 15.65, S+D 22.60 ms), 4 targets/lane
-// for N >= 2e4 (c3 D 1.355 vs 1.46 ms with 3; c4 centres at p = 8: 1.14 vs 1.17 ms), 8 x 3 below.
+// for N >= 2e4 (c3 D 1.355 vs 1.46 ms with 3; c4 centres at p = 8: 1.14 vs 1.17 ms), 8 x 3 below, and
+// 4 x 3 (two CTAs per SM) below N = 4000 (c1: 0.022 vs 0.028 ms; profiles/r02_k1_v8_ncu.md).
 // BPQN_K1_CFG = 0..3 forces one shape for A/B runs.
 static int k1_cfg() {
   static int v = -2;
@@ -842,7 +843,7 @@ static int k1_cfg() {
 static int sym_cfg(const Geom& g, int mode) {
   const int c = k1_cfg();
   if (c >= 0) return c;
-  return g.n >= 60000 ? (mode == MODE_SD ? 4 : 14) : (g.n >= 20000 ? 4 : 3);
+  return g.n >= 60000 ? (mode == MODE_SD ? 4 : 14) : (g.n >= 20000 ? 4 : (g.n >= 4000 ? 3 : 6));
 }
 
 // target-block size 32 W R of each launch shape (must match launch_sym's table): the packed
