@@ -614,12 +614,12 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
       }
     }
     __syncthreads();  // ring[buf] consumed by every warp; red[par] complete
-    if (!diag) {
-      if (tid < K1_TS * 3) {
+    if (!diag) {  // 192 values per tile: every thread of the block takes its share (4-warp shapes have 128)
+      for (int e = tid; e < K1_TS * 3; e += 32 * KS_W) {
         double sum = 0.0;
 #pragma unroll
-        for (int w = 0; w < KS_W; ++w) sum += red[par][w][tid];
-        P.psrc[(size_t)b_cur * P.psrc_ld + 3 * (size_t)t_cur * K1_TS + tid] = sum;
+        for (int w = 0; w < KS_W; ++w) sum += red[par][w][e];
+        P.psrc[(size_t)b_cur * P.psrc_ld + 3 * (size_t)t_cur * K1_TS + e] = sum;
       }
       par ^= 1;
     }

@@ -776,3 +776,21 @@ def test_solve_lcp_bi_dense_lo_c2(bp):
     assert rel(lam.cpu().numpy(), z["lam_bi"]) <= TOL_LAM
     if "A_dense" in z:
         assert _kkt(lam.cpu().numpy(), z["A_dense"], z["b"]) <= TOL_KKT
+
+
+@pytest.mark.parametrize("cfg", [0, 3, 4, 6, 11, 14, 15, 16, 19, 22])
+def test_k1_launch_shapes_agree(bp, cfg):
+    """Every selectable symmetric-K1 launch shape (BPQN_K1_CFG) equals the one-directional
+    kernel (BPQN_K1=asym) on c1 and c2 for S, D and S+D layer applies (a 4-warp shape once dropped the
+    source-side sums of the tile rows its 128 threads did not cover)."""
+    import subprocess
+    import sys
+    tool = os.path.join(ROOT, "tools", "k1_cfg_check.py")
+    for c in (1, 2):
+        out = subprocess.run([sys.executable, tool, "--config", str(c), "--cfgs", str(cfg)], capture_output=True,
+                             text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        line = [l for l in out.stdout.splitlines() if l.startswith("cfg")][-1]
+        errs = [float(x) for x in line.split("{")[1].replace("'", "").replace("}", "").replace(",", "").split()
+                if x[0].isdigit()]
+        assert len(errs) == 3 and max(errs) <= 1e-12, line
