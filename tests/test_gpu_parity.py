@@ -171,10 +171,11 @@ def test_layer_apply_block_padding_regression(bp):
     assert rel(us[tg], d.apply(f=f, targets=tg)) <= TOL_SUM
 
 
-@pytest.mark.parametrize("nsph,p", [(70, 12), (41, 16)])
+@pytest.mark.parametrize("nsph,p", [(70, 12), (41, 16), (125, 3)])
 def test_layer_apply_ragged_blocks(bp, nsph, p):
     """Mid-size scenes whose N is not a multiple of the K1 target block (70 x 312 = 21 840
-    with 1024-point blocks; 41 x 544 = 22 304), sampled targets against the oracle."""
+    with 1024-point blocks; 41 x 544 = 22 304), sampled targets against the oracle; 125 spheres at
+    p = 3 (Nq = 24 < 32: the one-directional K1 over three 1024-row blocks and its segment partials)."""
     from oracle.layer import Disc
     rng = np.random.default_rng(nsph)
     g1 = np.arange(5) * 2.04
