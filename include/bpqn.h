@@ -202,6 +202,12 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
 int bpqn_lcp_matrix_dense(bpqn_geom_t g, const bpqn_gmres_opts* gm, double* A_host, bpqn_gmres_stats* st,
                           void* stream);
 
+/* The handle's completed double-layer GMRES operator A_op = -I/2 + D_full + Pi_R (O7) as a dense
+ * row-major [3N][3N] matrix written to A_dev (caller-owned, 8 (3N)^2 bytes): A_dev q equals the matrix-free
+ * operator applied to q (coarse pairs, refined near rows, self blocks).  Diagnostic / preconditioner
+ * studies; N <= 65535, unsharded. */
+int bpqn_operator_dense(bpqn_geom_t g, double* A_dev, void* stream);
+
 /* Report of one DVI time step (bpqn_dvi_step). */
 typedef struct {
   int n_contacts;           /* candidate contacts (gap < delta) at the start of the step */

@@ -82,6 +82,7 @@ SYMBOLS = {
     "bpqn_geometry_shard_symmetric": (c_int, [c_void_p, c_void_p, c_void_p, ALLGATHER_FN, c_void_p]),
     "bpqn_nccl_unique_id": (c_int, [c_void_p]),
     "bpqn_lcp_matrix_dense": (c_int, [c_void_p, P(GmresOpts), c_void_p, P(GmresStats), c_void_p]),
+    "bpqn_operator_dense": (c_int, [c_void_p, c_void_p, c_void_p]),
     "bpqn_diag_rsqrt_seed": (c_int, [c_int, c_int, P(c_double)]),
     "bpqn_geometry_shard_nccl": (c_int, [c_void_p, c_int, c_int, c_void_p, c_int]),
     "bpqn_geometry_update": (c_int, [c_void_p, c_void_p, c_void_p]),
@@ -437,6 +438,16 @@ def lcp_matrix_dense(g, gmres=None, stream=None):
     _check(lib().bpqn_lcp_matrix_dense(g.h, ctypes.byref(gmres) if gmres is not None else None,
                                        A.ctypes.data_as(c_void_p), ctypes.byref(st), _stream(stream)))
     return A, st
+
+
+def operator_dense(g, out=None, stream=None):
+    """The completed double-layer operator as a dense CUDA tensor [3N, 3N] (bpqn_operator_dense)."""
+    import torch
+    n = 3 * g.N
+    if out is None:
+        out = torch.empty((n, n), dtype=torch.float64, device="cuda")
+    _check(lib().bpqn_operator_dense(g.h, _ptr(out), _stream(stream)))
+    return out
 
 
 def nccl_unique_id():

@@ -250,6 +250,7 @@ struct DenseLoStats {
   size_t bytes = 0;
 };
 size_t dense_lo_bytes(const Geom& g, int restart);
+void assemble_dense_operator(Geom& g, double* A_dev, cudaStream_t s);  // [3N][3N] row-major
 // A^ = D^T M D of the handle's contact set (row-major Nc x Nc, host) by one batched GMRES over all
 // Nc unit vectors with a dense operator; throws BPQN_ERR_OOM if it does not fit
 int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, DenseLoStats& st, cudaStream_t s);

@@ -951,6 +951,14 @@ int bpqn_lcp_matrix_dense(bpqn_geom_t g, const bpqn_gmres_opts* gm, double* A_ho
   });
 }
 
+int bpqn_operator_dense(bpqn_geom_t g, double* A_dev, void* stream) {
+  return guarded([&]() -> int {
+    BPQN_REQUIRE(g && A_dev, "null pointer");
+    assemble_dense_operator(*g, A_dev, S(stream));
+    return BPQN_OK;
+  });
+}
+
 int bpqn_gmres_recycle_reset(bpqn_geom_t g) {
   return guarded([&]() -> int {
     BPQN_REQUIRE(g, "null handle");

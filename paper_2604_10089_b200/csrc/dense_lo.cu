@@ -146,6 +146,23 @@ __global__ void k_dense_self(int N, int nq, const double* __restrict__ EA, doubl
   }
 }
 
+// The whole completed double-layer operator A_op of a handle as a dense row-major [3N][3N] matrix in
+// a caller-owned device buffer (bpqn_operator_dense; diagnostics and preconditioner studies).
+void assemble_dense_operator(Geom& g, double* A, cudaStream_t st) {
+  const int N = g.n;
+  BPQN_REQUIRE(N <= 65535 && !g.sharded(), "dense operator: N <= 65535 nodes, unsharded handle");
+  k_dense_coarse<<<dim3((N + 255) / 256, N), 256, 0, st>>>(N, g.src.p, A);
+  BPQN_CHECK_LAUNCH();
+  if (g.n_inc > 0) {
+    const int nbp = (g.nb + 1) & ~1;
+    k_dense_near<<<(unsigned)g.n_inc, 128, 6 * g.nb * sizeof(double), st>>>(N, g.nq, g.nb, nbp, g.cm_t.p, g.cm_m.p,
+                                                                             g.T_D.p, g.analysis.p, A);
+    BPQN_CHECK_LAUNCH();
+  }
+  k_dense_self<<<N, 256, 0, st>>>(N, g.nq, g.E_A.p, A);
+  BPQN_CHECK_LAUNCH();
+}
+
 // ---------------------------------------------------------------- batched GMRES, one CTA per column
 struct BgmParams {
   double* V;        // [(m+1)][R][n]
@@ -322,16 +339,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   double *H = sm.p, *CS = H + hs, *SN = CS + cs, *Y = SN + cs, *GV = Y + cs, *BETA = GV + gs, *RES = BETA + R,
          *BN = RES + R;
   // 1. assemble A_op (coarse -> near rows replace -> self blocks add)
-  k_dense_coarse<<<dim3((N + 255) / 256, N), 256, 0, st>>>(N, g.src.p, A.p);
-  BPQN_CHECK_LAUNCH();
-  if (g.n_inc > 0) {
-    const int nbp = (g.nb + 1) & ~1;
-    k_dense_near<<<(unsigned)g.n_inc, 128, 6 * g.nb * sizeof(double), st>>>(N, nq, g.nb, nbp, g.cm_t.p, g.cm_m.p,
-                                                                             g.T_D.p, g.analysis.p, A.p);
-    BPQN_CHECK_LAUNCH();
-  }
-  k_dense_self<<<N, 256, 0, st>>>(N, nq, g.E_A.p, A.p);
-  BPQN_CHECK_LAUNCH();
+  assemble_dense_operator(g, A.p, st);
   // 2. right-hand sides b_l = -S[P^T D e_l]
   BPQN_REQUIRE(g.E_S.p, "geometry built without single-layer data");
   DBuf<double> eye;
