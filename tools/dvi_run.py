@@ -21,13 +21,14 @@ ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--p", type=int, default=8)
 ap.add_argument("--p-lo", type=int, default=4)
 ap.add_argument("--dt", type=float, default=1e-2)
+ap.add_argument("--lo-dense", type=int, default=2)   # R38: 2 = auto
 a = ap.parse_args()
 cfg = make_config(4)
 C = np.ascontiguousarray(cfg["centers"].copy())
 A = np.ascontiguousarray(cfg["axes"].copy())
 hi = bp.Geometry(C, a.p)
 lo = bp.Geometry(C, a.p_lo)
-o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500)
+o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=a.lo_dense)
 o.gm_hi = bp.default_gmres_opts(tol=1e-8)
 o.gm_lo = bp.default_gmres_opts(tol=1e-8)
 t0 = time.perf_counter()
