@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--no-c5", action="store_true")
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--recycle", type=int, default=1)   # GMRES recycling inside the LCP solve (NEXT-3)
-    ap.add_argument("--solvers", default="bi,mono")     # comma list of bi, mono, bb (BB-PGD)
+    ap.add_argument("--solvers", default="bi,mono,bb")  # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--replicas", action="store_true")  # N > 1: independent replicas instead of the sharded MVP
     ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
