@@ -162,7 +162,7 @@ def oracle_kg(c, tol=1e-8):
     return 100, "assumed (no oracle record)"
 
 
-def oracle_mvp_sample(cfg, k_g, n_targets=0, n_inc_sample=2000, seed=7):
+def oracle_mvp_sample(cfg, k_g, n_targets=0, n_inc_sample=2000, seed=7, sd=False):
     """The oracle (oracle/: plain-C OpenMP direct sum for the coarse part, numpy for the near,
     self and GMRES vector work, exactly the operations oracle.mobility.gmres / oracle.layer.Disc
     perform per operator pass) timed on a bounded sample of one LCP MVP:
@@ -195,6 +195,7 @@ def oracle_mvp_sample(cfg, k_g, n_targets=0, n_inc_sample=2000, seed=7):
         excl[i].append(m)
     rng = np.random.default_rng(seed)
     q = rng.standard_normal((N, 3))
+    f = rng.standard_normal((N, 3)) if sd else None   # S+D layer apply (c5): both densities
     n_targets = n_targets or max(1, N // 8)
     idx = np.sort(rng.choice(N, size=min(n_targets, N), replace=False))
     excl_ptr = np.zeros(idx.size + 1, dtype=np.int64)
@@ -203,7 +204,7 @@ def oracle_mvp_sample(cfg, k_g, n_targets=0, n_inc_sample=2000, seed=7):
         ex.extend(excl[t])
         excl_ptr[k + 1] = len(ex)
     t0 = time.perf_counter()
-    native.far_sum(X[idx], sphere_of[idx], excl_ptr, np.array(ex, dtype=np.int64), npn, nq, X, NRM, W, None, q,
+    native.far_sum(X[idx], sphere_of[idx], excl_ptr, np.array(ex, dtype=np.int64), npn, nq, X, NRM, W, f, q,
                    cfg["mu"])
     t_far = (time.perf_counter() - t0) * N / idx.size
     nb = p * p + 2 * p
@@ -215,19 +216,21 @@ def oracle_mvp_sample(cfg, k_g, n_targets=0, n_inc_sample=2000, seed=7):
         out = np.zeros((ns, 3))
         t0 = time.perf_counter()
         np.add.at(out, np.arange(ns), np.einsum("kabn,knb->ka", T, cf))
-        t_near = (time.perf_counter() - t0) * len(inc) / ns
+        t_near = (time.perf_counter() - t0) * len(inc) / ns * (2 if sd else 1)
     D = rng.standard_normal((nq, 3, nq, 3))
     t0 = time.perf_counter()
     np.einsum("iajb,njb->nia", D, q.reshape(npn, nq, 3))
-    t_self = time.perf_counter() - t0
+    t_self = (time.perf_counter() - t0) * (2 if sd else 1)
     kb = max(1, k_g // 2)
-    V = [rng.standard_normal(3 * N) for _ in range(kb)]
-    w = rng.standard_normal(3 * N)
-    t0 = time.perf_counter()
-    for v in V:
-        h = np.dot(v, w)
-        w = w - h * v
-    t_gm = time.perf_counter() - t0
+    t_gm = 0.0
+    if k_g > 0:
+        V = [rng.standard_normal(3 * N) for _ in range(kb)]
+        w = rng.standard_normal(3 * N)
+        t0 = time.perf_counter()
+        for v in V:
+            h = np.dot(v, w)
+            w = w - h * v
+        t_gm = time.perf_counter() - t0
     per_pass = t_far + t_near + t_self + t_gm
     passes = k_g + 1
     return dict(ms=per_pass * passes * 1e3, passes=passes, N=N, n_inc=len(inc), n_targets=int(idx.size),
@@ -581,7 +584,12 @@ def run_c5(args, dev, stream):
     prof = bp.profile_get(g)
     m = float(np.mean(ms))
     k1_tflops = prof["allpairs_gflop"] / max(prof["ms_allpairs"], 1e-9)
+    r = oracle_mvp_sample(cfg, 0, sd=True)     # the CPU oracle's S+D layer apply, sampled (bench.py model)
     out = {"workload": "c5 layer apply S+D (216 spheres, p=24, N=%d)" % g.N, "ms": m,
+           "cpu_baseline": {"value": r["ms"], "unit": "ms", "cores": cores_used(), "kind": "oracle",
+                            "sample": "far S+D sum for %d of %d targets (plain C, OpenMP) + near / self einsums, one "
+                                      "application; host %s" % (r["n_targets"], r["N"], cpu_desc()),
+                            "per_pass_s": r["per_pass_s"]},
            "pair_interactions_per_s": float(g.N) * g.N / (m * 1e-3),
            "k1_ms": prof["ms_allpairs"] / args.c5_steps, "k2_ms": prof["ms_near"] / args.c5_steps,
            "k3_ms": prof["ms_self"] / args.c5_steps,
