@@ -17,6 +17,7 @@
 // test says stop -- the host synchronises once per cycle, not once per iteration.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -571,7 +572,11 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   // handle and restart length; not when profiling events, sharding or BPQN_GRAPHS=0 make the step
   // non-capturable)
   CycleGraph& CG = g.gm_cycle;
-  const bool use_graphs = graphs_enabled() && !g.prof.events && !g.sharded() && !g.overlap_k2 && CG.ok;
+  // callback sharding synchronises the stream inside the operator (not capturable); the NCCL sharding
+  // enqueues its collectives on the streams and is captured like the single-GPU step (falls back to
+  // host-driven steps if the capture or instantiation is refused)
+  const bool capturable_shard = !g.sharded() || (g.nccl_comm && !g.sh_fn && !g.sh_rs_fn);
+  const bool use_graphs = graphs_enabled() && !g.prof.events && capturable_shard && !g.overlap_k2 && CG.ok;
   if (CG.exec && (CG.m != m || CG.pre != pre || CG.V != g.V.p || CG.S != g.scal.p || CG.red != g.red.p))
     CG.clear();
   auto build_graph = [&]() -> bool {
@@ -612,6 +617,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       cudaGetLastError();
       CG.clear();
       CG.ok = false;  // not capturable here: host-driven steps from now on
+      if (getenv("BPQN_LOG_MVP")) fprintf(stderr, "gmres: cycle graph not capturable, host-driven steps\n");
       return false;
     }
     CG.m = m;

@@ -107,8 +107,8 @@ def test_nccl_sharding_one_rank_equals_single_gpu(c, sym):
     w_ref = w_ref.cpu().numpy()
     bp.geometry_shard_nccl(g, 0, 1, bp.nccl_unique_id(), symmetric=sym)
     u = bp.layer_apply(g, None, q).cpu().numpy()
-    w, _ = bp.lcp_mvp(g, lam, gmres=gm)
-    w2, _ = bp.lcp_mvp(g, lam, gmres=gm)
+    w, _ = bp.lcp_mvp(g, lam, gmres=gm)       # host-driven steps (first cycle on the handle)
+    w2, _ = bp.lcp_mvp(g, lam, gmres=gm)      # NCCL collectives inside the captured cycle graph
     assert np.linalg.norm(u - u_ref) / np.linalg.norm(u_ref) <= 1e-13
     assert np.linalg.norm(w.cpu().numpy() - w_ref) / np.linalg.norm(w_ref) <= 1e-10
     assert np.array_equal(w.cpu().numpy(), w2.cpu().numpy())
