@@ -18,7 +18,8 @@
 //    filled by one thread with TMA bulk copies (cp.async.bulk + mbarrier
 //    complete_tx); all threads read them back as broadcast 16-byte loads.
 //  * each thread owns K1_R targets in registers; a target block's partial sums are
-//    flushed with fp64 atomics when the CTA's range leaves the block (<= 2-3 per CTA).
+//    stored as partial sums when the CTA's range leaves the block (one segment per (CTA, block)),
+//    added in a fixed order by k_row_reduce (no floating-point atomics: bit-reproducible).
 //  * rho^-k from one MUFU.RSQ64H seed y (rsqrt.approx.ftz.f64) and the series
 //    (1-e)^(-k/2) = 1 + (k/2) e + (k/2)(k/2+1)/2 e^2, e = 1 - rho^2 y^2 (|e| <= 1.85e-6
 //    = 2^-19 measured, tools/rsq_micro.cu; truncation error < 7|e|^3 ~ 4e-17): rho^-5 costs
@@ -298,7 +299,7 @@ __global__ void __launch_bounds__(K1_THREADS, 2) k1_allpairs(K1Params P) {
 //    (l + k) mod 32 (lane-distinct, conflict-free LDS.128 from the TMA ring) and
 //    carries that source's accumulator, which rotates one lane per step by
 //    __shfl_sync; after 32 steps lane l holds source l's sum.  The 8 warps' sums
-//    are reduced through shared memory and added with one fp64 atomic per value.
+//    are reduced through shared memory and stored as the unit's source-side partial sums.
 //  * sources are points of spheres of radius a, so r.n_y = (h_m(x) - rho^2) / (2a) with
 //    h_m(x) = |x - c_m|^2 - a^2 per (target, source sphere): the forward r.n costs one FMA
 //    and the records carry no normals.  A 32-point source group spans at most two spheres

@@ -22,7 +22,8 @@ namespace bpqn {
 // sphere's nodes, weighted densities and coefficients in shared memory, and stream the
 // [6][nb] tensors from HBM once per application (16-byte streaming loads); the coarse
 // subtraction is recomputed from the staged nodes (~30 flops per pair, FP64 pipe).
-// One incidence per half-warp; each adds its 3 values to the target with fp64 atomics.
+// One incidence per half-warp; each stores its 3 values per incidence (k_row_reduce adds them per
+// target row in a fixed order).
 
 // coef[m][b][c] = sum_j A[b][j] sigma[m][j][c] (A row-major [nb][nq]); rows b in [nb, nbp) are zero.
 // A small tiled GEMM: block = 32 rows of A x 8 spheres; its 256 threads form 4 groups that take
