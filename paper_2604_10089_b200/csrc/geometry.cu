@@ -433,6 +433,260 @@ __global__ void __launch_bounds__(QT) k_quad_rows(QuadParams P) {
   }
 }
 
+// ------------------------------------------------------------------ near tensors by rotation
+// The same refined near rule (R8) as k_quad_rows kind 1, evaluated in the frame F = [e1 e2 d]
+// whose third axis d points from the source centre c_m to the target (the SH-
+// rotation idea behind the "FFT-based acceleration of near-evaluation" of P:425):
+//   * in that frame the target sits on the axis, x' = (0, 0, r'), and every kernel component
+//     K'_ef(x', y'(theta', phi')) is a trigonometric polynomial of degree <= 2 in phi';
+//   * the rule's 4p equispaced phi' nodes integrate (kernel) x (a degree-p SH) exactly, so only
+//     the rotated basis functions with |m'| <= 2 see the kernel:  with the frame-rotated
+//     coefficients D_b(m') of Y_b (Y_b(F eta') = sum_b' D_bb' Y_b'(eta'), b' of the same degree n),
+//        T[b] = F M[b] F^T,   M_xx = D0 A_n + D2c B_n,  M_yy = D0 A_n - D2c B_n,  M_zz = D0 Z_n,
+//                             M_xy = D2s B_n,  M_xz = D1c X_n,  M_yz = D1s X_n,
+//     where A, Z, X, B are the theta'-rule integrals of the axisymmetric kernel factors times the
+//     associated Legendre parts of degree n and order 0, 0, 1, 2 (4 (p+1) numbers per kernel);
+//   * D_b(m') for |m'| <= 2 are read off second-order jets of the solid harmonic r^n Y_b at d
+//     along e1, e2: value -> m' = 0, gradient -> m' = 1, traceless Hessian -> m' = 2 (every other
+//     rotated mode vanishes to that order at the pole), divided by the same jets of the
+//     reference functions at the pole (den[n][5], host).
+// Cost O(p^2 + p n_theta) per incidence instead of the O(p^2 n_theta n_phi) of k_quad_rows (c4:
+// 1.2 s -> milliseconds per geometry update); the values agree with k_quad_rows to rounding
+// (GPU test) whenever n_phi > p + 2 (exactness of the phi' rule, checked by the caller).
+struct Jet {  // second-order Taylor coefficients in (t1, t2): c0 + c1 t1 + c2 t2 + c11 t1^2 + c12 t1 t2 + c22 t2^2
+  double c0, c1, c2, c11, c12, c22;
+};
+__host__ __device__ inline Jet jmul(const Jet& a, const Jet& b) {
+  return Jet{a.c0 * b.c0,
+             a.c0 * b.c1 + a.c1 * b.c0,
+             a.c0 * b.c2 + a.c2 * b.c0,
+             a.c0 * b.c11 + a.c1 * b.c1 + a.c11 * b.c0,
+             a.c0 * b.c12 + a.c1 * b.c2 + a.c2 * b.c1 + a.c12 * b.c0,
+             a.c0 * b.c22 + a.c2 * b.c2 + a.c22 * b.c0};
+}
+__host__ __device__ inline Jet jlin(const Jet& a, const Jet& l) {  // l linear (l.c11 = l.c12 = l.c22 = 0)
+  return Jet{a.c0 * l.c0,
+             a.c0 * l.c1 + a.c1 * l.c0,
+             a.c0 * l.c2 + a.c2 * l.c0,
+             a.c1 * l.c1 + a.c11 * l.c0,
+             a.c1 * l.c2 + a.c2 * l.c1 + a.c12 * l.c0,
+             a.c2 * l.c2 + a.c22 * l.c0};
+}
+__host__ __device__ inline Jet jaxpy(double s, const Jet& a, const Jet& b) {  // s a + b
+  return Jet{fma(s, a.c0, b.c0), fma(s, a.c1, b.c1), fma(s, a.c2, b.c2),
+             fma(s, a.c11, b.c11), fma(s, a.c12, b.c12), fma(s, a.c22, b.c22)};
+}
+__host__ __device__ inline Jet jscale(double s, const Jet& a) {
+  return Jet{s * a.c0, s * a.c1, s * a.c2, s * a.c11, s * a.c12, s * a.c22};
+}
+
+// Jets of the solid harmonics of order m (cos and sin type, degrees l = m..lmax) at d along e1, e2
+// (|d| = 1, e1, e2 orthonormal and orthogonal to d, so r^2 = 1 + t1^2 + t2^2); calls
+// emit(l, jet_cos, jet_sin) for each l.  Same recurrences and normalisation as sh_column.
+template <class Emit>
+__host__ __device__ inline void solid_jets(int p, int lmax, int m, const double d[3], const double e1[3],
+                                           const double e2[3], const double* ra, const double* rb,
+                                           const double* cm, Emit emit) {
+  const Jet X{d[0], e1[0], e2[0], 0, 0, 0}, Y{d[1], e1[1], e2[1], 0, 0, 0}, Z{d[2], e1[2], e2[2], 0, 0, 0};
+  Jet re{1, 0, 0, 0, 0, 0}, im{0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < m; ++k) {  // (x + i y)^m
+    const Jet a = jlin(re, X), b = jlin(im, Y), c = jlin(re, Y), e = jlin(im, X);
+    re = jaxpy(-1.0, b, a);
+    im = jaxpy(1.0, e, c);
+  }
+  const double s2 = 1.4142135623730951;
+  const Jet cc = (m == 0) ? jscale(cm[0], re) : jscale(s2 * cm[m], re);
+  const Jet ss = jscale(s2 * cm[m], im);
+  Jet sm2{0, 0, 0, 0, 0, 0}, sm1{0, 0, 0, 0, 0, 0};
+  for (int l = m; l <= lmax; ++l) {
+    Jet s;
+    if (l == m) {
+      s = Jet{1, 0, 0, 0, 0, 0};
+    } else if (l == m + 1) {
+      s = jscale(ra[l * (p + 1) + m], jlin(sm1, Z));
+    } else {  // r^(l-m) R_lm = a (z r^(l-1-m) R_{l-1,m} - b r^2 r^(l-2-m) R_{l-2,m})
+      const Jet zs = jlin(sm1, Z);
+      const Jet r2s{sm2.c0, sm2.c1, sm2.c2, sm2.c11 + sm2.c0, sm2.c12, sm2.c22 + sm2.c0};
+      s = jscale(ra[l * (p + 1) + m], jaxpy(-rb[l * (p + 1) + m], r2s, zs));
+    }
+    sm2 = sm1;
+    sm1 = s;
+    emit(l, jmul(cc, s), jmul(ss, s));
+  }
+}
+
+// den[n][5]: jets of the reference functions Y_n0, Y^c_n1, Y^s_n1, Y^c_n2, Y^s_n2 at the pole along x, y
+// (value, d/dt1, d/dt2, the t1^2 - t2^2 and t1 t2 coefficients); zero where n < m'.
+struct DenEmit {
+  double* den;
+  int m;
+  __host__ __device__ void operator()(int l, const Jet& jc, const Jet& js) const {
+    if (m == 0) den[5 * l] = jc.c0;
+    if (m == 1) { den[5 * l + 1] = jc.c1; den[5 * l + 2] = js.c2; }
+    if (m == 2) { den[5 * l + 3] = jc.c11 - jc.c22; den[5 * l + 4] = js.c12; }
+  }
+};
+static void rot_denominators(int p, const std::vector<double>& ra, const std::vector<double>& rb,
+                             const std::vector<double>& cm, std::vector<double>& den) {
+  den.assign(5 * (size_t)(p + 1), 0.0);
+  const double d[3] = {0, 0, 1}, e1[3] = {1, 0, 0}, e2[3] = {0, 1, 0};
+  for (int m = 0; m <= std::min(2, p); ++m)
+    solid_jets(p, p, m, d, e1, e2, ra.data(), rb.data(), cm.data(), DenEmit{den.data(), m});
+}
+
+struct RotParams {
+  int p, nb, nbp, n1, n2;
+  double a, mu, theta_c;
+  const double *gl1_t, *gl1_w, *gl2_t, *gl2_w;
+  const int *inc_t, *inc_m;
+  const double *X, *centers;
+  ShTables T;
+  const double* den;  // [p+1][5]
+  double *outS, *outD;  // [nprob][6][nbp]
+  int want_s;
+};
+
+constexpr int NR_T = 128;
+__global__ void __launch_bounds__(NR_T) k_near_rot(RotParams P) {
+  extern __shared__ double rs[];
+  const int p = P.p, nb = P.nb, nth = P.n1 + P.n2, pl = p + 1;
+  double* Lg = rs;                  // [3][p+1][nth] Legendre parts of order 0, 1, 2
+  double* fac = Lg + 3 * pl * nth;  // [8][nth] kernel factors x weights: S (A, Z, X, B), D (A, Z, X, B)
+  double* W = fac + 8 * nth;        // [8][p+1]
+  double* D5 = W + 8 * pl;          // [nb][5]
+  int* degb = reinterpret_cast<int*>(D5 + 5 * (size_t)nb);  // [nb]
+  __shared__ double F[9], rp, delta;
+  const int prob = blockIdx.x, tid = threadIdx.x;
+  if (tid == 0) {
+    const int i = P.inc_t[prob], m = P.inc_m[prob];
+    const double rx = P.X[3 * (size_t)i] - P.centers[3 * m], ry = P.X[3 * (size_t)i + 1] - P.centers[3 * m + 1],
+                 rz = P.X[3 * (size_t)i + 2] - P.centers[3 * m + 2];
+    const double r = sqrt(rx * rx + ry * ry + rz * rz);
+    // frame from d = r / |r| with atan2 (acos loses ~1e-8 rad next to the poles)
+    const double te = atan2(sqrt(rx * rx + ry * ry), rz), pe = atan2(ry, rx);
+    const double ct = cos(te), st = sin(te), cp = cos(pe), sp = sin(pe);
+    F[0] = cp * ct; F[1] = -sp; F[2] = cp * st;  // row-major: columns e1, e2, d
+    F[3] = sp * ct; F[4] = cp;  F[5] = sp * st;
+    F[6] = -st;     F[7] = 0.0; F[8] = ct;
+    rp = r;
+    delta = (r - P.a) / P.a;
+  }
+  __syncthreads();
+  const double a = P.a, PI_ = PI;
+  const double cS = 1.0 / (8.0 * PI_ * P.mu), cD = -3.0 / (4.0 * PI_);
+  const double s2 = 1.4142135623730951;
+  for (int k = tid; k < nth; k += NR_T) {
+    double tt, ww;
+    if (k < P.n1) {  // sinh-graded panel [0, theta_c] (R8)
+      const double S = asinh(P.theta_c / delta);
+      const double s = 0.5 * S * (P.gl1_t[k] + 1.0);
+      tt = delta * sinh(s);
+      ww = 0.5 * S * P.gl1_w[k] * delta * cosh(s);
+    } else {
+      const int kk = k - P.n1;
+      tt = P.theta_c + 0.5 * (PI_ - P.theta_c) * (P.gl2_t[kk] + 1.0);
+      ww = 0.5 * (PI_ - P.theta_c) * P.gl2_w[kk];
+    }
+    const double s = sin(tt), c = cos(tt), sh = sin(0.5 * tt);
+    const double om = ww * s * a * a;
+    const double rz = (rp - a) + 2.0 * a * sh * sh;  // r' - a cos(theta') without cancellation
+    const double rho2 = a * a * s * s + rz * rz, ir = 1.0 / sqrt(rho2), ir2 = ir * ir, ir3 = ir * ir2;
+    // Legendre parts R_l,m(cos theta'), m = 0, 1, 2, times cm, sqrt2 cm sin^m
+    for (int m = 0; m <= 2; ++m) {
+      const double pref = (m == 0) ? P.T.cm[0] : (m == 1 ? s2 * P.T.cm[1] * s : s2 * P.T.cm[2] * s * s);
+      double rm2 = 0.0, rm1 = 0.0;
+      for (int l = 0; l <= p; ++l) {
+        double r = 0.0;
+        if (l >= m && m <= p) {
+          if (l == m) r = 1.0;
+          else if (l == m + 1) r = P.T.ra[l * pl + m] * c;
+          else r = P.T.ra[l * pl + m] * (c * rm1 - P.T.rb[l * pl + m] * rm2);
+          rm2 = rm1;
+          rm1 = r;
+        }
+        Lg[(m * pl + l) * nth + k] = pref * r;
+      }
+    }
+    const double tp = 2.0 * PI_ * om, op = PI_ * om;  // phi' integrals: 2 pi (m' = 0), pi (m' >= 1)
+    const double hs = 0.5 * a * a * s * s;
+    fac[0 * nth + k] = tp * cS * (ir + hs * ir3);
+    fac[1 * nth + k] = tp * cS * (ir + rz * rz * ir3);
+    fac[2 * nth + k] = -op * cS * a * s * rz * ir3;
+    fac[3 * nth + k] = op * cS * hs * ir3;
+    const double kdf = cD * (rp * c - a) * ir3 * ir2;  // r.n_y = r' cos(theta') - a
+    fac[4 * nth + k] = tp * kdf * hs;
+    fac[5 * nth + k] = tp * kdf * rz * rz;
+    fac[6 * nth + k] = -op * kdf * a * s * rz;
+    fac[7 * nth + k] = op * kdf * hs;
+  }
+  __syncthreads();
+  for (int e = tid; e < 8 * pl; e += NR_T) {  // W[q][l], theta' nodes summed in order
+    const int q = e / pl, l = e - q * pl;
+    const int mq = (q & 3) == 2 ? 1 : ((q & 3) == 3 ? 2 : 0);
+    const double* L = Lg + (mq * pl + l) * nth;
+    const double* f = fac + q * nth;
+    double acc = 0.0;
+    for (int k = 0; k < nth; ++k) acc = fma(f[k], L[k], acc);
+    W[e] = acc;
+  }
+  if (tid <= p) {  // one order m per thread: rotated coefficients D5[b][m'] from the jets
+    const int m = tid;
+    const double d[3] = {F[2], F[5], F[8]}, e1[3] = {F[0], F[3], F[6]}, e2[3] = {F[1], F[4], F[7]};
+    const double* den = P.den;
+    solid_jets(p, p, m, d, e1, e2, P.T.ra, P.T.rb, P.T.cm, [&](int l, const Jet& jc, const Jet& js) {
+      const double* dn = den + 5 * l;
+      const double i0 = 1.0 / dn[0], i1 = l >= 1 ? 1.0 / dn[1] : 0.0, i2 = l >= 1 ? 1.0 / dn[2] : 0.0,
+                   i3 = l >= 2 ? 1.0 / dn[3] : 0.0, i4 = l >= 2 ? 1.0 / dn[4] : 0.0;
+      const int bc = sh_cos_index(p, l, m);
+      double* o = D5 + 5 * bc;
+      o[0] = jc.c0 * i0; o[1] = jc.c1 * i1; o[2] = jc.c2 * i2; o[3] = (jc.c11 - jc.c22) * i3; o[4] = jc.c12 * i4;
+      degb[bc] = l;
+      if (m >= 1 && m < p) {
+        const int bs = sh_sin_index(p, l, m);
+        o = D5 + 5 * bs;
+        o[0] = js.c0 * i0; o[1] = js.c1 * i1; o[2] = js.c2 * i2; o[3] = (js.c11 - js.c22) * i3; o[4] = js.c12 * i4;
+        degb[bs] = l;
+      }
+    });
+  }
+  __syncthreads();
+  const int nbp = P.nbp;
+  const size_t o = (size_t)prob * 6 * nbp;
+  for (int b = tid; b < nbp; b += NR_T) {
+    double tS[6] = {0, 0, 0, 0, 0, 0}, tD[6] = {0, 0, 0, 0, 0, 0};
+    if (b < nb) {
+      const int l = degb[b];
+      const double* dv = D5 + 5 * b;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const double A = W[(4 * k) * pl + l], Zz = W[(4 * k + 1) * pl + l], Xx = W[(4 * k + 2) * pl + l],
+                     B = W[(4 * k + 3) * pl + l];
+        // M in the frame (symmetric), then T = F M F^T
+        const double Mxx = fma(dv[0], A, dv[3] * B), Myy = fma(dv[0], A, -dv[3] * B), Mzz = dv[0] * Zz;
+        const double Mxy = dv[4] * B, Mxz = dv[1] * Xx, Myz = dv[2] * Xx;
+        double G[3][3];  // G = M F^T: G[e][c] = sum_f M[e][f] F[c][f]
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double f0 = F[3 * c], f1 = F[3 * c + 1], f2 = F[3 * c + 2];
+          G[0][c] = Mxx * f0 + Mxy * f1 + Mxz * f2;
+          G[1][c] = Mxy * f0 + Myy * f1 + Myz * f2;
+          G[2][c] = Mxz * f0 + Myz * f1 + Mzz * f2;
+        }
+        double* t = k == 0 ? tS : tD;
+        const int ia[6] = {0, 0, 0, 1, 1, 2}, ic[6] = {0, 1, 2, 1, 2, 2};  // xx, xy, xz, yy, yz, zz
+#pragma unroll
+        for (int q = 0; q < 6; ++q)
+          t[q] = F[3 * ia[q]] * G[0][ic[q]] + F[3 * ia[q] + 1] * G[1][ic[q]] + F[3 * ia[q] + 2] * G[2][ic[q]];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 6; ++q) {
+      P.outD[o + (size_t)q * nbp + b] = tD[q];
+      if (P.want_s) P.outS[o + (size_t)q * nbp + b] = tS[q];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ self expansion
 // E_S[3i+a][3j+c] = (Rz(phi_l) Sring[k] Rz(phi_l)^T)[a][c] at j' = (k_j, l_j - l) - naive_S(i,j)
 // E_L likewise with Dring and naive_D; E_A = E_L - I/2 + Pi_R.
@@ -680,6 +934,38 @@ void precompute(Geom& g, cudaStream_t st, bool with_self) {
     if (g.single_layer) g.T_S.alloc((size_t)g.n_inc * per);
     P.kind = 1; P.inc_t = g.cm_t.p; P.inc_m = g.cm_m.p;
     P.want_s = g.single_layer ? 1 : 0;
+    // the rotation form needs an exact phi' rule for (kernel, degree <= 2) x (degree <= p)
+    const char* eb = getenv("BPQN_NEAR_BRUTE");
+    const bool rot = g.nphi > p + 2 && !(eb && eb[0] == '1');
+    if (rot) {
+      std::vector<double> den;
+      rot_denominators(p, ra, rb, cm, den);
+      DBuf<double> dden;
+      up(dden, den);
+      RotParams R{};
+      R.p = p; R.nb = nb; R.nbp = (nb + 1) & ~1; R.n1 = g.n1; R.n2 = g.n2;
+      R.a = g.a; R.mu = g.mu; R.theta_c = 1.0;
+      R.gl1_t = dt1.p; R.gl1_w = dw1.p; R.gl2_t = dt2.p; R.gl2_w = dw2.p;
+      R.X = g.X.p; R.centers = g.centers_d.p; R.T = T; R.den = dden.p;
+      R.want_s = P.want_s;
+      const int nth = g.n1 + g.n2;
+      const size_t rsm = (3 * (size_t)(p + 1) * nth + 8 * (size_t)nth + 8 * (size_t)(p + 1) + 5 * (size_t)nb) * 8 +
+                         4 * (size_t)nb;
+      BPQN_CUDA(cudaFuncSetAttribute(k_near_rot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));
+      const long long batch = 1 << 20;
+      for (long long b0 = 0; b0 < g.n_inc; b0 += batch) {
+        const long long nbt = std::min(batch, g.n_inc - b0);
+        RotParams Q = R;
+        Q.inc_t = g.cm_t.p + b0;
+        Q.inc_m = g.cm_m.p + b0;
+        Q.outD = g.T_D.p + b0 * per;
+        Q.outS = g.single_layer ? g.T_S.p + b0 * per : nullptr;
+        k_near_rot<<<(unsigned)nbt, NR_T, rsm, st>>>(Q);
+        BPQN_CHECK_LAUNCH();
+      }
+      BPQN_CUDA(cudaStreamSynchronize(st));  // dden is released at the end of this scope
+      return;
+    }
     // batch to keep grids modest
     const long long batch = 65535;
     for (long long b0 = 0; b0 < g.n_inc; b0 += batch) {

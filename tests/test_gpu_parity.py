@@ -795,3 +795,30 @@ def test_k1_launch_shapes_agree(bp, cfg):
         errs = [float(x) for x in line.split("{")[1].replace("'", "").replace("}", "").replace(",", "").split()
                 if x[0].isdigit()]
         assert len(errs) == 3 and max(errs) <= 1e-12, line
+
+
+@pytest.mark.parametrize("p,gap,axis", [(2, 0.05, "x"), (5, 1e-3, "z"), (8, 0.01, "rand"), (16, 0.02, "z"),
+                                        (16, 0.3, "rand"), (24, 0.004, "rand")])
+def test_near_rotation_equals_brute_force(bp, p, gap, axis):
+    """The rotation form of the near rule (k_near_rot: axisymmetric theta' integrals x second-order
+    jets of the rotated SH basis) equals the point-by-point refined rule (k_quad_rows, selected by
+    BPQN_NEAR_BRUTE=1) -- the same discrete operator, so S, D and S+D applies agree to rounding.
+    Targets next to the grid poles (axis z) exercise the frame construction."""
+    rng = np.random.default_rng(p)
+    e = {"x": np.array([1.0, 0, 0]), "z": np.array([0, 0, 1.0])}.get(axis)
+    if e is None:
+        e = rng.standard_normal(3)
+        e /= np.linalg.norm(e)
+    C = np.array([[0.1, -0.2, 0.3], [0.1, -0.2, 0.3] + (2.0 + gap) * e, [0.1, -0.2, 0.3] - (2.0 + 3 * gap) * e])
+    os.environ["BPQN_NEAR_BRUTE"] = "1"
+    try:
+        gb = bp.Geometry(C, p)
+    finally:
+        del os.environ["BPQN_NEAR_BRUTE"]
+    gr = bp.Geometry(C, p)
+    assert gr.n_incidences == gb.n_incidences > 0
+    f, q = rng.standard_normal((gr.N, 3)), rng.standard_normal((gr.N, 3))
+    for kw in (dict(f=T(f)), dict(q=T(q)), dict(f=T(f), q=T(q))):
+        ur = bp.layer_apply(gr, **kw).cpu().numpy()
+        ub = bp.layer_apply(gb, **kw).cpu().numpy()
+        assert rel(ur, ub) <= 1e-13, (list(kw), rel(ur, ub))
