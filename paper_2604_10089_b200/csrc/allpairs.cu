@@ -423,7 +423,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
         }
       } else {
         const double hm = MIXED ? (second ? h[r][1] : h[r][0]) : hu[r];
-        const double rn = fma(rr, -inv2a, hm);  // r . n_y on the source sphere
+        const double rn = MODE == MODE_D ? 0.0 : fma(rr, -inv2a, hm);  // r . n_y on the source sphere (S+D)
         const double rq = fma(r2, sc[QO + 2], fma(r1, sc[QO + 1], r0 * sc[QO]));
         double s, s3, s5;
         if (MODE == MODE_D) {
@@ -436,14 +436,17 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           s5 = s3 * s2;
         }
         if (MODE == MODE_D) {
-          const double tf = (rn * rq) * s5;
+          // D mode keeps r.n scaled by 2a (h, H unscaled; the 1/(2a) is folded into q~ by
+          // k1_pack_sym): 2a (r.n_y) rho^-5 = h s5 - rho^2 s5, one FMA per direction after the
+          // shared c3 = rho^2 s5 (30 FP64 instructions per unordered pair instead of 31)
+          const double c3 = rr * s5;
+          const double tf = fma(hm, s5, -c3) * rq;
           acc[r][0] = fma(r0, tf, acc[r][0]);
           acc[r][1] = fma(r1, tf, acc[r][1]);
           acc[r][2] = fma(r2, tf, acc[r][2]);
-          if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5, r.n_i = (rho^2 - H)/(2a)
-            const double rn2 = fma(rr, inv2a, -lds_f64(hb[r] + 8 * k));
+          if (SYM) {  // K_D(x_j, y_i) q_i = -(r.n_i)(r.q_i) r / rho^5, 2a r.n_i = rho^2 - H
             const double rq2 = fma(r2, K1_TGV(r, 5), fma(r1, K1_TGV(r, 4), r0 * K1_TGV(r, 3)));
-            const double tb = (rn2 * rq2) * s5;
+            const double tb = fma(-lds_f64(hb[r] + 8 * k), s5, c3) * rq2;
             as0 = fma(-r0, tb, as0);
             as1 = fma(-r1, tb, as1);
             as2 = fma(-r2, tb, as2);
@@ -521,6 +524,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     }
   }
   const double a = P.a, inv2a = 0.5 / P.a;
+  const double hsc = MODE == MODE_D ? 1.0 : inv2a;  // h, H scale (D mode: 2a r.n, see k1_group)
 
   double tg[R][TN], acc[R][3], hs[R][2];
   int slot[R];
@@ -566,7 +570,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
         const double* y = ring[buf] + j * REC;
         const double* c = cs + 3 * (fs + sl);
         const double d0 = y[0] - c[0], d1 = y[1] - c[1], d2 = y[2] - c[2];
-        const double H = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+        const double H = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * hsc;
         double* row = Hs + sl * (2 * K1_TS) + (j >> 5) * 64 + (j & 31);
         row[0] = H;
         row[32] = H;
@@ -590,7 +594,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
           for (int q = 0; q < 2; ++q) {
             const double* c = cs + 3 * (q ? m1 : m0);
             const double d0 = tg[r][0] - c[0], d1 = tg[r][1] - c[1], d2 = tg[r][2] - c[2];
-            hs[r][q] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * inv2a;
+            hs[r][q] = (fma(d2, d2, fma(d1, d1, d0 * d0)) - a * a) * hsc;
           }
         }
       }
@@ -966,7 +970,10 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
   BPQN_REQUIRE((size_t)npad * 14 <= g.packed.n, "K1 packed workspace too small (k1_reserve)");
   if (use_sym)
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
-                                                   1.0 / (8.0 * PI_A * g.mu), -3.0 / (4.0 * PI_A), g.packed.p);
+                                                   1.0 / (8.0 * PI_A * g.mu),
+                                                   // D mode: 1/(2a) folded into q~ (k1_group's 2a r.n)
+                                                   -3.0 / (4.0 * PI_A) / (mode == MODE_D ? 2.0 * g.a : 1.0),
+                                                   g.packed.p);
   else
     k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
                                                -3.0 / (4.0 * PI_A), g.packed.p);
