@@ -423,7 +423,6 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
         }
       } else {
         const double hm = MIXED ? (second ? h[r][1] : h[r][0]) : hu[r];
-        const double rn = MODE == MODE_D ? 0.0 : fma(rr, -inv2a, hm);  // r . n_y on the source sphere (S+D)
         const double rq = fma(r2, sc[QO + 2], fma(r1, sc[QO + 1], r0 * sc[QO]));
         double s, s3, s5;
         if (MODE == MODE_D) {
@@ -436,7 +435,7 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
           s5 = s3 * s2;
         }
         if (MODE == MODE_D) {
-          // D mode keeps r.n scaled by 2a (h, H unscaled; the 1/(2a) is folded into q~ by
+          // r.n kept scaled by 2a (h, H unscaled; the 1/(2a) is folded into q~ by
           // k1_pack_sym): 2a (r.n_y) rho^-5 = h s5 - rho^2 s5, one FMA per direction after the
           // shared c3 = rho^2 s5 (30 FP64 instructions per unordered pair instead of 31)
           const double c3 = rr * s5;
@@ -452,16 +451,16 @@ __device__ __forceinline__ void k1_group(const double* __restrict__ gr, const do
             as2 = fma(-r2, tb, as2);
           }
         } else {
+          // as D mode: 2a r.n rho^-5 = h s5 - rho^2 s5 with rho^2 s5 = s3 (to rounding), q~ / (2a)
           const double rf = fma(r2, sc[5], fma(r1, sc[4], r0 * sc[3]));
-          const double tf = fma(rf, s3, (rn * rq) * s5);
+          const double tf = fma(rf, s3, fma(hm, s5, -s3) * rq);
           acc[r][0] = fma(sc[3], s, fma(r0, tf, acc[r][0]));
           acc[r][1] = fma(sc[4], s, fma(r1, tf, acc[r][1]));
           acc[r][2] = fma(sc[5], s, fma(r2, tf, acc[r][2]));
           if (SYM) {
-            const double rn2 = fma(rr, inv2a, -lds_f64(hb[r] + 8 * k));
             const double rf2 = fma(r2, K1_TGV(r, 5), fma(r1, K1_TGV(r, 4), r0 * K1_TGV(r, 3)));
             const double rq2 = fma(r2, K1_TGV(r, 8), fma(r1, K1_TGV(r, 7), r0 * K1_TGV(r, 6)));
-            const double tb = fma(rf2, s3, -((rn2 * rq2) * s5));
+            const double tb = fma(rf2, s3, -(fma(-lds_f64(hb[r] + 8 * k), s5, s3) * rq2));
             as0 = fma(K1_TGV(r, 3), s, fma(r0, tb, as0));
             as1 = fma(K1_TGV(r, 4), s, fma(r1, tb, as1));
             as2 = fma(K1_TGV(r, 5), s, fma(r2, tb, as2));
@@ -524,7 +523,7 @@ __global__ void __launch_bounds__(32 * KS_W, MINB) k1_sym(K1SymParams P) {
     }
   }
   const double a = P.a, inv2a = 0.5 / P.a;
-  const double hsc = MODE == MODE_D ? 1.0 : inv2a;  // h, H scale (D mode: 2a r.n, see k1_group)
+  const double hsc = 1.0;  // h, H unscaled: k1_group keeps 2a r.n (the 1/(2a) is folded into q~)
 
   double tg[R][TN], acc[R][3], hs[R][2];
   int slot[R];
@@ -972,7 +971,7 @@ void launch_allpairs(Geom& g, int mode, const double* sigS, const double* sigD, 
     k1_pack_sym<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD,
                                                    1.0 / (8.0 * PI_A * g.mu),
                                                    // D mode: 1/(2a) folded into q~ (k1_group's 2a r.n)
-                                                   -3.0 / (4.0 * PI_A) / (mode == MODE_D ? 2.0 * g.a : 1.0),
+                                                   -3.0 / (4.0 * PI_A) / (mode == MODE_S ? 1.0 : 2.0 * g.a),
                                                    g.packed.p);
   else
     k1_pack<<<(npad + 255) / 256, 256, 0, st>>>(mode, g.n, npad, g.src.p, sigS, sigD, 1.0 / (8.0 * PI_A * g.mu),
