@@ -22,6 +22,7 @@ ap.add_argument("--p", type=int, default=8)
 ap.add_argument("--p-lo", type=int, default=4)
 ap.add_argument("--dt", type=float, default=1e-2)
 ap.add_argument("--lo-dense", type=int, default=2)   # R38: 2 = auto
+ap.add_argument("--recycle", type=int, default=1)    # GMRES recycling (R33) inside each step's solves (C default)
 a = ap.parse_args()
 cfg = make_config(4)
 C = np.ascontiguousarray(cfg["centers"].copy())
@@ -29,8 +30,8 @@ A = np.ascontiguousarray(cfg["axes"].copy())
 hi = bp.Geometry(C, a.p)
 lo = bp.Geometry(C, a.p_lo)
 o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=a.lo_dense)
-o.gm_hi = bp.default_gmres_opts(tol=1e-8)
-o.gm_lo = bp.default_gmres_opts(tol=1e-8)
+o.gm_hi = bp.default_gmres_opts(tol=1e-8, recycle=a.recycle)
+o.gm_lo = bp.default_gmres_opts(tol=1e-8, recycle=a.recycle)
 t0 = time.perf_counter()
 ms, gaps, bad = [], [], 0
 for k in range(a.steps):
@@ -38,8 +39,9 @@ for k in range(a.steps):
     ms.append(r.ms_total)
     gaps.append(r.min_gap_after)
     bad += rc != 0
-    print("step %3d rc %d contacts %3d active %3d hi %2d lo %3d min_gap %+.2e  %.0f ms" %
-          (k, rc, r.n_contacts, r.active_contacts, r.lcp.hi_mvps, r.lcp.lo_mvps, r.min_gap_after, r.ms_total),
+    print("step %3d rc %d contacts %3d active %3d hi %2d lo %3d GMRES its nc %3d c %3d min_gap %+.2e  %.0f ms" %
+          (k, rc, r.n_contacts, r.active_contacts, r.lcp.hi_mvps, r.lcp.lo_mvps, r.gm_nc.iters, r.gm_c.iters,
+           r.min_gap_after, r.ms_total),
           flush=True)
 wall = time.perf_counter() - t0
 print("steps %d  failed %d  mean %.0f ms/step  min gap over run %+.2e  wall %.1f s" %
