@@ -36,10 +36,12 @@ typedef int (*cublasCreate_t)(void**);
 typedef int (*cublasSetStream_t)(void*, cudaStream_t);
 typedef int (*cublasDgemm_t)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int,
                              const double*, double*, int);
+typedef int (*cublasDtrsm_t)(void*, int, int, int, int, int, int, const double*, const double*, int, double*, int);
 struct Cublas {
   cublasCreate_t create = nullptr;
   cublasSetStream_t setStream = nullptr;
   cublasDgemm_t dgemm = nullptr;
+  cublasDtrsm_t dtrsm = nullptr;
   std::string why;
 };
 // one cuBLAS handle per calling thread (distinct geometry handles may be used from different threads)
@@ -58,7 +60,8 @@ static Cublas& cublas() {
     c.create = reinterpret_cast<cublasCreate_t>(dlsym(h, "cublasCreate_v2"));
     c.setStream = reinterpret_cast<cublasSetStream_t>(dlsym(h, "cublasSetStream_v2"));
     c.dgemm = reinterpret_cast<cublasDgemm_t>(dlsym(h, "cublasDgemm_v2"));
-    if (!c.create || !c.setStream || !c.dgemm) c.why = "cuBLAS lacks a required symbol";
+    c.dtrsm = reinterpret_cast<cublasDtrsm_t>(dlsym(h, "cublasDtrsm_v2"));
+    if (!c.create || !c.setStream || !c.dgemm || !c.dtrsm) c.why = "cuBLAS lacks a required symbol";
   });
   if (!c.why.empty()) throw Error{BPQN_ERR_CUDA, c.why};
   return c;
@@ -79,6 +82,25 @@ static void gemm_rowA(cudaStream_t st, int m, int n, int k, const double* A_row,
   if (cb.setStream(h, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
   if (cb.dgemm(h, CUBLAS_OP_T_, CUBLAS_OP_N_, m, n, k, &one, A_row, k, B, ldb, &beta, C, ldc) != 0)
     throw Error{BPQN_ERR_CUDA, "cublasDgemm failed"};
+}
+
+// plain column-major DGEMM / DTRSM (cuBLAS conventions)
+static void dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double alpha, const double* A, int lda,
+                  const double* B, int ldb, double beta, double* C, int ldc) {
+  Cublas& cb = cublas();
+  void* h = cublas_handle();
+  if (cb.setStream(h, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
+  if (cb.dgemm(h, ta, tb, m, n, k, &alpha, A, lda, B, ldb, &beta, C, ldc) != 0)
+    throw Error{BPQN_ERR_CUDA, "cublasDgemm failed"};
+}
+constexpr int CB_LEFT = 0, CB_RIGHT = 1, CB_LOWER = 0, CB_NONUNIT = 0;
+static void dtrsm(cudaStream_t st, int side, int trans, int m, int n, const double* L, int ldl, double* B, int ldb) {
+  Cublas& cb = cublas();
+  void* h = cublas_handle();
+  const double one = 1.0;
+  if (cb.setStream(h, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
+  if (cb.dtrsm(h, side, CB_LOWER, trans, CB_NONUNIT, m, n, &one, L, ldl, B, ldb) != 0)
+    throw Error{BPQN_ERR_CUDA, "cublasDtrsm failed"};
 }
 
 // ---------------------------------------------------------------- dense operator assembly
@@ -303,10 +325,254 @@ __global__ void k_col_norms(const double* b, int n, double* out) {
   if (threadIdx.x == 0) out[blockIdx.x] = s;
 }
 
+
+// ---------------------------------------------------------------- block GMRES (one Krylov space for all columns)
+// Lower Cholesky of a column-major n x n SPD block (n <= 64) in shared memory, one CTA; a pivot below
+// 1e-28 x the block's largest diagonal entry is clamped there (a rank-deficient block carries no residual).
+constexpr int POTRF_NB = 64;
+__global__ void __launch_bounds__(256) k_potrf_small(double* A, int n, int lda) {
+  __shared__ double a[POTRF_NB][POTRF_NB + 1];
+  __shared__ double dmax, dinv;
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) a[e / n][e % n] = A[(size_t)(e / n) * lda + e % n];  // a[col][row]
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double mx = 0.0;
+    for (int j = 0; j < n; ++j) mx = fmax(mx, a[j][j]);
+    dmax = mx;
+  }
+  __syncthreads();
+  for (int j = 0; j < n; ++j) {
+    if (threadIdx.x == 0) {
+      const double d = sqrt(fmax(a[j][j], 1e-28 * dmax + 1e-300));
+      a[j][j] = d;
+      dinv = 1.0 / d;
+    }
+    __syncthreads();
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x) a[j][i] *= dinv;
+    __syncthreads();
+    const int m = n - j - 1;
+    for (int e = threadIdx.x; e < m * m; e += blockDim.x) {
+      const int i = j + 1 + e % m, l = j + 1 + e / m;
+      if (i >= l) a[l][i] -= a[j][i] * a[j][l];
+    }
+    __syncthreads();
+  }
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    const int l = e / n, i = e % n;
+    A[(size_t)l * lda + i] = i >= l ? a[l][i] : 0.0;
+  }
+}
+
+// C[rows x cols] (ldc) = B (ldb)
+__global__ void k_copy_block(double* C, int ldc, const double* B, int ldb, int rows, int cols) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int i = e % rows, j = e / rows;
+    C[(size_t)j * ldc + i] = B[(size_t)j * ldb + i];
+  }
+}
+
+__global__ void k_zero_upper(double* A, int n, int lda) {
+  for (size_t e = (size_t)blockIdx.x * blockDim.x + threadIdx.x; e < (size_t)n * n; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % n), l = (int)(e / n);
+    if (i < l) A[(size_t)l * lda + i] = 0.0;
+  }
+}
+
+static int grid_for(size_t work) { return (int)std::max<size_t>(1, std::min<size_t>((work + 255) / 256, 4096)); }
+
+// Blocked right-looking Cholesky A = L L^T (column-major, lower, the strict upper triangle zeroed): panels of 64 in shared memory, the
+// panel below by DTRSM and the trailing update by DGEMM (cuBLAS).
+static void potrf(cudaStream_t st, double* A, int n, int lda) {
+  for (int j = 0; j < n; j += POTRF_NB) {
+    const int jb = std::min(POTRF_NB, n - j);
+    double* Ajj = A + (size_t)j * lda + j;
+    k_potrf_small<<<1, 256, 0, st>>>(Ajj, jb, lda);
+    BPQN_CHECK_LAUNCH();
+    const int r = n - j - jb;
+    if (r > 0) {
+      double* P = Ajj + jb;  // rows j+jb.., columns j..j+jb
+      dtrsm(st, CB_RIGHT, CUBLAS_OP_T_, r, jb, Ajj, lda, P, lda);
+      dgemm(st, CUBLAS_OP_N_, CUBLAS_OP_T_, r, r, jb, -1.0, P, lda, P, lda, 1.0, Ajj + (size_t)jb * lda + jb, lda);
+    }
+  }
+  k_zero_upper<<<grid_for((size_t)n * n), 256, 0, st>>>(A, n, lda);
+  BPQN_CHECK_LAUNCH();
+}
+
+// C[rows x cols] (ldc) += B[rows x cols] (ldb)
+__global__ void k_add_block(double* C, int ldc, const double* B, int ldb, int rows, int cols) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int i = e % rows, j = e / rows;
+    C[(size_t)j * ldc + i] += B[(size_t)j * ldb + i];
+  }
+}
+
+// C[rows x cols] (ldc) = B^T, B [cols x rows] (ldb)
+__global__ void k_transpose_block(double* C, int ldc, const double* B, int ldb, int rows, int cols) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < rows * cols; e += gridDim.x * blockDim.x) {
+    const int i = e % rows, j = e / rows;
+    C[(size_t)j * ldc + i] = B[(size_t)i * ldb + j];
+  }
+}
+
+// column norms of a column-major [n x cols] block (ld) relative to bnorm: out[c] = |X[:, c]| / bnorm[c]
+__global__ void k_col_rel_norms(const double* X, int n, int ld, const double* bnorm, double* out) {
+  __shared__ double sred[32];
+  const double* xc = X + (size_t)blockIdx.x * ld;
+  double s = 0.0;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) s = fma(xc[e], xc[e], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) sred[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += sred[w];
+    const double bn = bnorm[blockIdx.x];
+    out[blockIdx.x] = bn > 0.0 ? sqrt(t) / bn : 0.0;
+  }
+}
+
 // ---------------------------------------------------------------- driver
+// Right-preconditioned block GMRES for all R columns at once (one Krylov space of dimension R per block
+// iteration; the columns share the operator's slow modes, so far fewer operator applications than R
+// independent GMRES processes: c4 lo 23 block iterations against 42, tools/block_gmres_study.py):
+//   * block Arnoldi with block CGS2 (DGEMM) and Cholesky-QR2 of each new block (blocked Cholesky in
+//     shared memory + DTRSM/DGEMM), so V_{k+1} H_{k+1,k} = W with H_{k+1,k} upper triangular;
+//   * the least-squares problem min |E1 S0 - Hbar Y| of every column by the normal equations of Hbar,
+//     whose Cholesky factor grows by one block row per iteration (DTRSM + a 64-panel Cholesky), with one
+//     step of refinement from the explicit residual (corrected semi-normal equations);
+//   * every column's explicit LS residual relative to its |b| decides convergence; restarted every kmax
+//     block iterations from the true residual b - A x.
+// X (x0 = 0 on entry) receives M^-1 V Y, the density of each column.
+static int block_gmres(Geom& g, const double* A, const double* B, const double* BN, double* X, int R, size_t n,
+                       int kmax, double tol, int max_blocks, cudaStream_t st, long long& col_iters) {
+  const int s = R, M3 = 3 * g.nq;
+  const int ldH = (kmax + 1) * s, ldL = kmax * s;
+  DBuf<double> V, H, L, F, Y, Y2, Res, Tb, Gs, G2, Z, Wt, S0, RES;
+  V.alloc((size_t)(kmax + 1) * s * n);
+  H.alloc((size_t)ldH * ldL);
+  L.alloc((size_t)ldL * ldL);
+  F.alloc((size_t)ldL * s);
+  Y.alloc((size_t)ldL * s);
+  Y2.alloc((size_t)ldL * s);
+  Res.alloc((size_t)ldH * s);
+  Tb.alloc((size_t)ldH * s);
+  Gs.alloc((size_t)s * s);
+  G2.alloc((size_t)s * s);
+  Z.alloc((size_t)s * n);
+  Wt.alloc((size_t)s * n);
+  S0.alloc((size_t)s * s);
+  RES.alloc(s);
+  const int T_ = CUBLAS_OP_T_, N_ = CUBLAS_OP_N_;
+  // W = Q R with Q overwriting W, R = (L1 L2)^T upper (ld ldr)
+  auto cholqr2 = [&](double* W, double* Rout, int ldr) {
+    dgemm(st, T_, N_, s, s, (int)n, 1.0, W, (int)n, W, (int)n, 0.0, Gs.p, s);
+    potrf(st, Gs.p, s, s);
+    dtrsm(st, CB_RIGHT, T_, (int)n, s, Gs.p, s, W, (int)n);
+    dgemm(st, T_, N_, s, s, (int)n, 1.0, W, (int)n, W, (int)n, 0.0, G2.p, s);
+    potrf(st, G2.p, s, s);
+    dtrsm(st, CB_RIGHT, T_, (int)n, s, G2.p, s, W, (int)n);
+    dgemm(st, T_, T_, s, s, s, 1.0, G2.p, s, Gs.p, s, 0.0, Rout, ldr);  // L2^T L1^T
+  };
+  // Res = E1 S0 - Hbar[0:kk+s, 0:kk] Y  (ld ldH)
+  auto residual = [&](int kk, const double* Yp) {
+    BPQN_CUDA(cudaMemsetAsync(Res.p, 0, 8 * (size_t)ldH * s, st));
+    k_copy_block<<<grid_for((size_t)s * s), 256, 0, st>>>(Res.p, ldH, S0.p, s, s, s);
+    BPQN_CHECK_LAUNCH();
+    dgemm(st, N_, N_, kk + s, s, kk, -1.0, H.p, ldH, Yp, ldL, 1.0, Res.p, ldH);
+  };
+  auto cholsolve = [&](int kk, double* Yp) {  // Yp <- (L L^T)^-1 Yp on the leading kk rows
+    dtrsm(st, CB_LEFT, N_, kk, s, L.p, ldL, Yp, ldL);
+    dtrsm(st, CB_LEFT, T_, kk, s, L.p, ldL, Yp, ldL);
+  };
+  std::vector<double> res(s);
+  int total = 0;
+  bool first = true;
+  for (;;) {
+    double* V0 = V.p;
+    if (first) {
+      BPQN_CUDA(cudaMemcpyAsync(V0, B, 8 * (size_t)s * n, cudaMemcpyDeviceToDevice, st));
+    } else {  // restart from the true residual b - A_op x
+      gemm_rowA(st, (int)n, s, (int)n, A, X, (int)n, Wt.p, (int)n);
+      k_sub_cols<<<grid_for((size_t)s * n), 256, 0, st>>>(V0, B, Wt.p, (size_t)s * n);
+      BPQN_CHECK_LAUNCH();
+    }
+    first = false;
+    cholqr2(V0, S0.p, s);
+    BPQN_CUDA(cudaMemsetAsync(H.p, 0, 8 * (size_t)ldH * ldL, st));
+    bool done = false;
+    for (int k = 0; k < kmax; ++k) {
+      double* Vk = V.p + (size_t)k * s * n;
+      double* Vn = Vk + (size_t)s * n;
+      double* Hk = H.p + (size_t)k * s * ldH;
+      const int kk = (k + 1) * s;
+      // W = A_op M^-1 V_k (block-Jacobi GEMM over all spheres of all columns, then the dense operator)
+      gemm_rowA(st, M3, g.np * s, M3, g.Minv.p, Vk, M3, Z.p, M3);
+      gemm_rowA(st, (int)n, s, (int)n, A, Z.p, (int)n, Vn, (int)n);
+      // block CGS2 against V_0..V_k
+      dgemm(st, T_, N_, kk, s, (int)n, 1.0, V.p, (int)n, Vn, (int)n, 0.0, Hk, ldH);
+      dgemm(st, N_, N_, (int)n, s, kk, -1.0, V.p, (int)n, Hk, ldH, 1.0, Vn, (int)n);
+      dgemm(st, T_, N_, kk, s, (int)n, 1.0, V.p, (int)n, Vn, (int)n, 0.0, Tb.p, kk);
+      dgemm(st, N_, N_, (int)n, s, kk, -1.0, V.p, (int)n, Tb.p, kk, 1.0, Vn, (int)n);
+      k_add_block<<<grid_for((size_t)kk * s), 256, 0, st>>>(Hk, ldH, Tb.p, kk, kk, s);
+      BPQN_CHECK_LAUNCH();
+      cholqr2(Vn, Hk + kk, ldH);  // H_{k+1,k}
+      // normal equations: new block column of Hbar^T Hbar, then block row k of its Cholesky factor
+      dgemm(st, T_, N_, kk, s, kk + s, 1.0, H.p, ldH, Hk, ldH, 0.0, Tb.p, kk);
+      double* Lkk = L.p + (size_t)k * s * ldL + (size_t)k * s;
+      if (k > 0) {
+        dtrsm(st, CB_LEFT, N_, k * s, s, L.p, ldL, Tb.p, kk);                           // X = L^-1 G[0:ks, k]
+        dgemm(st, T_, N_, s, s, k * s, -1.0, Tb.p, kk, Tb.p, kk, 1.0, Tb.p + (size_t)k * s, kk);  // G_kk - X^T X
+        k_transpose_block<<<grid_for((size_t)s * k * s), 256, 0, st>>>(L.p + (size_t)k * s, ldL, Tb.p, kk, s, k * s);
+        BPQN_CHECK_LAUNCH();
+      }
+      k_copy_block<<<grid_for((size_t)s * s), 256, 0, st>>>(Lkk, ldL, Tb.p + (size_t)k * s, kk, s, s);
+      BPQN_CHECK_LAUNCH();
+      potrf(st, Lkk, s, ldL);
+      // F block k = Hbar[0:s, block k]^T S0 (E1 S0 is zero below the first block row)
+      dgemm(st, T_, N_, s, s, s, 1.0, Hk, ldH, S0.p, s, 0.0, F.p + (size_t)k * s, ldL);
+      // Y = (L L^T)^-1 F, one refinement step from the explicit residual
+      k_copy_block<<<grid_for((size_t)kk * s), 256, 0, st>>>(Y.p, ldL, F.p, ldL, kk, s);
+      BPQN_CHECK_LAUNCH();
+      cholsolve(kk, Y.p);
+      residual(kk, Y.p);
+      dgemm(st, T_, N_, kk, s, kk + s, 1.0, H.p, ldH, Res.p, ldH, 0.0, Y2.p, ldL);
+      cholsolve(kk, Y2.p);
+      k_add_block<<<grid_for((size_t)kk * s), 256, 0, st>>>(Y.p, ldL, Y2.p, ldL, kk, s);
+      BPQN_CHECK_LAUNCH();
+      residual(kk, Y.p);
+      k_col_rel_norms<<<s, 256, 0, st>>>(Res.p, kk + s, ldH, BN, RES.p);
+      BPQN_CHECK_LAUNCH();
+      BPQN_CUDA(cudaMemcpyAsync(res.data(), RES.p, 8 * (size_t)s, cudaMemcpyDeviceToHost, st));
+      BPQN_CUDA(cudaStreamSynchronize(st));
+      ++total;
+      col_iters += s;
+      double worst = 0.0;
+      for (double v : res) {
+        if (!std::isfinite(v)) throw Error{BPQN_ERR_NAN, "NaN in the block low-fidelity GMRES"};
+        worst = std::max(worst, v);
+      }
+      done = worst <= tol;
+      if (done || k + 1 == kmax || total >= max_blocks) {  // x += M^-1 V_{0..k} Y
+        dgemm(st, N_, N_, (int)n, s, kk, 1.0, V.p, (int)n, Y.p, ldL, 0.0, Wt.p, (int)n);
+        gemm_rowA(st, M3, g.np * s, M3, g.Minv.p, Wt.p, M3, X, M3, 1.0);
+        break;
+      }
+    }
+    if (done) return total;
+    if (total >= max_blocks) throw Error{BPQN_ERR_NOCONV, "block low-fidelity GMRES did not converge"};
+  }
+}
+
 size_t dense_lo_bytes(const Geom& g, int m) {
   const size_t n = 3 * (size_t)g.n, R = (size_t)std::max(g.nc, 1);
   return 8 * (n * n + (size_t)(m + 1) * R * n + 4 * R * n);
+}
+// block GMRES with kmax block iterations per cycle: operator, V, Hbar, L, and the [n x R] buffers
+static size_t dense_lo_block_bytes(const Geom& g, int kmax) {
+  const size_t n = 3 * (size_t)g.n, R = (size_t)std::max(g.nc, 1), K = (size_t)kmax;
+  return 8 * (n * n + (K + 1) * R * n + (K + 1) * R * K * R + K * R * K * R + 6 * R * n + 6 * K * R * R);
 }
 
 int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, DenseLoStats& stt, cudaStream_t st) {
@@ -316,28 +582,31 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   BPQN_REQUIRE(R > 0, "no contacts installed");
   BPQN_REQUIRE(N <= 65535 && !g.sharded(), "dense low fidelity: N <= 65535 nodes, unsharded handle");
   BPQN_REQUIRE(g.Minv.p && g.E_A.p, "geometry has no self operators");
-  int m = std::max(4, std::min(o.restart, GM_BATCH_MAX_M));
   size_t fr = 0, tot = 0;
   BPQN_CUDA(cudaMemGetInfo(&fr, &tot));
-  while (m > 8 && dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr) m /= 2;
-  if (dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr)
-    throw Error{BPQN_ERR_OOM, "dense low-fidelity operator does not fit in device memory"};
+  // block GMRES (default) or the batched per-column GMRES (BPQN_LO_BATCHED=1)
+  const char* eb = getenv("BPQN_LO_BATCHED");
+  const bool blockmode = !(eb && eb[0] == '1');
+  int m = std::max(4, std::min(o.restart, GM_BATCH_MAX_M));
+  int kmax = std::max(2, std::min(40, (int)(n / std::max(R, 1)) - 1));
+  if (blockmode) {
+    while (kmax > 4 && dense_lo_block_bytes(g, kmax) + ((size_t)1 << 30) > fr) kmax -= 4;
+    if (dense_lo_block_bytes(g, kmax) + ((size_t)1 << 30) > fr)
+      throw Error{BPQN_ERR_OOM, "dense low-fidelity operator does not fit in device memory"};
+  } else {
+    while (m > 8 && dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr) m /= 2;
+    if (dense_lo_bytes(g, m) + ((size_t)1 << 30) > fr)
+      throw Error{BPQN_ERR_OOM, "dense low-fidelity operator does not fit in device memory"};
+  }
   cublas_handle();  // fail early if cuBLAS is missing
   DBuf<double> A, V, B, Wb, X, Z, G, sm;
   DBuf<int> didx, dkk;
   A.alloc(n * n);
-  G.alloc((size_t)R * n);
-  didx.alloc(R);
-  dkk.alloc(R);
-  V.alloc((size_t)(m + 1) * R * n);
   B.alloc((size_t)R * n);
-  Wb.alloc((size_t)R * n);
   X.alloc((size_t)R * n);
-  Z.alloc((size_t)R * n);
-  const size_t hs = (size_t)R * (m + 1) * m, cs = (size_t)R * m, gs = (size_t)R * (m + 1);
-  sm.alloc(hs + 3 * cs + gs + 4 * (size_t)R);
-  double *H = sm.p, *CS = H + hs, *SN = CS + cs, *Y = SN + cs, *GV = Y + cs, *BETA = GV + gs, *RES = BETA + R,
-         *BN = RES + R;
+  DBuf<double> bn_blk;
+  bn_blk.alloc(R);
+  double* BN = bn_blk.p;
   // 1. assemble A_op (coarse -> near rows replace -> self blocks add)
   assemble_dense_operator(g, A.p, st);
   // 2. right-hand sides b_l = -S[P^T D e_l]
@@ -359,8 +628,23 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   k_col_norms<<<R, 512, 0, st>>>(B.p, (int)n, BN);
   BPQN_CHECK_LAUNCH();
   const auto t1 = std::chrono::steady_clock::now();
-  // 3. batched right-preconditioned GMRES(m), x0 = 0
   BPQN_CUDA(cudaMemsetAsync(X.p, 0, 8 * (size_t)R * n, st));
+  int iters = 0;
+  long long col_iters = 0;
+  if (blockmode) {
+    iters = block_gmres(g, A.p, B.p, BN, X.p, R, n, kmax, o.tol, std::max(1, o.max_iters), st, col_iters);
+    m = kmax;
+  } else {
+  G.alloc((size_t)R * n);
+  didx.alloc(R);
+  dkk.alloc(R);
+  V.alloc((size_t)(m + 1) * R * n);
+  Wb.alloc((size_t)R * n);
+  Z.alloc((size_t)R * n);
+  const size_t hs = (size_t)R * (m + 1) * m, cs = (size_t)R * m, gs = (size_t)R * (m + 1);
+  sm.alloc(hs + 3 * cs + gs + 3 * (size_t)R);
+  double *H = sm.p, *CS = H + hs, *SN = CS + cs, *Y = SN + cs, *GV = Y + cs, *BETA = GV + gs, *RES = BETA + R;
+  // 3. batched right-preconditioned GMRES(m), x0 = 0
   const int M3 = 3 * nq;
   auto apply_op = [&](const double* in, int ncol, double* out) {  // out = A_op Minv in (ncol columns)
     gemm_rowA(st, M3, g.np * ncol, M3, g.Minv.p, in, M3, Z.p, M3);
@@ -368,9 +652,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   };
   std::vector<double> res(R);
   std::vector<int> active, kkc(R);
-  int iters = 0;
   bool first = true, done = false;
-  long long col_iters = 0;
   while (!done) {
     const double* r0 = B.p;
     if (!first) {  // restart: r = b - A x  (x holds the solution so far, already M^-1 applied)
@@ -422,6 +704,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
     BPQN_CHECK_LAUNCH();
     gemm_rowA(st, M3, g.np * R, M3, g.Minv.p, Wb.p, M3, X.p, M3, 1.0);
   }
+  }  // batched
   // 4. A^ e_l = D^T (-Pi[q_l])
   DBuf<double> Ad;
   Ad.alloc((size_t)R * R);
@@ -442,7 +725,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   stt.restart = m;
   stt.ms_rhs = std::chrono::duration<double, std::milli>(t1 - t0).count();
   stt.ms_total = std::chrono::duration<double, std::milli>(t2 - t0).count();
-  stt.bytes = dense_lo_bytes(g, m);
+  stt.bytes = blockmode ? dense_lo_block_bytes(g, kmax) : dense_lo_bytes(g, m);
   return BPQN_OK;
 }
 

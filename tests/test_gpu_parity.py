@@ -759,6 +759,27 @@ def test_lcp_matrix_dense_equals_mvps(bp, c, p):
         assert rel(A, fixture(1)["A_dense"]) <= TOL_VEL
 
 
+@pytest.mark.parametrize("c,p", [(1, 8), (2, 6)])
+def test_lcp_matrix_dense_block_equals_batched(bp, c, p):
+    """The block GMRES that forms A^ by default (one Krylov space for all Nc columns, normal equations of
+    the block Hessenberg with one refinement step) equals the batched per-column GMRES
+    (BPQN_LO_BATCHED=1) to the GMRES tolerance, in fewer operator applications."""
+    from synth import make_config
+    cfg = make_config(c)
+    g = bp.Geometry(cfg["centers"], p)
+    bp.contacts(g, cfg["delta"])
+    for tol in (1e-6, 1e-12):
+        gm = bp.default_gmres_opts(tol=tol)
+        Ab, stb = bp.lcp_matrix_dense(g, gmres=gm)
+        os.environ["BPQN_LO_BATCHED"] = "1"
+        try:
+            Aa, sta = bp.lcp_matrix_dense(g, gmres=gm)
+        finally:
+            del os.environ["BPQN_LO_BATCHED"]
+        assert rel(Ab, Aa) <= 100 * tol, (tol, rel(Ab, Aa))
+        assert stb.iters < sta.iters, (stb.iters, sta.iters)
+
+
 def test_solve_lcp_bi_dense_lo_c2(bp):
     """Bi-PQN with the low-fidelity LCP matrix formed once (lo_dense = 1, R38) reaches the oracle's
     lambda* at c2 (<= 1e-7) with the oracle-A complementarity (R26) <= 1e-8; every low-fidelity MVP
