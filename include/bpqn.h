@@ -108,7 +108,7 @@ typedef struct {
                                  secant pairs (reading R34) with extra, uncounted lo MVPs;
                                  reported in bpqn_report.secant_residual */
   int lo_dense;               /* Bi-PQN: 1 = form the low-fidelity LCP matrix A^ = D^T M_lo D once per solve
-                                 (all Nc mobility solves as one batched GMRES on the dense completed
+                                 (all Nc mobility solves as one block GMRES on the dense completed
                                  double-layer operator of `lo`, FP64 GEMMs on the tensor cores; gm_lo's
                                  tolerance per column; R38) and apply it as an Nc x Nc product for
                                  every low-fidelity MVP; falls back to matrix-free lo MVPs if the dense
@@ -194,11 +194,12 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
                    const bpqn_solve_opts* o, bpqn_report* rep, void* stream);
 
 /* The whole LCP matrix A = D^T M D of the handle's contact set, row-major [Nc][Nc] into A_host:
- * all Nc mobility solves as one batched right-preconditioned GMRES on the dense completed double-layer
+ * all Nc mobility solves as one right-preconditioned block GMRES on the dense completed double-layer
  * operator (8 (3N)^2 bytes of device memory, FP64 GEMMs; gm's tolerance per column).  This is how
  * bpqn_solve_opts.lo_dense forms the low-fidelity A^ (R38); the paper analyses dense A / A^ offline
  * (Fig. 3).  BPQN_ERR_OOM if the dense operator does not fit; N <= 65535 nodes.  st: iters =
- * batched GMRES iterations, ms = wall time.  Synchronises the stream. */
+ * block GMRES iterations (each one operator application to all Nc columns; BPQN_LO_BATCHED=1 selects Nc
+ * per-column GMRES processes instead), ms = wall time.  Synchronises the stream. */
 int bpqn_lcp_matrix_dense(bpqn_geom_t g, const bpqn_gmres_opts* gm, double* A_host, bpqn_gmres_stats* st,
                           void* stream);
 
