@@ -589,6 +589,7 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   const bool blockmode = !(eb && eb[0] == '1');
   int m = std::max(4, std::min(o.restart, GM_BATCH_MAX_M));
   int kmax = std::max(2, std::min(40, (int)(n / std::max(R, 1)) - 1));
+  if (const char* ek = getenv("BPQN_LO_BLOCK_KMAX")) kmax = std::max(1, std::min(kmax, atoi(ek)));  // tests: restarts
   if (blockmode) {
     while (kmax > 4 && dense_lo_block_bytes(g, kmax) + ((size_t)1 << 30) > fr) kmax -= 4;
     if (dense_lo_block_bytes(g, kmax) + ((size_t)1 << 30) > fr)

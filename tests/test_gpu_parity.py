@@ -778,6 +778,13 @@ def test_lcp_matrix_dense_block_equals_batched(bp, c, p):
             del os.environ["BPQN_LO_BATCHED"]
         assert rel(Ab, Aa) <= 100 * tol, (tol, rel(Ab, Aa))
         assert stb.iters < sta.iters, (stb.iters, sta.iters)
+    # restarted block GMRES (3 block iterations per cycle, restarts from the true residual)
+    os.environ["BPQN_LO_BLOCK_KMAX"] = "3"
+    try:
+        Ar, str_ = bp.lcp_matrix_dense(g, gmres=bp.default_gmres_opts(tol=1e-10))
+    finally:
+        del os.environ["BPQN_LO_BLOCK_KMAX"]
+    assert str_.iters > 3 and rel(Ar, Aa) <= 1e-8, (str_.iters, rel(Ar, Aa))
 
 
 def test_solve_lcp_bi_dense_lo_c2(bp):
