@@ -84,6 +84,25 @@ def test_layer_apply_small(bp, name):
     assert rel(usd, ref_s + ref_d) <= TOL_SUM
 
 
+@pytest.mark.parametrize("a,mu", [(0.7, 1.3), (2.5, 0.4)])
+def test_layer_apply_radius_viscosity(bp, a, mu):
+    """Spheres of radius a != 1 in a fluid of viscosity mu != 1 (the near rule's graded theta' panel,
+    the rotation-form tensors and the self rules all scale with a): three spheres at gaps 0.004 a /
+    0.05 a against the oracle."""
+    from oracle.layer import Disc
+    e = np.array([0.6, -0.48, 0.64])
+    C = np.array([[0.2, 0.1, -0.3], [0.2, 0.1, -0.3] + a * 2.004 * e,
+                  [0.2, 0.1, -0.3] + a * np.array([0.3, 2.05, 0.1]) / np.linalg.norm([0.3, 2.05, 0.1]) * 2.05])
+    p = 7
+    d = Disc(C, p, a, mu)
+    g = bp.Geometry(C, p, radius=a, mu=mu)
+    assert g.N == d.N and g.n_incidences == len(d.inc) > 0
+    rng = np.random.default_rng(13)
+    f, q = rng.standard_normal((d.N, 3)), rng.standard_normal((d.N, 3))
+    usd = bp.layer_apply(g, f=T(f), q=T(q)).cpu().numpy()
+    assert rel(usd, d.apply_all(f=f) + d.apply_all(q=q)) <= TOL_SUM
+
+
 def _random_scene(seed):
     """Seeded random packing: 2-12 unit spheres, gaps >= 0.01, order p in 3..9 (both K1 variants,
     ragged target blocks and source tiles, near and far pairs)."""
