@@ -194,12 +194,13 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
                    const bpqn_solve_opts* o, bpqn_report* rep, void* stream);
 
 /* The whole LCP matrix A = D^T M D of the handle's contact set, row-major [Nc][Nc] into A_host:
- * all Nc mobility solves as one right-preconditioned block GMRES on the dense completed double-layer
+ * all Nc mobility solves by right-preconditioned (block) GMRES on the dense completed double-layer
  * operator (8 (3N)^2 bytes of device memory, FP64 GEMMs; gm's tolerance per column).  This is how
  * bpqn_solve_opts.lo_dense forms the low-fidelity A^ (R38); the paper analyses dense A / A^ offline
  * (Fig. 3).  BPQN_ERR_OOM if the dense operator does not fit; N <= 65535 nodes.  st: iters =
- * block GMRES iterations (each one operator application to all Nc columns; BPQN_LO_BATCHED=1 selects Nc
- * per-column GMRES processes instead), ms = wall time.  Synchronises the stream. */
+ * GMRES iterations (one block GMRES over all Nc columns when 3N >= 100 Nc, each iteration one operator
+ * application to all columns; otherwise Nc per-column GMRES processes advancing together), ms = wall time.
+ * Synchronises the stream. */
 int bpqn_lcp_matrix_dense(bpqn_geom_t g, const bpqn_gmres_opts* gm, double* A_host, bpqn_gmres_stats* st,
                           void* stream);
 

@@ -584,9 +584,13 @@ int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, De
   BPQN_REQUIRE(g.Minv.p && g.E_A.p, "geometry has no self operators");
   size_t fr = 0, tot = 0;
   BPQN_CUDA(cudaMemGetInfo(&fr, &tot));
-  // block GMRES (default) or the batched per-column GMRES (BPQN_LO_BATCHED=1)
+  // block GMRES or the batched per-column GMRES.  Block CGS2 costs ~8 k s^2 n flops per block iteration
+  // against 2 n^2 s for the operator, so the block form pays when n >> s (measured: c4 lo n = 173 s,
+  // block 9.8 s vs batched 12.6 s; c4 centres at p = 4, n = 48 s, block 1.43 s vs batched 1.17 s):
+  // block when n >= 100 s; BPQN_LO_BATCHED=1 / BPQN_LO_BLOCK=1 force either.
   const char* eb = getenv("BPQN_LO_BATCHED");
-  const bool blockmode = !(eb && eb[0] == '1');
+  const char* ek = getenv("BPQN_LO_BLOCK");
+  const bool blockmode = (ek && ek[0] == '1') || (!(eb && eb[0] == '1') && n >= (size_t)100 * R);
   int m = std::max(4, std::min(o.restart, GM_BATCH_MAX_M));
   int kmax = std::max(2, std::min(40, (int)(n / std::max(R, 1)) - 1));
   if (const char* ek = getenv("BPQN_LO_BLOCK_KMAX")) kmax = std::max(1, std::min(kmax, atoi(ek)));  // tests: restarts
