@@ -54,6 +54,11 @@ typedef struct {
   double d_near;
   int near_n1, near_n2, near_nphi;
   int build_single_layer; /* 1 (default): also precompute S-kernel near/self data */
+  int fmm_order;          /* 0 (default): K1 is the direct all-pairs sum.  3..12: the all-pairs coarse sum is
+                             evaluated by a kernel-independent FMM (fmm_order points per edge of the
+                             equivalent / check cube surfaces, uniform octree; SURVEY NEXT-4,
+                             for N >> 3e5) -- an approximation whose relative error is set by the order
+                             (measured: profiles/r02_fmm.md); not with sharding. */
 } bpqn_disc_opts;
 
 /* GMRES options (R9).  NULL -> tol 1e-12 (relative residual), restart 100 (<= 500),

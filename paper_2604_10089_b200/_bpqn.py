@@ -17,7 +17,7 @@ P = ctypes.POINTER
 
 class DiscOpts(ctypes.Structure):
     _fields_ = [("p_s", c_int), ("d_near", c_double), ("near_n1", c_int), ("near_n2", c_int),
-                ("near_nphi", c_int), ("build_single_layer", c_int)]
+                ("near_nphi", c_int), ("build_single_layer", c_int), ("fmm_order", c_int)]
 
 
 class GmresOpts(ctypes.Structure):

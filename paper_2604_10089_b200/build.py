@@ -6,7 +6,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libbpqn.so")
-SOURCES = ["capi.cu", "geometry.cu", "allpairs.cu", "layer.cu", "gmres.cu", "contacts.cu", "comm.cu", "diag.cu", "dense_lo.cu", "pqn.cpp"]
+SOURCES = ["capi.cu", "geometry.cu", "allpairs.cu", "layer.cu", "gmres.cu", "contacts.cu", "comm.cu", "diag.cu", "dense_lo.cu", "fmm.cu", "pqn.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-Xcompiler", "-O3"]

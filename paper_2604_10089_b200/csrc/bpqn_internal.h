@@ -205,6 +205,9 @@ struct Geom {
   void* nccl_comm = nullptr;
   bool sh_sym_nccl = false;  // symmetric K1 split with the NCCL reduce-scatter
   DBuf<double> sh_own_send, sh_own_recv, sh_own_rs_send, sh_own_rs_recv;
+  // far-field FMM replacing K1 (fmm.cu; bpqn_disc_opts.fmm_order > 0)
+  int fmm_order = 0, fmm_max_leaf = 0;
+  struct Fmm* fmm = nullptr;
   bool sharded() const { return shard_world > 1 || nccl_comm != nullptr; }
   ~Geom();
 };
@@ -254,6 +257,19 @@ void assemble_dense_operator(Geom& g, double* A_dev, cudaStream_t s);  // [3N][3
 // A^ = D^T M D of the handle's contact set (row-major Nc x Nc, host) by one batched GMRES over all
 // Nc unit vectors with a dense operator; throws BPQN_ERR_OOM if it does not fit
 int densify_lcp(Geom& g, const bpqn_gmres_opts& o, std::vector<double>& Ahat, DenseLoStats& st, cudaStream_t s);
+
+// dense linear algebra on the device (dense_lo.cu): column-major cuBLAS DGEMM / DTRSM (lower
+// triangular, non-unit; side 0 = left, 1 = right; trans 0 = N, 1 = T), blocked Cholesky (lower,
+// strict upper triangle zeroed)
+void blas_dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double alpha, const double* A, int lda,
+                const double* B, int ldb, double beta, double* C, int ldc);
+void blas_dtrsm(cudaStream_t st, int side, int trans, int m, int n, const double* L, int ldl, double* B, int ldb);
+void dev_potrf(cudaStream_t st, double* A, int n, int lda);
+
+// FMM (fmm.cu): tree and lists from the host node positions; the K1 coarse sum into out [N][3]
+void fmm_build(Geom& g, const std::vector<double>& X_host, cudaStream_t st);
+void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cudaStream_t st);
+void fmm_free(struct Fmm* f);
 
 // NCCL (comm.cu)
 void comm_unique_id(void* out128);

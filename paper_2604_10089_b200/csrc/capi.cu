@@ -22,6 +22,7 @@ Geom::~Geom() {
     comm_destroy(*this);
   } catch (...) {
   }
+  fmm_free(fmm);
   if (host_scal) cudaFreeHost(host_scal);
   for (auto& e : prof.pool)
     if (e) cudaEventDestroy(e);
@@ -108,6 +109,7 @@ static void set_centers(Geom& G, const double* centers_host, cudaStream_t st) {
   upload(g->X, X, st);
   upload(g->src, src, st);
   upload(g->centers_d, g->centers, st);
+  fmm_build(*g, X, st);  // far-field FMM tree and lists (only when fmm_order > 0)
   std::vector<std::pair<int, int>> inc;
   for (int n = 0; n < g->np; ++n)
     for (int m = 0; m < g->np; ++m) {
@@ -213,6 +215,7 @@ void bpqn_default_disc_opts(bpqn_disc_opts* o) {
   o->near_n2 = 0;
   o->near_nphi = 0;
   o->build_single_layer = 1;
+  o->fmm_order = 0;
 }
 
 void bpqn_default_gmres_opts(bpqn_gmres_opts* o) {
@@ -279,6 +282,8 @@ int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_ho
       BPQN_REQUIRE(g->p_s + 1 <= 128 && 2 * g->p_s <= 256 && g->n1 + g->n2 <= 128 && g->nphi <= 256,
                    "discretisation options exceed the precompute tables (p_s <= 63, n1 + n2 <= 128, nphi <= 256)");
       g->single_layer = o.build_single_layer != 0;
+      g->fmm_order = o.fmm_order;
+      BPQN_REQUIRE(o.fmm_order == 0 || (o.fmm_order >= 3 && o.fmm_order <= 12), "fmm_order must be 0 or in [3, 12]");
       const char* ov = getenv("BPQN_OVERLAP_K2");
       g->overlap_k2 = ov && ov[0] == '1';
       build_grid(p, radius, g->grid);

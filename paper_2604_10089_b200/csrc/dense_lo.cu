@@ -85,8 +85,8 @@ static void gemm_rowA(cudaStream_t st, int m, int n, int k, const double* A_row,
 }
 
 // plain column-major DGEMM / DTRSM (cuBLAS conventions)
-static void dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double alpha, const double* A, int lda,
-                  const double* B, int ldb, double beta, double* C, int ldc) {
+void blas_dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double alpha, const double* A, int lda,
+                const double* B, int ldb, double beta, double* C, int ldc) {
   Cublas& cb = cublas();
   void* h = cublas_handle();
   if (cb.setStream(h, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
@@ -94,7 +94,7 @@ static void dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double a
     throw Error{BPQN_ERR_CUDA, "cublasDgemm failed"};
 }
 constexpr int CB_LEFT = 0, CB_RIGHT = 1, CB_LOWER = 0, CB_NONUNIT = 0;
-static void dtrsm(cudaStream_t st, int side, int trans, int m, int n, const double* L, int ldl, double* B, int ldb) {
+void blas_dtrsm(cudaStream_t st, int side, int trans, int m, int n, const double* L, int ldl, double* B, int ldb) {
   Cublas& cb = cublas();
   void* h = cublas_handle();
   const double one = 1.0;
@@ -382,7 +382,7 @@ static int grid_for(size_t work) { return (int)std::max<size_t>(1, std::min<size
 
 // Blocked right-looking Cholesky A = L L^T (column-major, lower, the strict upper triangle zeroed): panels of 64 in shared memory, the
 // panel below by DTRSM and the trailing update by DGEMM (cuBLAS).
-static void potrf(cudaStream_t st, double* A, int n, int lda) {
+void dev_potrf(cudaStream_t st, double* A, int n, int lda) {
   for (int j = 0; j < n; j += POTRF_NB) {
     const int jb = std::min(POTRF_NB, n - j);
     double* Ajj = A + (size_t)j * lda + j;
@@ -391,8 +391,8 @@ static void potrf(cudaStream_t st, double* A, int n, int lda) {
     const int r = n - j - jb;
     if (r > 0) {
       double* P = Ajj + jb;  // rows j+jb.., columns j..j+jb
-      dtrsm(st, CB_RIGHT, CUBLAS_OP_T_, r, jb, Ajj, lda, P, lda);
-      dgemm(st, CUBLAS_OP_N_, CUBLAS_OP_T_, r, r, jb, -1.0, P, lda, P, lda, 1.0, Ajj + (size_t)jb * lda + jb, lda);
+      blas_dtrsm(st, CB_RIGHT, CUBLAS_OP_T_, r, jb, Ajj, lda, P, lda);
+      blas_dgemm(st, CUBLAS_OP_N_, CUBLAS_OP_T_, r, r, jb, -1.0, P, lda, P, lda, 1.0, Ajj + (size_t)jb * lda + jb, lda);
     }
   }
   k_zero_upper<<<grid_for((size_t)n * n), 256, 0, st>>>(A, n, lda);
@@ -467,24 +467,24 @@ static int block_gmres(Geom& g, const double* A, const double* B, const double* 
   const int T_ = CUBLAS_OP_T_, N_ = CUBLAS_OP_N_;
   // W = Q R with Q overwriting W, R = (L1 L2)^T upper (ld ldr)
   auto cholqr2 = [&](double* W, double* Rout, int ldr) {
-    dgemm(st, T_, N_, s, s, (int)n, 1.0, W, (int)n, W, (int)n, 0.0, Gs.p, s);
-    potrf(st, Gs.p, s, s);
-    dtrsm(st, CB_RIGHT, T_, (int)n, s, Gs.p, s, W, (int)n);
-    dgemm(st, T_, N_, s, s, (int)n, 1.0, W, (int)n, W, (int)n, 0.0, G2.p, s);
-    potrf(st, G2.p, s, s);
-    dtrsm(st, CB_RIGHT, T_, (int)n, s, G2.p, s, W, (int)n);
-    dgemm(st, T_, T_, s, s, s, 1.0, G2.p, s, Gs.p, s, 0.0, Rout, ldr);  // L2^T L1^T
+    blas_dgemm(st, T_, N_, s, s, (int)n, 1.0, W, (int)n, W, (int)n, 0.0, Gs.p, s);
+    dev_potrf(st, Gs.p, s, s);
+    blas_dtrsm(st, CB_RIGHT, T_, (int)n, s, Gs.p, s, W, (int)n);
+    blas_dgemm(st, T_, N_, s, s, (int)n, 1.0, W, (int)n, W, (int)n, 0.0, G2.p, s);
+    dev_potrf(st, G2.p, s, s);
+    blas_dtrsm(st, CB_RIGHT, T_, (int)n, s, G2.p, s, W, (int)n);
+    blas_dgemm(st, T_, T_, s, s, s, 1.0, G2.p, s, Gs.p, s, 0.0, Rout, ldr);  // L2^T L1^T
   };
   // Res = E1 S0 - Hbar[0:kk+s, 0:kk] Y  (ld ldH)
   auto residual = [&](int kk, const double* Yp) {
     BPQN_CUDA(cudaMemsetAsync(Res.p, 0, 8 * (size_t)ldH * s, st));
     k_copy_block<<<grid_for((size_t)s * s), 256, 0, st>>>(Res.p, ldH, S0.p, s, s, s);
     BPQN_CHECK_LAUNCH();
-    dgemm(st, N_, N_, kk + s, s, kk, -1.0, H.p, ldH, Yp, ldL, 1.0, Res.p, ldH);
+    blas_dgemm(st, N_, N_, kk + s, s, kk, -1.0, H.p, ldH, Yp, ldL, 1.0, Res.p, ldH);
   };
   auto cholsolve = [&](int kk, double* Yp) {  // Yp <- (L L^T)^-1 Yp on the leading kk rows
-    dtrsm(st, CB_LEFT, N_, kk, s, L.p, ldL, Yp, ldL);
-    dtrsm(st, CB_LEFT, T_, kk, s, L.p, ldL, Yp, ldL);
+    blas_dtrsm(st, CB_LEFT, N_, kk, s, L.p, ldL, Yp, ldL);
+    blas_dtrsm(st, CB_LEFT, T_, kk, s, L.p, ldL, Yp, ldL);
   };
   std::vector<double> res(s);
   int total = 0;
@@ -511,33 +511,33 @@ static int block_gmres(Geom& g, const double* A, const double* B, const double* 
       gemm_rowA(st, M3, g.np * s, M3, g.Minv.p, Vk, M3, Z.p, M3);
       gemm_rowA(st, (int)n, s, (int)n, A, Z.p, (int)n, Vn, (int)n);
       // block CGS2 against V_0..V_k
-      dgemm(st, T_, N_, kk, s, (int)n, 1.0, V.p, (int)n, Vn, (int)n, 0.0, Hk, ldH);
-      dgemm(st, N_, N_, (int)n, s, kk, -1.0, V.p, (int)n, Hk, ldH, 1.0, Vn, (int)n);
-      dgemm(st, T_, N_, kk, s, (int)n, 1.0, V.p, (int)n, Vn, (int)n, 0.0, Tb.p, kk);
-      dgemm(st, N_, N_, (int)n, s, kk, -1.0, V.p, (int)n, Tb.p, kk, 1.0, Vn, (int)n);
+      blas_dgemm(st, T_, N_, kk, s, (int)n, 1.0, V.p, (int)n, Vn, (int)n, 0.0, Hk, ldH);
+      blas_dgemm(st, N_, N_, (int)n, s, kk, -1.0, V.p, (int)n, Hk, ldH, 1.0, Vn, (int)n);
+      blas_dgemm(st, T_, N_, kk, s, (int)n, 1.0, V.p, (int)n, Vn, (int)n, 0.0, Tb.p, kk);
+      blas_dgemm(st, N_, N_, (int)n, s, kk, -1.0, V.p, (int)n, Tb.p, kk, 1.0, Vn, (int)n);
       k_add_block<<<grid_for((size_t)kk * s), 256, 0, st>>>(Hk, ldH, Tb.p, kk, kk, s);
       BPQN_CHECK_LAUNCH();
       cholqr2(Vn, Hk + kk, ldH);  // H_{k+1,k}
       // normal equations: new block column of Hbar^T Hbar, then block row k of its Cholesky factor
-      dgemm(st, T_, N_, kk, s, kk + s, 1.0, H.p, ldH, Hk, ldH, 0.0, Tb.p, kk);
+      blas_dgemm(st, T_, N_, kk, s, kk + s, 1.0, H.p, ldH, Hk, ldH, 0.0, Tb.p, kk);
       double* Lkk = L.p + (size_t)k * s * ldL + (size_t)k * s;
       if (k > 0) {
-        dtrsm(st, CB_LEFT, N_, k * s, s, L.p, ldL, Tb.p, kk);                           // X = L^-1 G[0:ks, k]
-        dgemm(st, T_, N_, s, s, k * s, -1.0, Tb.p, kk, Tb.p, kk, 1.0, Tb.p + (size_t)k * s, kk);  // G_kk - X^T X
+        blas_dtrsm(st, CB_LEFT, N_, k * s, s, L.p, ldL, Tb.p, kk);                           // X = L^-1 G[0:ks, k]
+        blas_dgemm(st, T_, N_, s, s, k * s, -1.0, Tb.p, kk, Tb.p, kk, 1.0, Tb.p + (size_t)k * s, kk);  // G_kk - X^T X
         k_transpose_block<<<grid_for((size_t)s * k * s), 256, 0, st>>>(L.p + (size_t)k * s, ldL, Tb.p, kk, s, k * s);
         BPQN_CHECK_LAUNCH();
       }
       k_copy_block<<<grid_for((size_t)s * s), 256, 0, st>>>(Lkk, ldL, Tb.p + (size_t)k * s, kk, s, s);
       BPQN_CHECK_LAUNCH();
-      potrf(st, Lkk, s, ldL);
+      dev_potrf(st, Lkk, s, ldL);
       // F block k = Hbar[0:s, block k]^T S0 (E1 S0 is zero below the first block row)
-      dgemm(st, T_, N_, s, s, s, 1.0, Hk, ldH, S0.p, s, 0.0, F.p + (size_t)k * s, ldL);
+      blas_dgemm(st, T_, N_, s, s, s, 1.0, Hk, ldH, S0.p, s, 0.0, F.p + (size_t)k * s, ldL);
       // Y = (L L^T)^-1 F, one refinement step from the explicit residual
       k_copy_block<<<grid_for((size_t)kk * s), 256, 0, st>>>(Y.p, ldL, F.p, ldL, kk, s);
       BPQN_CHECK_LAUNCH();
       cholsolve(kk, Y.p);
       residual(kk, Y.p);
-      dgemm(st, T_, N_, kk, s, kk + s, 1.0, H.p, ldH, Res.p, ldH, 0.0, Y2.p, ldL);
+      blas_dgemm(st, T_, N_, kk, s, kk + s, 1.0, H.p, ldH, Res.p, ldH, 0.0, Y2.p, ldL);
       cholsolve(kk, Y2.p);
       k_add_block<<<grid_for((size_t)kk * s), 256, 0, st>>>(Y.p, ldL, Y2.p, ldL, kk, s);
       BPQN_CHECK_LAUNCH();
@@ -555,7 +555,7 @@ static int block_gmres(Geom& g, const double* A, const double* B, const double* 
       }
       done = worst <= tol;
       if (done || k + 1 == kmax || total >= max_blocks) {  // x += M^-1 V_{0..k} Y
-        dgemm(st, N_, N_, (int)n, s, kk, 1.0, V.p, (int)n, Y.p, ldL, 0.0, Wt.p, (int)n);
+        blas_dgemm(st, N_, N_, (int)n, s, kk, 1.0, V.p, (int)n, Y.p, ldL, 0.0, Wt.p, (int)n);
         gemm_rowA(st, M3, g.np * s, M3, g.Minv.p, Wt.p, M3, X, M3, 1.0);
         break;
       }

@@ -567,6 +567,24 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   if (ev) BPQN_CUDA(cudaEventRecord(ev[2], sk2));
   launch_near(g, sigS, sigD, sk2);
   if (ev) BPQN_CUDA(cudaEventRecord(ev[3], sk2));
+  if (g.fmm) {  // far-field FMM in place of K1 (fmm.cu): the coarse sum into far, then far + K2, K3
+    BPQN_REQUIRE(!sharded, "the FMM far field does not combine with sharding");
+    if (ev) BPQN_CUDA(cudaEventRecord(ev[0], st));
+    fmm_apply(g, sigS, sigD, g.far.p, st);
+    if (ev) {
+      BPQN_CUDA(cudaEventRecord(ev[1], st));
+      P.allpairs_flop += (double)g.n * (double)g.n * allpairs_flops_per_pair(mode);  // nominal
+    }
+    if (overlap) {
+      BPQN_CUDA(cudaEventRecord(g.ev_join, g.side));
+      BPQN_CUDA(cudaStreamWaitEvent(st, g.ev_join, 0));
+    }
+    launch_row_reduce(g, false, g.far.p, true, out, r0, r1, st);
+    if (sigS) launch_self_gemm(g, Es, sigS, out, 1, st, s0, s1);
+    if (sigD) launch_self_gemm(g, Ed, sigD, out, 1, st, s0, s1);
+    if (ev) BPQN_CUDA(cudaEventRecord(ev[4], st));
+    return;
+  }
   if (ev) BPQN_CUDA(cudaEventRecord(ev[0], st));
   launch_allpairs(g, mode, sigS, sigD, g.far.p, st);
   if (ev) {
