@@ -869,3 +869,68 @@ def test_near_rotation_equals_brute_force(bp, p, gap, axis):
         ur = bp.layer_apply(gr, **kw).cpu().numpy()
         ub = bp.layer_apply(gb, **kw).cpu().numpy()
         assert rel(ur, ub) <= 1e-13, (list(kw), rel(ur, ub))
+
+
+# ------------------------------------------------------------------ NEXT-4: FMM far field (fmm_order)
+def _lattice(n, seed, spacing=2.02, jitter=0.01):
+    rng = np.random.default_rng(seed)
+    g1 = np.arange(n) * spacing
+    return np.array([[x, y, z] for x in g1 for y in g1 for z in g1]) + rng.uniform(-jitter, jitter, (n ** 3, 3))
+
+
+def _fmm_geometry(bp, C, p, order, levels=None):
+    op = bp.default_disc_opts()
+    op.fmm_order = order
+    if levels:
+        os.environ["BPQN_FMM_LEVELS"] = str(levels)
+    try:
+        return bp.Geometry(C, p, opts=op)
+    finally:
+        os.environ.pop("BPQN_FMM_LEVELS", None)
+
+
+@pytest.mark.parametrize("levels", [2, 3, 4])
+def test_fmm_layer_apply_vs_direct(bp, levels):
+    """The FMM far field (order 10) against the direct all-pairs K1 on the same geometry: S, D and S+D layer
+    applies within the measured FMM accuracy (order 10: ~3e-8 S, ~2e-7 D; bound 1e-6), with 2, 3 and 4 tree
+    levels (M2M / L2L exercised); two applies are bit-identical."""
+    C = _lattice(6, 41)
+    gd = bp.Geometry(C, 6)
+    gf = _fmm_geometry(bp, C, 6, 10, levels)
+    rng = np.random.default_rng(42)
+    f, q = T(rng.standard_normal((gd.N, 3))), T(rng.standard_normal((gd.N, 3)))
+    for kw in (dict(f=f), dict(q=q), dict(f=f, q=q)):
+        ud = bp.layer_apply(gd, **kw).cpu().numpy()
+        uf = bp.layer_apply(gf, **kw).cpu().numpy()
+        assert rel(uf, ud) <= 1e-6, (list(kw), rel(uf, ud))
+    u1 = bp.layer_apply(gf, f=f, q=q).cpu().numpy()
+    u2 = bp.layer_apply(gf, f=f, q=q).cpu().numpy()
+    assert np.array_equal(u1, u2)
+
+
+def test_fmm_layer_apply_vs_oracle(bp):
+    """FMM-mode layer apply (order 10, 3 levels) against the oracle's direct operator on sampled targets."""
+    from oracle.layer import Disc
+    C = _lattice(4, 43)
+    d = Disc(C, 5)
+    g = _fmm_geometry(bp, C, 5, 10, 3)
+    rng = np.random.default_rng(44)
+    f, q = rng.standard_normal((d.N, 3)), rng.standard_normal((d.N, 3))
+    u = bp.layer_apply(g, f=T(f), q=T(q)).cpu().numpy()
+    tg = _sample_targets(d, 48, 45)
+    assert rel(u[tg], d.apply(f=f, q=q, targets=tg)) <= 1e-6
+
+
+def test_fmm_lcp_mvp_vs_direct(bp):
+    """An LCP MVP (GMRES 1e-10) with the FMM far field equals the direct one to the FMM accuracy."""
+    C = _lattice(4, 46)
+    gd = bp.Geometry(C, 6)
+    gf = _fmm_geometry(bp, C, 6, 10, 2)
+    bp.contacts(gd, 0.1)
+    bp.contacts(gf, 0.1)
+    assert gd.nc == gf.nc > 0
+    lam = T(np.random.default_rng(47).uniform(0, 1, gd.nc))
+    gm = bp.default_gmres_opts(tol=1e-10)
+    wd, _ = bp.lcp_mvp(gd, lam, gmres=gm)
+    wf, _ = bp.lcp_mvp(gf, lam, gmres=gm)
+    assert rel(wf.cpu().numpy(), wd.cpu().numpy()) <= 1e-5
