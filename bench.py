@@ -52,6 +52,8 @@ def parse():
     ap.add_argument("--no-solve", action="store_true")
     ap.add_argument("--recycle", type=int, default=1)   # GMRES recycling inside the LCP solve (NEXT-3)
     ap.add_argument("--solvers", default="bi,mono,bb")  # comma list of bi, mono, bb (BB-PGD)
+    ap.add_argument("--no-fmm", action="store_true")    # skip the N >> 3e5 FMM context run (NEXT-4)
+    ap.add_argument("--fmm-order", type=int, default=10)
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--replicas", action="store_true")  # N > 1: independent replicas instead of the sharded MVP
     ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
@@ -417,6 +419,8 @@ def run_ours(args, ws, rank, local):
 
     if not args.no_c5 and ws == 1:
         line["layer_apply_c5"] = run_c5(args, dev, stream)
+    if not args.no_fmm and ws == 1:
+        line["fmm_large"] = run_fmm_large(args, dev, stream)
     if not args.no_paper and ws == 1:
         line["paper_setting_6x6x6"] = run_paper_setting(args, dev, stream)
 
@@ -551,6 +555,65 @@ def run_paper_setting(args, dev, stream):
                              "source": "PAPER.md Table 3 (P:613-629): 6x6x6 BB-PGD collision 5d 0h 25m / 200 steps"}}
     hi.close()
     lo.close()
+    return out
+
+
+def run_fmm_large(args, dev, stream):
+    """Context (an FMM for N >> 3e5): 4 096 unit spheres on a 16^3 lattice (the c4 recipe:
+    spacing 2.02, jitter +-0.01) at the paper's p = 8, N = 589 824.  One D layer apply with the direct K1 and
+    with the FMM far field (bpqn_disc_opts.fmm_order), their relative L2 difference, and one LCP MVP at
+    GMRES 1e-8 in each mode (the FMM is an approximation; the direct sum is the north star's kernel)."""
+    import torch
+    import paper_2604_10089_b200 as bp
+    rng = np.random.default_rng(20260099)
+    n = 16
+    g1 = np.arange(n) * 2.02
+    C = np.array([[x, y, z] for x in g1 for y in g1 for z in g1]) + rng.uniform(-0.01, 0.01, (n ** 3, 3))
+    q = None
+    out = {"workload": "4096 spheres (16^3 lattice, spacing 2.02, jitter 0.01), p = 8", "fmm_order": args.fmm_order}
+    ref = None
+    for mode in ("direct", "fmm"):
+        op = bp.default_disc_opts()
+        op.fmm_order = args.fmm_order if mode == "fmm" else 0
+        t0 = time.time()
+        g = bp.Geometry(C, 8, opts=op)
+        torch.cuda.synchronize()
+        t_init = time.time() - t0
+        if q is None:
+            q = torch.tensor(rng.standard_normal((g.N, 3)), device=dev)
+            out["N"] = g.N
+        u = torch.empty((g.N, 3), dtype=torch.float64, device=dev)
+        bp.layer_apply(g, None, q, out=u)
+        ms = []
+        for _ in range(3):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            bp.layer_apply(g, None, q, out=u)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        r = {"geometry_init_s": round(t_init, 2), "ms_layer_apply_d": float(np.median(ms))}
+        if ref is None:
+            ref = u.clone()
+        else:
+            r["rel_l2_vs_direct"] = float(torch.linalg.norm(u - ref) / torch.linalg.norm(ref))
+        bp.contacts(g, 0.1)
+        lam = torch.tensor(np.random.default_rng(20262099).uniform(0, 1, g.nc), device=dev)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        w, st = bp.lcp_mvp(g, lam, gmres=bp.default_gmres_opts(tol=1e-8))
+        e1.record(stream)
+        torch.cuda.synchronize()
+        r.update({"contacts": g.nc, "ms_lcp_mvp": e0.elapsed_time(e1), "gmres_iters": st.iters})
+        if mode == "direct":
+            wref = w.clone()
+        else:
+            r["mvp_rel_l2_vs_direct"] = float(torch.linalg.norm(w - wref) / torch.linalg.norm(wref))
+        out[mode] = r
+        del g, u
+        torch.cuda.empty_cache()
+    out["speedup_layer_apply"] = out["direct"]["ms_layer_apply_d"] / out["fmm"]["ms_layer_apply_d"]
+    out["speedup_mvp"] = out["direct"]["ms_lcp_mvp"] / out["fmm"]["ms_lcp_mvp"]
     return out
 
 
