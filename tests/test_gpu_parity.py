@@ -908,6 +908,28 @@ def test_fmm_layer_apply_vs_direct(bp, levels):
     assert np.array_equal(u1, u2)
 
 
+@pytest.mark.parametrize("scene", ["c3_rsa", "single", "two_far"])
+def test_fmm_sparse_trees(bp, scene):
+    """FMM on trees with many empty boxes: the c3 random sequential packing (64 spheres, 3 levels), one sphere,
+    two spheres far apart (most boxes empty, leaves with points only at two corners)."""
+    from synth import make_config
+    if scene == "c3_rsa":
+        C, p, lv = make_config(3)["centers"], 6, 3
+    elif scene == "single":
+        C, p, lv = np.array([[0.3, -0.2, 0.1]]), 8, 2
+    else:
+        C, p, lv = np.array([[0.0, 0.0, 0.0], [9.0, 7.5, -6.0]]), 8, 3
+    gd = bp.Geometry(C, p)
+    gf = _fmm_geometry(bp, C, p, 10, lv)
+    rng = np.random.default_rng(48)
+    f, q = T(rng.standard_normal((gd.N, 3))), T(rng.standard_normal((gd.N, 3)))
+    ud = bp.layer_apply(gd, f=f, q=q).cpu().numpy()
+    uf = bp.layer_apply(gf, f=f, q=q).cpu().numpy()
+    # one sphere: every far pair lies on the same sphere and the sum cancels more (|u| ~ 1/4 of the
+    # multi-sphere scenes'), so the FMM's error relative to |u| is larger
+    assert rel(uf, ud) <= (5e-6 if scene == "single" else 1e-6), rel(uf, ud)
+
+
 def test_fmm_layer_apply_vs_oracle(bp):
     """FMM-mode layer apply (order 10, 3 levels) against the oracle's direct operator on sampled targets."""
     from oracle.layer import Disc
