@@ -213,44 +213,90 @@ __global__ void __launch_bounds__(128) k_fmm_p2m(const double* __restrict__ rec,
   }
 }
 
-// Leaves: near field (27 neighbour leaves, i != j) + L2P from the leaf's downward equivalent density; writes
-// out[node] in the original order
-__global__ void __launch_bounds__(128) k_fmm_leaf(const double* __restrict__ rec, const int* __restrict__ start,
-                                                  const int* __restrict__ nbr, const int* __restrict__ perm,
-                                                  const double* __restrict__ surf, int ns, const double* __restrict__ ctr,
-                                                  double rad, const double* __restrict__ deq, bool doS, bool doD,
-                                                  double* __restrict__ out) {
-  __shared__ double sr[128 * 12];
-  const int b = blockIdx.x, t0 = start[b], t1 = start[b + 1];
-  const int k = t0 + blockIdx.y * 128 + threadIdx.x;
-  const bool act = k < t1;
-  double x0 = 0, x1 = 0, x2 = 0, u0 = 0, u1 = 0, u2 = 0;
-  if (act) {
-    x0 = rec[12 * (size_t)k];
-    x1 = rec[12 * (size_t)k + 1];
-    x2 = rec[12 * (size_t)k + 2];
+// The K1 pair kernel with K1's rsqrt (one MUFU.RSQ64H seed + the series to e^2, |e| <= 2^-19; allpairs.cu);
+// rho = 0 (the target itself) contributes nothing
+__device__ __forceinline__ double fmm_seed(double rr) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(rr));
+  return rr > 0.0 ? y : 0.0;
+}
+template <int MODE>
+__device__ __forceinline__ void fmm_pair_fast(double x0, double x1, double x2, const double* s, double& u0,
+                                              double& u1, double& u2) {
+  const double r0 = x0 - s[0], r1 = x1 - s[1], r2 = x2 - s[2];
+  const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+  const double y = fmm_seed(rr), y2 = y * y;
+  const double e = fma(-rr, y2, 1.0);
+  double t;
+  if (MODE == MODE_D) {
+    const double s5 = (y * (y2 * y2)) * fma(e, fma(e, 4.375, 2.5), 1.0);
+    const double rn = fma(r2, s[5], fma(r1, s[4], r0 * s[3]));
+    const double rq = fma(r2, s[11], fma(r1, s[10], r0 * s[9]));
+    t = (rn * rq) * s5;
+  } else {
+    const double sv = fma(y * e, fma(e, 0.375, 0.5), y);
+    const double s2 = sv * sv, s3 = s2 * sv;
+    const double rf = fma(r2, s[8], fma(r1, s[7], r0 * s[6]));
+    t = rf * s3;
+    if (MODE == MODE_SD) {
+      const double rn = fma(r2, s[5], fma(r1, s[4], r0 * s[3]));
+      const double rq = fma(r2, s[11], fma(r1, s[10], r0 * s[9]));
+      t = fma(rn * rq, s3 * s2, t);
+    }
+    u0 = fma(s[6], sv, u0);
+    u1 = fma(s[7], sv, u1);
+    u2 = fma(s[8], sv, u2);
   }
+  u0 = fma(r0, t, u0);
+  u1 = fma(r1, t, u1);
+  u2 = fma(r2, t, u2);
+}
+
+// Leaves: near field (27 neighbour leaves) + L2P from the leaf's downward equivalent density; two targets per
+// thread share every staged source; writes out[node] in the original order
+constexpr int FL_T = 128, FL_R = 2;
+template <int MODE>
+__global__ void __launch_bounds__(FL_T) k_fmm_leaf(const double* __restrict__ rec, const int* __restrict__ start,
+                                                   const int* __restrict__ nbr, const int* __restrict__ perm,
+                                                   const double* __restrict__ surf, int ns,
+                                                   const double* __restrict__ ctr, double rad,
+                                                   const double* __restrict__ deq, double* __restrict__ out) {
+  __shared__ __align__(16) double sr[FL_T * 12];
+  const int b = blockIdx.x, t0 = start[b], t1 = start[b + 1];
+  int k[FL_R];
+  double x[FL_R][3], u[FL_R][3];
+#pragma unroll
+  for (int r = 0; r < FL_R; ++r) {
+    k[r] = t0 + blockIdx.y * FL_T * FL_R + r * FL_T + threadIdx.x;
+    const int kk = min(k[r], t1 - 1);  // inactive lanes compute a duplicate and do not store
+    x[r][0] = rec[12 * (size_t)kk];
+    x[r][1] = rec[12 * (size_t)kk + 1];
+    x[r][2] = rec[12 * (size_t)kk + 2];
+    u[r][0] = u[r][1] = u[r][2] = 0.0;
+  }
+  if (t0 + blockIdx.y * FL_T * FL_R >= t1) return;
   for (int q = 0; q < 27; ++q) {
     const int nb = nbr[27 * b + q];
     if (nb < 0) continue;
     const int s0 = start[nb], s1 = start[nb + 1];
-    for (int j0 = s0; j0 < s1; j0 += 128) {
-      const int nj = min(128, s1 - j0);
+    for (int j0 = s0; j0 < s1; j0 += FL_T) {
+      const int nj = min(FL_T, s1 - j0);
       __syncthreads();
-      for (int e = threadIdx.x; e < nj * 12; e += 128) sr[e] = rec[12 * (size_t)j0 + e];
+      for (int e = threadIdx.x; e < nj * 12; e += FL_T) sr[e] = rec[12 * (size_t)j0 + e];
       __syncthreads();
-      if (act)
-        for (int j = 0; j < nj; ++j)
-          if (j0 + j != k) fmm_pair(x0, x1, x2, sr + 12 * j, doS, doD, u0, u1, u2);
+#pragma unroll 2
+      for (int j = 0; j < nj; ++j)
+#pragma unroll
+        for (int r = 0; r < FL_R; ++r) fmm_pair_fast<MODE>(x[r][0], x[r][1], x[r][2], sr + 12 * j, u[r][0], u[r][1], u[r][2]);
     }
   }
   // L2P: Stokeslet equivalent density on the downward equivalent surface (2.95 r)
   const double c0 = ctr[3 * b], c1 = ctr[3 * b + 1], c2 = ctr[3 * b + 2];
   const double* ph = deq + (size_t)b * 3 * ns;
-  for (int j0 = 0; j0 < ns; j0 += 128) {
-    const int nj = min(128, ns - j0);
+  for (int j0 = 0; j0 < ns; j0 += FL_T) {
+    const int nj = min(FL_T, ns - j0);
     __syncthreads();
-    for (int e = threadIdx.x; e < nj; e += 128) {
+    for (int e = threadIdx.x; e < nj; e += FL_T) {
       const int j = j0 + e;
       sr[6 * e] = c0 + rad * surf[3 * j];
       sr[6 * e + 1] = c1 + rad * surf[3 * j + 1];
@@ -260,24 +306,28 @@ __global__ void __launch_bounds__(128) k_fmm_leaf(const double* __restrict__ rec
       sr[6 * e + 5] = ph[3 * j + 2];
     }
     __syncthreads();
-    if (act)
-      for (int j = 0; j < nj; ++j) {
-        const double* s = sr + 6 * j;
-        const double r0 = x0 - s[0], r1 = x1 - s[1], r2 = x2 - s[2];
+    for (int j = 0; j < nj; ++j) {
+      const double* sp = sr + 6 * j;
+#pragma unroll
+      for (int r = 0; r < FL_R; ++r) {
+        const double r0 = x[r][0] - sp[0], r1 = x[r][1] - sp[1], r2 = x[r][2] - sp[2];
         const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
         const double ir = rsqrt(rr), ir3 = ir * ir * ir;
-        const double t = fma(r2, s[5], fma(r1, s[4], r0 * s[3])) * ir3;
-        u0 = fma(s[3], ir, fma(r0, t, u0));
-        u1 = fma(s[4], ir, fma(r1, t, u1));
-        u2 = fma(s[5], ir, fma(r2, t, u2));
+        const double t = fma(r2, sp[5], fma(r1, sp[4], r0 * sp[3])) * ir3;
+        u[r][0] = fma(sp[3], ir, fma(r0, t, u[r][0]));
+        u[r][1] = fma(sp[4], ir, fma(r1, t, u[r][1]));
+        u[r][2] = fma(sp[5], ir, fma(r2, t, u[r][2]));
       }
+    }
   }
-  if (act) {
-    const int i = perm[k];
-    out[3 * (size_t)i] = u0;
-    out[3 * (size_t)i + 1] = u1;
-    out[3 * (size_t)i + 2] = u2;
-  }
+#pragma unroll
+  for (int r = 0; r < FL_R; ++r)
+    if (k[r] < t1) {
+      const int i = perm[k[r]];
+      out[3 * (size_t)i] = u[r][0];
+      out[3 * (size_t)i + 1] = u[r][1];
+      out[3 * (size_t)i + 2] = u[r][2];
+    }
 }
 
 // dst[:, j] = src[:, idx[j]] (columns of length m)
@@ -660,9 +710,17 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
   }
   // leaves: near field + L2P
   const int maxpts = g.fmm_max_leaf;  // the largest leaf sets the grid's second dimension
-  k_fmm_leaf<<<dim3(LV.nocc, (maxpts + 127) / 128), 128, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p,
-                                                                   F.surf.p, ns, LV.ctr.p, FMM_OUT * LV.r, LV.deq.p,
-                                                                   doS, doD, out);
+  const dim3 lg(LV.nocc, (maxpts + FL_T * FL_R - 1) / (FL_T * FL_R));
+  const double rad = FMM_OUT * LV.r;
+  if (doS && doD)
+    k_fmm_leaf<MODE_SD><<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p,
+                                             rad, LV.deq.p, out);
+  else if (doS)
+    k_fmm_leaf<MODE_S><<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p,
+                                            rad, LV.deq.p, out);
+  else
+    k_fmm_leaf<MODE_D><<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p,
+                                            rad, LV.deq.p, out);
   BPQN_CHECK_LAUNCH();
   g.prof.launches += 8;
 }
