@@ -872,6 +872,11 @@ def test_near_rotation_equals_brute_force(bp, p, gap, axis):
 
 
 # ------------------------------------------------------------------ NEXT-4: FMM far field (fmm_order)
+def torch_equal(a, b):
+    import torch
+    return bool(torch.equal(a, b))
+
+
 def _lattice(n, seed, spacing=2.02, jitter=0.01):
     rng = np.random.default_rng(seed)
     g1 = np.arange(n) * spacing
@@ -956,3 +961,7 @@ def test_fmm_lcp_mvp_vs_direct(bp):
     wd, _ = bp.lcp_mvp(gd, lam, gmres=gm)
     wf, _ = bp.lcp_mvp(gf, lam, gmres=gm)
     assert rel(wf.cpu().numpy(), wd.cpu().numpy()) <= 1e-5
+    # later MVPs replay the captured GMRES cycle graph (cuBLAS M2L GEMMs inside the capture): bit-identical
+    for _ in range(2):
+        w2, _ = bp.lcp_mvp(gf, lam, gmres=gm)
+        assert torch_equal(w2, wf)
