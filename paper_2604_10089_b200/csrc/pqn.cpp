@@ -10,6 +10,7 @@
 // crosses PCIe per MVP.  C^{-1} = (D + UU^T)^{-1} is applied by the Woodbury identity.
 #include <algorithm>
 #include <chrono>
+#include <immintrin.h>
 #include <omp.h>
 #include <cstdio>
 #include <cstdlib>
@@ -128,52 +129,78 @@ bool Bfgs::update(const Vec& s, const Vec& y, const Vec* Bs_in, double curv) {
 // earlier secant pair, so r reaches a few hundred, "full memory").
 static bool par(long long work) { return work > 200000; }
 
-// C[m x p] = A[m x k] B[p x k]^T (+ C if acc).  2 x 4 register blocks of C (each A / B row
-// chunk is reused 4 / 2 times from registers), the k loop vectorised; OpenMP over row pairs.
-static void gemm_nt(const double* A, const double* B, double* C, int m, int p, int k, bool acc) {
-  const int m2 = m / 2 * 2, p4 = p / 4 * 4;
-  auto put = [&](int i, int j, double s) { C[(size_t)i * p + j] = acc ? C[(size_t)i * p + j] + s : s; };
-  auto dot = [&](const double* a, const double* b) {
-    double s = 0.0;
-#pragma omp simd reduction(+ : s)
-    for (int e = 0; e < k; ++e) s += a[e] * b[e];
-    return s;
-  };
-#pragma omp parallel for schedule(static) if (par((long long)m * p * k))
-  for (int i = 0; i < m2; i += 2) {
-    const double* a0 = A + (size_t)i * k;
-    const double* a1 = a0 + k;
-    for (int j = 0; j < p4; j += 4) {
-      const double *b0 = B + (size_t)j * k, *b1 = b0 + k, *b2 = b1 + k, *b3 = b2 + k;
-      double s00 = 0, s01 = 0, s02 = 0, s03 = 0, s10 = 0, s11 = 0, s12 = 0, s13 = 0;
-#pragma omp simd reduction(+ : s00, s01, s02, s03, s10, s11, s12, s13)
-      for (int e = 0; e < k; ++e) {
-        const double x0 = a0[e], x1 = a1[e];
-        s00 += x0 * b0[e];
-        s01 += x0 * b1[e];
-        s02 += x0 * b2[e];
-        s03 += x0 * b3[e];
-        s10 += x1 * b0[e];
-        s11 += x1 * b1[e];
-        s12 += x1 * b2[e];
-        s13 += x1 * b3[e];
+// C[m x n] (ldc) += sign A[m x k] (lda) B[k x n] (ldb), row-major.  AVX2 micro-kernel: 4 rows x 8 columns of
+// C in 8 ymm accumulators, per k two B loads and four broadcasts of A; scalar edges; OpenMP over 4-row
+// blocks (each C element has one owner: deterministic).
+static void mk_gemm(double* C, int ldc, const double* A, int lda, const double* B, int ldb, int m, int n, int k,
+                    bool subtract) {
+  const int m4 = m / 4 * 4, n8 = n / 8 * 8;
+  const double sg = subtract ? -1.0 : 1.0;
+#pragma omp parallel for schedule(static) if (par((long long)m * n * k))
+  for (int i = 0; i < m4; i += 4) {
+    const double* l0 = A + (size_t)i * lda;
+    const double* l1 = l0 + lda;
+    const double* l2 = l1 + lda;
+    const double* l3 = l2 + lda;
+    for (int j = 0; j < n8; j += 8) {
+      double* c0 = C + (size_t)i * ldc + j;
+      __m256d a00 = _mm256_loadu_pd(c0), a01 = _mm256_loadu_pd(c0 + 4);
+      __m256d a10 = _mm256_loadu_pd(c0 + ldc), a11 = _mm256_loadu_pd(c0 + ldc + 4);
+      __m256d a20 = _mm256_loadu_pd(c0 + 2 * ldc), a21 = _mm256_loadu_pd(c0 + 2 * ldc + 4);
+      __m256d a30 = _mm256_loadu_pd(c0 + 3 * ldc), a31 = _mm256_loadu_pd(c0 + 3 * ldc + 4);
+      const double* u = B + j;
+      if (subtract) {
+        for (int kk = 0; kk < k; ++kk, u += ldb) {
+          const __m256d u0 = _mm256_loadu_pd(u), u1 = _mm256_loadu_pd(u + 4);
+          __m256d t = _mm256_broadcast_sd(l0 + kk);
+          a00 = _mm256_fnmadd_pd(t, u0, a00); a01 = _mm256_fnmadd_pd(t, u1, a01);
+          t = _mm256_broadcast_sd(l1 + kk);
+          a10 = _mm256_fnmadd_pd(t, u0, a10); a11 = _mm256_fnmadd_pd(t, u1, a11);
+          t = _mm256_broadcast_sd(l2 + kk);
+          a20 = _mm256_fnmadd_pd(t, u0, a20); a21 = _mm256_fnmadd_pd(t, u1, a21);
+          t = _mm256_broadcast_sd(l3 + kk);
+          a30 = _mm256_fnmadd_pd(t, u0, a30); a31 = _mm256_fnmadd_pd(t, u1, a31);
+        }
+      } else {
+        for (int kk = 0; kk < k; ++kk, u += ldb) {
+          const __m256d u0 = _mm256_loadu_pd(u), u1 = _mm256_loadu_pd(u + 4);
+          __m256d t = _mm256_broadcast_sd(l0 + kk);
+          a00 = _mm256_fmadd_pd(t, u0, a00); a01 = _mm256_fmadd_pd(t, u1, a01);
+          t = _mm256_broadcast_sd(l1 + kk);
+          a10 = _mm256_fmadd_pd(t, u0, a10); a11 = _mm256_fmadd_pd(t, u1, a11);
+          t = _mm256_broadcast_sd(l2 + kk);
+          a20 = _mm256_fmadd_pd(t, u0, a20); a21 = _mm256_fmadd_pd(t, u1, a21);
+          t = _mm256_broadcast_sd(l3 + kk);
+          a30 = _mm256_fmadd_pd(t, u0, a30); a31 = _mm256_fmadd_pd(t, u1, a31);
+        }
       }
-      put(i, j, s00);
-      put(i, j + 1, s01);
-      put(i, j + 2, s02);
-      put(i, j + 3, s03);
-      put(i + 1, j, s10);
-      put(i + 1, j + 1, s11);
-      put(i + 1, j + 2, s12);
-      put(i + 1, j + 3, s13);
+      _mm256_storeu_pd(c0, a00); _mm256_storeu_pd(c0 + 4, a01);
+      _mm256_storeu_pd(c0 + ldc, a10); _mm256_storeu_pd(c0 + ldc + 4, a11);
+      _mm256_storeu_pd(c0 + 2 * ldc, a20); _mm256_storeu_pd(c0 + 2 * ldc + 4, a21);
+      _mm256_storeu_pd(c0 + 3 * ldc, a30); _mm256_storeu_pd(c0 + 3 * ldc + 4, a31);
     }
-    for (int j = p4; j < p; ++j) {
-      put(i, j, dot(a0, B + (size_t)j * k));
-      put(i + 1, j, dot(a1, B + (size_t)j * k));
-    }
+    for (int r = 0; r < 4; ++r)
+      for (int j = n8; j < n; ++j) {
+        double acc = 0.0;
+        for (int kk = 0; kk < k; ++kk) acc += A[(size_t)(i + r) * lda + kk] * B[(size_t)kk * ldb + j];
+        C[(size_t)(i + r) * ldc + j] += sg * acc;
+      }
   }
-  for (int i = m2; i < m; ++i)
-    for (int j = 0; j < p; ++j) put(i, j, dot(A + (size_t)i * k, B + (size_t)j * k));
+  for (int i = m4; i < m; ++i)
+    for (int j = 0; j < n; ++j) {
+      double acc = 0.0;
+      for (int kk = 0; kk < k; ++kk) acc += A[(size_t)i * lda + kk] * B[(size_t)kk * ldb + j];
+      C[(size_t)i * ldc + j] += sg * acc;
+    }
+}
+
+// C[m x p] = A[m x k] B[p x k]^T (+ C if acc): B transposed once, then the micro-kernel GEMM
+static void gemm_nt(const double* A, const double* B, double* C, int m, int p, int k, bool acc) {
+  std::vector<double> Bt((size_t)k * p);
+  for (int j = 0; j < p; ++j)
+    for (int e = 0; e < k; ++e) Bt[(size_t)e * p + j] = B[(size_t)j * k + e];
+  if (!acc) std::fill(C, C + (size_t)m * p, 0.0);
+  mk_gemm(C, p, A, k, Bt.data(), p, m, p, k, false);
 }
 
 // in-place Cholesky K = L L^T (lower), false if not positive definite
@@ -303,23 +330,9 @@ static bool lu_solve_blocked(std::vector<double>& A, int n, Vec& b) {
           }
       }
     }
-    // trailing update A22 -= L21 U12 as one register-blocked GEMM (gemm_nt: C = A B^T with
-    // contiguous k = kb rows): L21 and U12^T are copied to contiguous panels first
+    // trailing update A22 -= L21 U12 in place (micro-kernel GEMM, row blocks over the OpenMP team)
     const int m = n - k1;
-    std::vector<double> Lp((size_t)m * kb), Up((size_t)m * kb), Cp((size_t)m * m);
-    for (int i = 0; i < m; ++i)
-      for (int k = 0; k < kb; ++k) {
-        Lp[(size_t)i * kb + k] = A[(size_t)(k1 + i) * n + k0 + k];
-        Up[(size_t)i * kb + k] = A[(size_t)(k0 + k) * n + k1 + i];
-      }
-    gemm_nt(Lp.data(), Up.data(), Cp.data(), m, m, kb, false);
-#pragma omp parallel for schedule(static) if (par((long long)m * m))
-    for (int i = 0; i < m; ++i) {
-      double* ri = &A[(size_t)(k1 + i) * n + k1];
-      const double* ci = &Cp[(size_t)i * m];
-#pragma omp simd
-      for (int j = 0; j < m; ++j) ri[j] -= ci[j];
-    }
+    mk_gemm(&A[(size_t)k1 * n + k1], n, &A[(size_t)k1 * n + k0], n, &A[(size_t)k0 * n + k1], n, m, m, kb, true);
   }
   if (!ok) return false;
   for (int k = 0; k < n; ++k)
@@ -543,7 +556,7 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
     std::vector<char> act;
     residual(al, L, z, act);
     double nr = infn(L);
-    std::vector<double> Ua, Va, CVa, Ui, CVi, blk((size_t)r * r);
+    std::vector<double> Ua, Va, Ui, UaT, CVaT, CViT;
     int jj;
     for (jj = 0; jj < jmax && nr > tol; ++jj) {
       g_pt.newton++;
@@ -552,35 +565,32 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
       std::vector<int> ia, ii;
       for (int e = 0; e < n; ++e) (act[e] ? ia : ii).push_back(e);
       const int na = (int)ia.size(), ni = (int)ii.size();
+      // compacted rows (A operands, [r][na|ni]) and transposed columns (B operands, [na|ni][r])
       Ua.assign((size_t)r * na, 0.0);
       Va.assign((size_t)r * na, 0.0);
-      CVa.assign((size_t)r * na, 0.0);
       Ui.assign((size_t)r * ni, 0.0);
-      CVi.assign((size_t)r * ni, 0.0);
+      UaT.assign((size_t)na * r, 0.0);
+      CVaT.assign((size_t)na * r, 0.0);
+      CViT.assign((size_t)ni * r, 0.0);
+#pragma omp parallel for schedule(static) if (par((long long)r * n * 8))
       for (int c = 0; c < r; ++c) {
         for (int t = 0; t < na; ++t) {
-          Ua[(size_t)c * na + t] = Um[(size_t)c * n + ia[t]];
+          const double u = Um[(size_t)c * n + ia[t]];
+          Ua[(size_t)c * na + t] = u;
+          UaT[(size_t)t * r + c] = u;
           Va[(size_t)c * na + t] = Vm[(size_t)c * n + ia[t]];
-          CVa[(size_t)c * na + t] = CV[(size_t)c * n + ia[t]];
+          CVaT[(size_t)t * r + c] = CV[(size_t)c * n + ia[t]];
         }
         for (int t = 0; t < ni; ++t) {
           Ui[(size_t)c * ni + t] = Um[(size_t)c * n + ii[t]];
-          CVi[(size_t)c * ni + t] = CV[(size_t)c * n + ii[t]];
+          CViT[(size_t)t * r + c] = CV[(size_t)c * n + ii[t]];
         }
       }
       std::vector<double> J((size_t)d * d, 0.0);
-      auto put = [&](int r0, int c0, double sgn) {
-        for (int a = 0; a < r; ++a)
-          for (int b = 0; b < r; ++b) J[(size_t)(r0 + a) * d + c0 + b] = sgn * blk[(size_t)a * r + b];
-      };
-      gemm_nt(Ua.data(), Ua.data(), blk.data(), r, r, na, false);
-      put(0, 0, 1.0);
-      gemm_nt(Ui.data(), CVi.data(), blk.data(), r, r, ni, false);
-      put(0, r, 1.0);
-      gemm_nt(Va.data(), Ua.data(), blk.data(), r, r, na, false);
-      put(r, 0, 1.0);
-      gemm_nt(Va.data(), CVa.data(), blk.data(), r, r, na, false);
-      put(r, r, -1.0);
+      mk_gemm(&J[0], d, Ua.data(), na, UaT.data(), r, r, r, na, false);                   // U^T Lam U
+      mk_gemm(&J[r], d, Ui.data(), ni, CViT.data(), r, r, r, ni, false);                  // U^T (I - Lam) CV
+      mk_gemm(&J[(size_t)r * d], d, Va.data(), na, UaT.data(), r, r, r, na, false);      // V^T Lam U
+      mk_gemm(&J[(size_t)r * d + r], d, Va.data(), na, CVaT.data(), r, r, r, na, true);  // -V^T Lam CV
       for (int i = 0; i < d; ++i) J[(size_t)i * d + i] += 1.0;
       double t_2 = now_s();
       g_pt.jac += t_2 - t_1;
