@@ -136,7 +136,7 @@ static void mk_gemm(double* C, int ldc, const double* A, int lda, const double* 
                     bool subtract) {
   const int m4 = m / 4 * 4, n8 = n / 8 * 8;
   const double sg = subtract ? -1.0 : 1.0;
-#pragma omp parallel for schedule(static) if (par((long long)m * n * k))
+#pragma omp parallel for schedule(static) if ((long long)m * n * k > 4000000)  // fork/join pays only here
   for (int i = 0; i < m4; i += 4) {
     const double* l0 = A + (size_t)i * lda;
     const double* l1 = l0 + lda;
@@ -572,7 +572,7 @@ Vec weighted_prox(const Bfgs& q, const Vec& xt, double tol, int jmax, int* iters
       UaT.assign((size_t)na * r, 0.0);
       CVaT.assign((size_t)na * r, 0.0);
       CViT.assign((size_t)ni * r, 0.0);
-#pragma omp parallel for schedule(static) if (par((long long)r * n * 8))
+#pragma omp parallel for schedule(static) if ((long long)r * n > 1000000)
       for (int c = 0; c < r; ++c) {
         for (int t = 0; t < na; ++t) {
           const double u = Um[(size_t)c * n + ia[t]];
