@@ -265,6 +265,9 @@ void blas_dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double alp
                 const double* B, int ldb, double beta, double* C, int ldc);
 void blas_dtrsm(cudaStream_t st, int side, int trans, int m, int n, const double* L, int ldl, double* B, int ldb);
 void dev_potrf(cudaStream_t st, double* A, int n, int lda);
+bool blas_dgemm_grouped(cudaStream_t st, int G, const int* m, const int* n, const int* k, const double* alpha,
+                        const double* const* A_dev, const int* lda, const double* const* B_dev, const int* ldb,
+                        double* const* C_dev, const int* ldc);
 
 // FMM (fmm.cu): tree and lists from the host node positions; the K1 coarse sum into out [N][3]
 void fmm_build(Geom& g, const std::vector<double>& X_host, cudaStream_t st);

@@ -37,11 +37,15 @@ typedef int (*cublasSetStream_t)(void*, cudaStream_t);
 typedef int (*cublasDgemm_t)(void*, int, int, int, int, int, const double*, const double*, int, const double*, int,
                              const double*, double*, int);
 typedef int (*cublasDtrsm_t)(void*, int, int, int, int, int, int, const double*, const double*, int, double*, int);
+typedef int (*cublasDgemmGrouped_t)(void*, const int*, const int*, const int*, const int*, const int*, const double*,
+                                    const double* const*, const int*, const double* const*, const int*, const double*,
+                                    double* const*, const int*, int, const int*);
 struct Cublas {
   cublasCreate_t create = nullptr;
   cublasSetStream_t setStream = nullptr;
   cublasDgemm_t dgemm = nullptr;
   cublasDtrsm_t dtrsm = nullptr;
+  cublasDgemmGrouped_t dgemm_grouped = nullptr;  // optional (cuBLAS >= 12.5)
   std::string why;
 };
 // one cuBLAS handle per calling thread (distinct geometry handles may be used from different threads)
@@ -61,6 +65,7 @@ static Cublas& cublas() {
     c.setStream = reinterpret_cast<cublasSetStream_t>(dlsym(h, "cublasSetStream_v2"));
     c.dgemm = reinterpret_cast<cublasDgemm_t>(dlsym(h, "cublasDgemm_v2"));
     c.dtrsm = reinterpret_cast<cublasDtrsm_t>(dlsym(h, "cublasDtrsm_v2"));
+    c.dgemm_grouped = reinterpret_cast<cublasDgemmGrouped_t>(dlsym(h, "cublasDgemmGroupedBatched"));
     if (!c.create || !c.setStream || !c.dgemm || !c.dtrsm) c.why = "cuBLAS lacks a required symbol";
   });
   if (!c.why.empty()) throw Error{BPQN_ERR_CUDA, c.why};
@@ -94,6 +99,23 @@ void blas_dgemm(cudaStream_t st, int ta, int tb, int m, int n, int k, double alp
     throw Error{BPQN_ERR_CUDA, "cublasDgemm failed"};
 }
 constexpr int CB_LEFT = 0, CB_RIGHT = 1, CB_LOWER = 0, CB_NONUNIT = 0;
+// G column-major GEMMs C_g = alpha_g A_g B_g (no transposes, beta 0) in one cuBLAS grouped-batched call (one
+// problem per group); pointer arrays in device memory.  Returns false if the library lacks the entry point.
+bool blas_dgemm_grouped(cudaStream_t st, int G, const int* m, const int* n, const int* k, const double* alpha,
+                        const double* const* A_dev, const int* lda, const double* const* B_dev, const int* ldb,
+                        double* const* C_dev, const int* ldc) {
+  Cublas& cb = cublas();
+  if (!cb.dgemm_grouped) return false;
+  void* h = cublas_handle();
+  if (cb.setStream(h, st) != 0) throw Error{BPQN_ERR_CUDA, "cublasSetStream failed"};
+  std::vector<int> tr(G, CUBLAS_OP_N_), one(G, 1);
+  std::vector<double> beta(G, 0.0);
+  if (cb.dgemm_grouped(h, tr.data(), tr.data(), m, n, k, alpha, A_dev, lda, B_dev, ldb, beta.data(), C_dev, ldc, G,
+                       one.data()) != 0)
+    throw Error{BPQN_ERR_CUDA, "cublasDgemmGroupedBatched failed"};
+  return true;
+}
+
 void blas_dtrsm(cudaStream_t st, int side, int trans, int m, int n, const double* L, int ldl, double* B, int ldb) {
   Cublas& cb = cublas();
   void* h = cublas_handle();

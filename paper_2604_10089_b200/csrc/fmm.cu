@@ -40,6 +40,12 @@ struct FmmLevel {
   int n_pairs = 0;
   std::vector<int> off_start;  // [FMM_NOFF + 1]
   DBuf<int> m2l_src, tgt_ptr, tgt_pos;
+  // the level's M2L GEMMs as one grouped-batched cuBLAS call: per non-empty offset the sizes and the
+  // device pointers of (M2L_o, its gathered sources, its outputs)
+  std::vector<int> g_m, g_n, g_k, g_lda, g_ldb, g_ldc;
+  std::vector<double> g_alpha;
+  DBuf<const double*> g_A, g_B;
+  DBuf<double*> g_C;
   void reset() {
     nocc = 0;
     r = 0.0;
@@ -641,6 +647,30 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
     F.bufC.alloc(m * maxcols);
     F.buf_cols = maxcols;
   }
+  // grouped-batched M2L: per level the non-empty offsets' GEMMs (pointers into the fixed buffers)
+  {
+    const int mm3 = 3 * F.ns, muu = mm3 + 1;
+    for (int l = 2; l <= L; ++l) {
+      FmmLevel& V = F.lev[l];
+      V.g_m.clear(); V.g_n.clear(); V.g_k.clear(); V.g_lda.clear(); V.g_ldb.clear(); V.g_ldc.clear();
+      V.g_alpha.clear();
+      std::vector<const double*> pa, pb;
+      std::vector<double*> pc;
+      for (int o = 0; o < FMM_NOFF; ++o) {
+        const int c0 = V.off_start[o], cnt = V.off_start[o + 1] - c0;
+        if (!cnt) continue;
+        V.g_m.push_back(mm3); V.g_n.push_back(cnt); V.g_k.push_back(muu);
+        V.g_lda.push_back(mm3); V.g_ldb.push_back(muu); V.g_ldc.push_back(mm3);
+        V.g_alpha.push_back(1.0 / V.r);
+        pa.push_back(F.M2L.p + (size_t)o * mm3 * muu);
+        pb.push_back(F.bufB.p + (size_t)c0 * muu);
+        pc.push_back(F.bufC.p + (size_t)c0 * mm3);
+      }
+      fmm_upload(V.g_A, pa, st);
+      fmm_upload(V.g_B, pb, st);
+      fmm_upload(V.g_C, pc, st);
+    }
+  }
   size_t maxocc = 1;
   for (int l = 0; l <= L; ++l) maxocc = std::max(maxocc, (size_t)F.lev[l].nocc);
   F.tmpA.alloc(m * maxocc);
@@ -696,12 +726,17 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
     if (V.n_pairs > 0) {
       k_fmm_gather<<<fgrid((size_t)mu * V.n_pairs), 256, 0, st>>>(V.ueq.p, mu, V.m2l_src.p, V.n_pairs, F.bufB.p);
       BPQN_CHECK_LAUNCH();
-      for (int o = 0; o < FMM_NOFF; ++o) {
-        const int c0 = V.off_start[o], cnt = V.off_start[o + 1] - c0;
-        if (!cnt) continue;
-        blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, cnt, mu, 1.0 / V.r, F.M2L.p + o * mmu, m, F.bufB.p + (size_t)c0 * mu,
-                   mu, 0.0, F.bufC.p + (size_t)c0 * m, m);
-      }
+      static const bool grouped = !(getenv("BPQN_FMM_GROUPED") && getenv("BPQN_FMM_GROUPED")[0] == '0');
+      const int G = (int)V.g_m.size();
+      if (!(grouped && G > 0 &&
+            blas_dgemm_grouped(st, G, V.g_m.data(), V.g_n.data(), V.g_k.data(), V.g_alpha.data(), V.g_A.p,
+                               V.g_lda.data(), V.g_B.p, V.g_ldb.data(), V.g_C.p, V.g_ldc.data())))
+        for (int o = 0; o < FMM_NOFF; ++o) {
+          const int c0 = V.off_start[o], cnt = V.off_start[o + 1] - c0;
+          if (!cnt) continue;
+          blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, cnt, mu, 1.0 / V.r, F.M2L.p + o * mmu, m,
+                     F.bufB.p + (size_t)c0 * mu, mu, 0.0, F.bufC.p + (size_t)c0 * m, m);
+        }
       k_fmm_m2l_reduce<<<fgrid((size_t)m * V.nocc), 256, 0, st>>>(V.dck.p, m, V.nocc, V.tgt_ptr.p, V.tgt_pos.p,
                                                                   F.bufC.p);
       BPQN_CHECK_LAUNCH();
