@@ -260,7 +260,7 @@ __device__ __forceinline__ void fmm_pair_fast(double x0, double x1, double x2, c
 
 // Leaves: near field (27 neighbour leaves) + L2P from the leaf's downward equivalent density; two targets per
 // thread share every staged source; writes out[node] in the original order
-constexpr int FL_T = 128, FL_R = 2;
+constexpr int FL_T = 64, FL_R = 3;
 template <int MODE>
 __global__ void __launch_bounds__(FL_T) k_fmm_leaf(const double* __restrict__ rec, const int* __restrict__ start,
                                                    const int* __restrict__ nbr, const int* __restrict__ perm,
