@@ -965,3 +965,16 @@ def test_fmm_lcp_mvp_vs_direct(bp):
     for _ in range(2):
         w2, _ = bp.lcp_mvp(gf, lam, gmres=gm)
         assert torch_equal(w2, wf)
+
+
+def test_fmm_geometry_update_equals_fresh(bp):
+    """bpqn_geometry_update on an FMM handle rebuilds the tree and lists: it equals a fresh FMM handle at the
+    new centres bit for bit (the unit-box operators are kept)."""
+    C = _lattice(4, 49)
+    C1 = 1.01 * C + np.array([0.2, -0.1, 0.3])
+    g = _fmm_geometry(bp, C, 6, 8)
+    bp.geometry_update(g, C1)
+    h = _fmm_geometry(bp, C1, 6, 8)
+    rng = np.random.default_rng(50)
+    f, q = T(rng.standard_normal((g.N, 3))), T(rng.standard_normal((g.N, 3)))
+    assert np.array_equal(bp.layer_apply(g, f=f, q=q).cpu().numpy(), bp.layer_apply(h, f=f, q=q).cpu().numpy())
