@@ -640,9 +640,13 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
     // lo_dense = 2 (auto): form A^ when the LCP looks hard -- at least a quarter of the contacts start
     // approaching (b_l < 0), where Bi-PQN needs hundreds of lo MVPs (c4: 41 % negative, 386 lo MVPs);
     // warm online steps with a few approaching contacts need tens and stay matrix-free
+    // In a time-stepping loop the same handles solve one LCP per step: the auto mode also forms A^ when the
+    // previous Bi-PQN solve on this lo handle needed >= Nc / 4 lo MVPs (forming costs about that many
+    // matrix-free lo MVPs: c4 lo 9.9 s ~ 116 x 85 ms; p_lo = 4 1.2 s ~ 170 x 7 ms).
     int n_neg = 0;
     for (double v : b) n_neg += v < 0.0;
-    const bool want_dense = o.lo_dense == 1 || (o.lo_dense == 2 && 4 * n_neg >= nc);
+    const bool busy_before = bi && lo->last_lo_mvps >= 0 && 4 * lo->last_lo_mvps >= nc;
+    const bool want_dense = o.lo_dense == 1 || (o.lo_dense == 2 && (4 * n_neg >= nc || busy_before));
     if (bi && want_dense) {
       try {
         densify_lcp(*lo, glo, Ahat, dls, s);
@@ -675,6 +679,7 @@ int bpqn_solve_lcp(bpqn_geom_t hi, bpqn_geom_t lo, const double* b_dev, double* 
       term = r.termination;
       hi_mvps = r.hi_mvps;
       lo_mvps = r.lo_mvps;
+      lo->last_lo_mvps = r.lo_mvps;
       kkt = r.kkt;
       kkt_rel = r.kkt_rel;
       secant_res = r.secant_residual;
