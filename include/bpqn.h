@@ -120,6 +120,10 @@ typedef struct {
                                  operator (8 (3 N_lo)^2 bytes) does not fit.  2: auto -- form A^ when at least
                                  a quarter of the b_l are negative (a hard LCP with hundreds of lo MVPs).
                                  0 (default): matrix-free */
+  int warm_start;             /* bpqn_dvi_step only: 1 (default) starts each step's LCP from the previous step's
+                                 lambda of the same sphere pairs (0 for new pairs) -- Alg. 1 / 3's x^(-1)
+                                 (P:336); 0: from lambda = 0.  The solution is the same unique lambda*
+                                 (P:190); only the iteration counts change. */
 } bpqn_solve_opts;
 
 typedef struct {
@@ -230,7 +234,8 @@ typedef struct {
  * NEXT-2) on the spheres of `hi` (and its low-fidelity twin `lo`, or NULL):
  *   contacts (gap < delta) at the current centres;
  *   U_nc = M_slip(F_nc, 0; u_s) with the Janus slip of the current axes (R13, B = slip_B);
- *   b = Phi/dt + D^T U_nc;  lambda from bpqn_solve_lcp(hi, lo, b, 0, o);
+ *   b = Phi/dt + D^T U_nc;  lambda from bpqn_solve_lcp(hi, lo, b, x_init, o), x_init = the previous
+ *   step's lambda of the same pairs (o->warm_start, default) or 0;
  *   U = U_nc + M D lambda;  c <- c + dt U,  a <- normalise(a + dt Omega x a)
  *   (orientation reading R32; quaternions are out of scope);
  * then both handles are moved to the new centres (bpqn_geometry_update).

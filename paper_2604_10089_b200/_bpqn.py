@@ -35,7 +35,7 @@ class SolveOpts(ctypes.Structure):
                 ("tau", c_double), ("refresh_period", c_int), ("sub_eps_factor", c_double),
                 ("sub_k_max", c_int), ("prox_tol", c_double), ("prox_jmax", c_int), ("curv_skip", c_double),
                 ("gm_hi", GmresOpts), ("gm_lo", GmresOpts), ("cost_ratio", c_double), ("sub_forcing", c_double),
-                ("verify_secants", c_int), ("lo_dense", c_int)]
+                ("verify_secants", c_int), ("lo_dense", c_int), ("warm_start", c_int)]
 
 
 class Report(ctypes.Structure):

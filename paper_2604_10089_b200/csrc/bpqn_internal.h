@@ -207,7 +207,9 @@ struct Geom {
   DBuf<double> sh_own_send, sh_own_recv, sh_own_rs_send, sh_own_rs_recv;
   // far-field FMM replacing K1 (fmm.cu; bpqn_disc_opts.fmm_order > 0)
   int fmm_order = 0, fmm_max_leaf = 0;
-  int last_lo_mvps = -1;  // lo handle: lo MVPs of the last Bi-PQN solve it served (the lo_dense auto rule)
+  int last_lo_mvps = -1;
+  std::vector<long long> dvi_keys;  // DVI warm start: the last step's contact pairs (i Np + j, sorted) and lambda
+  std::vector<double> dvi_lam;  // lo handle: lo MVPs of the last Bi-PQN solve it served (the lo_dense auto rule)
   struct Fmm* fmm = nullptr;
   bool sharded() const { return shard_world > 1 || nccl_comm != nullptr; }
   ~Geom();

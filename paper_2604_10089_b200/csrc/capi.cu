@@ -247,6 +247,7 @@ void bpqn_default_solve_opts(bpqn_solve_opts* o) {
   o->sub_forcing = 0.0;
   o->verify_secants = 0;
   o->lo_dense = 0;
+  o->warm_start = 1;
 }
 
 int bpqn_geometry_init(bpqn_geom_t* out, int n_spheres, const double* centers_host, double radius, double mu,
@@ -811,7 +812,19 @@ int bpqn_dvi_step(bpqn_geom_t hi, bpqn_geom_t lo, double* centers_host, double* 
       lam.alloc(nc);
       launch_dt_gather(g, uo_nc.p, bvec.p, 1.0, nullptr, s);
       launch_axpby(bvec.p, 1.0 / dt, g.gaps.p, 1.0, nc, s);
-      BPQN_CUDA(cudaMemsetAsync(lam.p, 0, sizeof(double) * nc, s));
+      // x^(-1): the previous step's lambda of the same sphere pairs (warm start), 0 for new pairs
+      std::vector<int> ph(2 * (size_t)nc);
+      BPQN_CUDA(cudaMemcpyAsync(ph.data(), g.pairs.p, 2 * sizeof(int) * nc, cudaMemcpyDeviceToHost, s));
+      BPQN_CUDA(cudaStreamSynchronize(s));
+      std::vector<long long> keys(nc);
+      for (int l = 0; l < nc; ++l) keys[l] = (long long)ph[2 * l] * np + ph[2 * l + 1];
+      std::vector<double> x0(nc, 0.0);
+      if (o.warm_start && !g.dvi_keys.empty())
+        for (int l = 0; l < nc; ++l) {
+          auto it = std::lower_bound(g.dvi_keys.begin(), g.dvi_keys.end(), keys[l]);
+          if (it != g.dvi_keys.end() && *it == keys[l]) x0[l] = g.dvi_lam[it - g.dvi_keys.begin()];
+        }
+      BPQN_CUDA(cudaMemcpyAsync(lam.p, x0.data(), sizeof(double) * nc, cudaMemcpyHostToDevice, s));
       R.solve_rc = bpqn_solve_lcp(hi, lo, bvec.p, lam.p, &o, &R.lcp, stream);
       if (R.solve_rc != BPQN_OK && R.solve_rc != BPQN_ERR_NOCONV && R.solve_rc != BPQN_ERR_STALLED)
         return R.solve_rc;
@@ -824,6 +837,19 @@ int bpqn_dvi_step(bpqn_geom_t hi, bpqn_geom_t lo, double* centers_host, double* 
       BPQN_CUDA(cudaStreamSynchronize(s));
       for (size_t i = 0; i < U.size(); ++i) U[i] += Uc[i];
       for (double v : lh) R.active_contacts += v > 0.0;
+      // keep (pair, lambda) sorted by pair for the next step's warm start (contact lists are lexicographic)
+      std::vector<int> ord(nc);
+      for (int l = 0; l < nc; ++l) ord[l] = l;
+      std::sort(ord.begin(), ord.end(), [&](int a2, int b2) { return keys[a2] < keys[b2]; });
+      g.dvi_keys.resize(nc);
+      g.dvi_lam.resize(nc);
+      for (int l = 0; l < nc; ++l) {
+        g.dvi_keys[l] = keys[ord[l]];
+        g.dvi_lam[l] = lh[ord[l]];
+      }
+    } else {
+      g.dvi_keys.clear();
+      g.dvi_lam.clear();
     }
     // forward Euler on centres and Janus axes
     std::vector<double> cn(3 * (size_t)np), an(3 * (size_t)np);
