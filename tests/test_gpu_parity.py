@@ -978,3 +978,26 @@ def test_fmm_geometry_update_equals_fresh(bp):
     rng = np.random.default_rng(50)
     f, q = T(rng.standard_normal((g.N, 3))), T(rng.standard_normal((g.N, 3)))
     assert np.array_equal(bp.layer_apply(g, f=f, q=q).cpu().numpy(), bp.layer_apply(h, f=f, q=q).cpu().numpy())
+
+
+def test_fmm_bi_pqn_solve_matches_direct(bp):
+    """A Bi-PQN LCP solve whose high fidelity uses the FMM far field (order 10) reaches the direct solve's
+    lambda* to the FMM accuracy (the LCP is strongly monotone: a perturbed A moves lambda* by
+    O(|dA|), Lemma 2)."""
+    C = _lattice(4, 51, spacing=2.03, jitter=0.015)
+    gd = bp.Geometry(C, 6)
+    gf = _fmm_geometry(bp, C, 6, 10, 2)
+    lo = bp.Geometry(C, 4)
+    pr, nr, gp = bp.contacts(gd, 0.1)
+    bp.set_contacts(gf, pr, nr, gp)
+    bp.set_contacts(lo, pr, nr, gp)
+    b = T(np.random.default_rng(52).uniform(-0.05, 0.02, gd.nc))
+    out = []
+    for g in (gd, gf):
+        o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-10)
+        o.gm_hi.tol = 1e-11
+        o.gm_lo.tol = 1e-11
+        lam, rep, rc = bp.solve_lcp(g, lo, b, T(np.zeros(gd.nc)), opts=o)
+        assert rc == 0
+        out.append(lam.cpu().numpy())
+    assert rel(out[1], out[0]) <= 1e-5, rel(out[1], out[0])
