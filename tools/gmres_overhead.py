@@ -2,7 +2,7 @@
 the captured cycle graph (device-side stopping test, one host sync per restart cycle) against the
 kernel time of the operator alone (K1 + K2 + K3 from the library's CUDA events).  The difference
 is the per-iteration overhead (CGS2 / Givens kernels, launch gaps).
-  python tools/gmres_overhead.py [configs...]   (1, 2, 4; "4lo" = c4 centres at p = 8)"""
+  python tools/gmres_overhead.py [configs...]   (1, 2, 4; "4lo" = c4 centres at p = 8; "4p4" = at p = 4)"""
 import json
 import os
 import sys
@@ -19,7 +19,7 @@ from synth import lambda_test, make_config  # noqa: E402
 def run(tag):
     c = int(tag[0])
     cfg = make_config(c)
-    p = cfg["p_lo"] if tag.endswith("lo") else cfg["p"]
+    p = cfg["p_lo"] if tag.endswith("lo") else (int(tag.split("p")[1]) if "p" in tag else cfg["p"])
     g = bp.Geometry(cfg["centers"], p)
     bp.contacts(g, cfg["delta"])
     lam = torch.tensor(lambda_test(c, g.nc, 0), device="cuda")
