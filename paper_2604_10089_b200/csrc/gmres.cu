@@ -547,7 +547,8 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   A.z = g.gm_z.p;
   A.vin = g.gm_vin.p;
   A.red = g.red.p;
-  A.nbx = std::max(1, std::min<int>(2 * g.sms, (int)((n / 2 + AT - 1) / AT)));
+  // up to 2 blocks per SM, slices of >= 64 double2: small systems (c1, p_lo = 4) still fill the GPU
+  A.nbx = std::max(1, std::min<int>(2 * g.sms, (int)((n / 2 + 63) / 64)));
   A.chunk2 = (int)((n / 2 + A.nbx - 1) / A.nbx);
   A.ctl = ctl;
   A.S = S;
