@@ -54,6 +54,8 @@ def parse():
     ap.add_argument("--solvers", default="bi,mono,bb")  # comma list of bi, mono, bb (BB-PGD)
     ap.add_argument("--no-fmm", action="store_true")    # skip the N >> 3e5 FMM context run (NEXT-4)
     ap.add_argument("--fmm-order", type=int, default=10)
+    ap.add_argument("--no-refine", action="store_true")  # skip the FMM-refinement MVP / solve at the bench config
+    ap.add_argument("--refine-order", type=int, default=6)  # FMM order of the refinement's Krylov steps
     ap.add_argument("--no-paper", action="store_true")  # skip the paper-setting context runs (p=8/4)
     ap.add_argument("--replicas", action="store_true")  # N > 1: independent replicas instead of the sharded MVP
     ap.add_argument("--shard-callback", action="store_true")  # N > 1: sharded via torch.distributed callbacks
@@ -354,6 +356,8 @@ def run_ours(args, ws, rank, local):
     k_g = float(np.mean(gm_iters))
     n_pairs_step = (k_g + 1.0) * g.N * g.N      # nominal N^2 per operator pass (RHS S-pass + k_g D-passes)
 
+    w_ref = w.clone()   # the direct MVP at the bench tolerance (reference for the FMM refinement key)
+
     # e2e: the same MVP through the C ABI from pinned HOST lambda to a HOST w
     lam_pin = torch.tensor(lam_h, dtype=torch.float64).pin_memory()
     w_pin = torch.empty(nc, dtype=torch.float64).pin_memory()
@@ -416,6 +420,9 @@ def run_ours(args, ws, rank, local):
             line[key] = run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth)
     del g
     torch.cuda.empty_cache()
+    if not args.no_refine and not shard:
+        line["mvp_fmm_refine"] = run_fmm_refine(args, cfg, dev, stream, lam, w_ref, ms_per_step / per_unit,
+                                                pairs, nrm, gaps, flush)
 
     if not args.no_c5 and ws == 1:
         line["layer_apply_c5"] = run_c5(args, dev, stream)
@@ -438,13 +445,14 @@ def run_ours(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
-def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
+def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi", relax=False):
     """One full LCP solve at the bench config: b from the Janus-slip non-collisional
     mobility solve, then Bi-PQN (Alg. 3) with the low fidelity at p_lo
     (or Mono-PQN when the config has none), paper-mode tolerances."""
     import torch
     import paper_2604_10089_b200 as bp
-    gmo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart, recycle=int(args.recycle))
+    gmo = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart, recycle=int(args.recycle),
+                                relax_fmm=int(relax))
     t0 = time.time()
     lo = None
     if meth == "bi" and cfg.get("p_lo"):
@@ -478,6 +486,9 @@ def run_solve(args, cfg, g, pairs, nrm, gaps, dev, meth="bi"):
            "rc": rc, "lo_geometry_init_s": round(t_lo_init, 3),
            "negative_b_fraction": float((b < 0).double().mean().item()),
            "active_contacts": int((lam > 0).sum().item())}
+    if relax:
+        out["hi_mvps_with"] = "FMM refinement (relax_fmm = 1, fmm_order %d): Krylov steps with the FMM far field, " \
+                              "every cycle from the direct residual" % args.refine_order
     out.update({k: r[k] for k in ("iterations", "hi_mvps", "lo_mvps", "lo_mvps_init", "lo_dense_columns",
                                   "lo_dense_gmres_iters", "ms_lo_dense", "e_mvps", "cost_ratio", "kkt_abs",
                                   "gmres_iters_hi", "gmres_iters_lo", "ms_hi", "ms_lo", "termination")})
@@ -555,6 +566,63 @@ def run_paper_setting(args, dev, stream):
                              "source": "PAPER.md Table 3 (P:613-629): 6x6x6 BB-PGD collision 5d 0h 25m / 200 steps"}}
     hi.close()
     lo.close()
+    return out
+
+
+def run_fmm_refine(args, cfg, dev, stream, lam, w_ref, ms_direct, pairs, nrm, gaps, flush):
+    """The same c4 LCP MVP (same lambda, contacts, GMRES tolerance) with FMM-accelerated refinement
+    (bpqn_gmres_opts.relax_fmm, NEXT-4; the paper's far field is an FMM): every Krylov step applies the
+    operator with an order-`refine_order` FMM far field, each cycle starts from -- and the solve stops only on --
+    the DIRECT residual b - A x (all-pairs K1), so the MVP meets the GMRES tolerance for the direct operator.
+    Timed like the main MVP (CUDA events per MVP, L2 flushed between MVPs, contacts recomputed); its difference
+    from the direct MVP is at the tolerance level.  Then the Bi-PQN solve with these hi MVPs."""
+    import torch
+    import paper_2604_10089_b200 as bp
+    op = bp.default_disc_opts()
+    op.fmm_order = args.refine_order
+    t0 = time.time()
+    g = bp.Geometry(cfg["centers"], cfg["p"], cfg["radius"], cfg["mu"], opts=op)
+    torch.cuda.synchronize()
+    t_init = time.time() - t0
+    bp.contacts(g, cfg["delta"])
+    w = torch.empty_like(w_ref)
+    gm = bp.default_gmres_opts(tol=args.gmres_tol, restart=args.gmres_restart, relax_fmm=1)
+    for _ in range(max(1, args.warmup)):
+        bp.lcp_mvp(g, lam, out=w, gmres=gm)
+    ms, its, fmm, dres, res = [], [], [], [], []
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        bp.contacts(g, cfg["delta"])
+        _, st = bp.lcp_mvp(g, lam, out=w, gmres=gm)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+        its.append(st.iters)
+        fmm.append(st.fmm_applies)
+        dres.append(st.applies - st.fmm_applies)
+        res.append(st.rel_resid)
+    u = torch.empty((g.N, 3), dtype=torch.float64, device=dev)
+    q = torch.tensor(np.random.default_rng(20264000).standard_normal((g.N, 3)), device=dev)
+    bp.layer_apply(g, None, q, out=u)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    bp.layer_apply(g, None, q, out=u)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    out = {"ms_per_mvp": float(np.mean(ms)), "speedup_vs_direct_mvp": ms_direct / float(np.mean(ms)),
+           "fmm_order": args.refine_order, "gmres_tol": args.gmres_tol, "fmm_krylov_steps_per_mvp": float(np.mean(fmm)),
+           "direct_residuals_per_mvp": float(np.mean(dres)), "gmres_iters_per_mvp": float(np.mean(its)),
+           "final_direct_rel_residual_max": float(np.max(res)),
+           "mvp_rel_l2_vs_direct_mvp": float(torch.linalg.norm(w - w_ref) / torch.linalg.norm(w_ref)),
+           "ms_fmm_layer_apply_d": e0.elapsed_time(e1), "geometry_init_s": round(t_init, 2),
+           "timing": "CUDA events per MVP (contacts + MVP), L2 flushed between MVPs, %d MVPs" % args.steps}
+    if not args.no_solve:
+        pr, nr, gp = bp.contacts(g, cfg["delta"])
+        out["lcp_solve_bi"] = run_solve(args, cfg, g, pr, nr, gp, dev, args.solvers.split(",")[0], relax=True)
+    del g, u
+    torch.cuda.empty_cache()
     return out
 
 

@@ -80,6 +80,18 @@ typedef struct {
                          -- never inside an MVP: without a reserved store recycle = 1 is a no-op.
                          A solve's pair is kept if its new direction has norm > 1e-8 |rhs|.
                          0: off. */
+  int relax_fmm;      /* 1: FMM-accelerated refinement on a handle built with fmm_order > 0 (NEXT-4;
+                         the paper's far field is an FMM): every Krylov step applies the
+                         operator with the FMM far field, each restart cycle reduces its own residual
+                         by relax_delta, and every cycle starts from -- and the solve stops only on --
+                         the DIRECT residual b - A x (the all-pairs K1).  Defect correction with an
+                         approximate inner operator: the returned x meets tol for the direct operator,
+                         exactly like relax_fmm = 0 on a direct handle.  Everything outside the Krylov
+                         steps (the mobility right-hand side S[f], the residuals) is direct.
+                         BPQN_ERR_INVALID on a handle without an FMM.  0 (default): off -- an FMM
+                         handle then uses the FMM for every application, a direct handle the direct
+                         sum.  Measured: profiles/r02_fmm_refine.md. */
+  double relax_delta; /* residual reduction per refinement cycle; <= 0 (default) -> 3e-3 */
 } bpqn_gmres_opts;
 
 typedef struct {
@@ -88,6 +100,8 @@ typedef struct {
   double rel_resid;   /* final relative residual estimate ||b - A x|| / ||b|| */
   double ms;          /* device time of the whole call (CUDA events) */
   int applies;        /* operator applications (iterations + restart / initial-guess residuals) */
+  int fmm_applies;    /* of which with the FMM far field (relax_fmm, or an FMM handle); with relax_fmm
+                         restarts counts the refinement cycles after the first */
 } bpqn_gmres_stats;
 
 typedef struct {

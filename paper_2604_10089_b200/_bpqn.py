@@ -22,12 +22,12 @@ class DiscOpts(ctypes.Structure):
 
 class GmresOpts(ctypes.Structure):
     _fields_ = [("tol", c_double), ("restart", c_int), ("max_iters", c_int), ("precond", c_int),
-                ("recycle", c_int)]
+                ("recycle", c_int), ("relax_fmm", c_int), ("relax_delta", c_double)]
 
 
 class GmresStats(ctypes.Structure):
     _fields_ = [("iters", c_int), ("restarts", c_int), ("rel_resid", c_double), ("ms", c_double),
-                ("applies", c_int)]
+                ("applies", c_int), ("fmm_applies", c_int)]
 
 
 class SolveOpts(ctypes.Structure):
@@ -151,9 +151,14 @@ def default_disc_opts():
     return o
 
 
-def default_gmres_opts(tol=None, restart=None, max_iters=None, precond=None, recycle=None):
+def default_gmres_opts(tol=None, restart=None, max_iters=None, precond=None, recycle=None, relax_fmm=None,
+                       relax_delta=None):
     o = GmresOpts()
     lib().bpqn_default_gmres_opts(ctypes.byref(o))
+    if relax_fmm is not None:
+        o.relax_fmm = relax_fmm
+    if relax_delta is not None:
+        o.relax_delta = relax_delta
     if recycle is not None:
         o.recycle = recycle
     if precond is not None:

@@ -207,12 +207,25 @@ struct Geom {
   DBuf<double> sh_own_send, sh_own_recv, sh_own_rs_send, sh_own_rs_recv;
   // far-field FMM replacing K1 (fmm.cu; bpqn_disc_opts.fmm_order > 0)
   int fmm_order = 0, fmm_max_leaf = 0;
+  // false: apply_operator uses the direct K1 even though the handle has an FMM (relaxed GMRES,
+  // bpqn_gmres_opts.relax_fmm: direct in the early steps, the FMM once the residual allows it)
+  bool fmm_on = true;
   int last_lo_mvps = -1;
   std::vector<long long> dvi_keys;  // DVI warm start: the last step's contact pairs (i Np + j, sorted) and lambda
   std::vector<double> dvi_lam;  // lo handle: lo MVPs of the last Bi-PQN solve it served (the lo_dense auto rule)
   struct Fmm* fmm = nullptr;
   bool sharded() const { return shard_world > 1 || nccl_comm != nullptr; }
   ~Geom();
+};
+
+// scope in which an FMM handle's applications use the direct K1 (when `on`); restores the flag
+struct FmmDirect {
+  Geom& g;
+  bool prev;
+  FmmDirect(Geom& g_, bool on) : g(g_), prev(g_.fmm_on) {
+    if (on) g.fmm_on = false;
+  }
+  ~FmmDirect() { g.fmm_on = prev; }
 };
 
 // ---------------------------------------------------------------- kernels / passes

@@ -181,7 +181,10 @@ static int mobility(Geom& g, const double* ft, const double* slip, double* uo, c
                     bpqn_gmres_stats& st, cudaStream_t s) {
   BPQN_REQUIRE(g.E_S.p, "geometry built without single-layer data (build_single_layer = 0)");
   launch_pt(g, ft, g.tmp.p, s);
-  apply_operator(g, g.tmp.p, nullptr, g.E_S.p, nullptr, g.rhs.p, s);
+  {
+    FmmDirect direct(g, o.relax_fmm != 0);  // relaxed GMRES: the right-hand side with the direct K1
+    apply_operator(g, g.tmp.p, nullptr, g.E_S.p, nullptr, g.rhs.p, s);
+  }
   const size_t n3 = 3 * (size_t)g.n;
   if (slip) launch_axpby(g.rhs.p, 1.0, slip, -1.0, n3, s);
   else launch_axpby(g.rhs.p, 0.0, g.rhs.p, -1.0, n3, s);
@@ -225,6 +228,8 @@ void bpqn_default_gmres_opts(bpqn_gmres_opts* o) {
   o->max_iters = 1000;
   o->precond = 1;
   o->recycle = 0;
+  o->relax_fmm = 0;
+  o->relax_delta = 0.0;
 }
 
 void bpqn_default_solve_opts(bpqn_solve_opts* o) {

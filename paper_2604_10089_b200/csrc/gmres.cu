@@ -492,6 +492,15 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   const int m = std::max(1, std::min(o.restart, GM_MAX_RESTART));
   const bool pre = o.precond != 0 && g.Minv.p != nullptr;  // block-Jacobi (K4)
   GmLayout L(m);
+  // FMM-accelerated refinement (bpqn_gmres_opts.relax_fmm): every Krylov step applies the operator with
+  // the FMM far field; each cycle reduces its own residual by relax_delta and the next one starts from the
+  // DIRECT residual b - A x, which alone decides convergence (defect correction with an approximate inner
+  // operator: the error contracts by ~|I - A A_fmm^-1| + delta per cycle)
+  const bool relax = o.relax_fmm != 0;
+  BPQN_REQUIRE(!relax || g.fmm, "relax_fmm needs a handle built with fmm_order > 0");
+  const double relax_delta = o.relax_delta > 0.0 ? std::min(o.relax_delta, 0.5) : 3e-3;
+  double cycle_tol = o.tol;
+  FmmDirect direct(g, relax);  // direct applications outside the Krylov steps
   gmres_reserve(g, m);  // no-op unless this restart length exceeds the reserved one
   const int nbx_v = nbx_for(n, g.sms);
   double* S = g.scal.p;
@@ -508,6 +517,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
     float ms = 0;
     cudaEventElapsedTime(&ms, e0, e1);
     stt.ms = ms;
+    if (!relax && g.fmm && g.fmm_on) stt.fmm_applies = stt.applies;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
     return status;
@@ -520,6 +530,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   stt.restarts = 0;
   stt.rel_resid = 0.0;
   stt.applies = 0;
+  stt.fmm_applies = 0;
   if (!(beta_b > 0.0)) return finish(std::isfinite(beta_b) ? BPQN_OK : BPQN_ERR_NAN);
   // Recycling (R33): W orthonormal past right-hand sides, Z with
   // A_op Z = W (to the past solves' tolerance).  Initial guess x0 = Z W^T b.  Needs a store
@@ -577,7 +588,8 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
   // enqueues its collectives on the streams and is captured like the single-GPU step (falls back to
   // host-driven steps if the capture or instantiation is refused)
   const bool capturable_shard = !g.sharded() || (g.nccl_comm && !g.sh_fn && !g.sh_rs_fn);
-  const bool use_graphs = graphs_enabled() && !g.prof.events && capturable_shard && !g.overlap_k2 && CG.ok;
+  const bool use_graphs =
+      graphs_enabled() && !g.prof.events && capturable_shard && !g.overlap_k2 && CG.ok;
   if (CG.exec && (CG.m != m || CG.pre != pre || CG.V != g.V.p || CG.S != g.scal.p || CG.red != g.red.p))
     CG.clear();
   auto build_graph = [&]() -> bool {
@@ -656,9 +668,14 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
         status = BPQN_ERR_NAN;
         break;
       }
+      if (relax && getenv("BPQN_LOG_MVP")) fprintf(stderr, "fmm refinement: direct residual %.3e\n", resid);
       if (resid <= o.tol) break;
     }
     first = false;
+    if (relax) {  // this cycle's target: its own residual reduced by relax_delta (never below tol)
+      cycle_tol = std::max(o.tol, relax_delta * beta / beta_b);
+      k_set<<<1, 1, 0, st>>>(S + 4, cycle_tol);
+    }
     k_cycle_init<<<blocks_vec, 256, 0, st>>>(src, g.V.p, g.gm_vin.p, n, S, L, ctl, beta, stt.iters);
     BPQN_CHECK_LAUNCH();
     g.prof.launches++;
@@ -666,7 +683,8 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       status = BPQN_ERR_NOCONV;
       break;
     }
-    // steps of this cycle
+    // steps of this cycle (FMM refinement: with the FMM far field -- the same graph as a plain FMM handle's)
+    if (relax) g.fmm_on = true;
     bool graphed = false;
     if (use_graphs && CG.ok) {
       if (!CG.exec && CG.warm) build_graph();
@@ -685,6 +703,7 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       }
       CG.warm = true;  // first use done uncaptured (attribute setup, occupancy queries)
     }
+    if (relax) g.fmm_on = false;
     BPQN_CUDA(cudaMemcpyAsync(h, ctl, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     BPQN_CUDA(cudaMemcpyAsync(g.host_scal, S + 1, sizeof(double), cudaMemcpyDeviceToHost, st));
     BPQN_CUDA(cudaStreamSynchronize(st));
@@ -694,14 +713,17 @@ int gmres_solve(Geom& g, const double* b, double* x, const bpqn_gmres_opts& o, b
       g.prof.allpairs_launches += CG.k1 * kk;
     }
     stt.applies += kk;
+    if (relax) stt.fmm_applies += kk;
     stt.iters = h[1];
     resid = g.host_scal[0];
     bool done = false;
     if (h[2] || !std::isfinite(resid)) {
       status = BPQN_ERR_NAN;
       done = true;
-    } else if (resid <= o.tol) {
-      done = true;
+    } else if (resid <= cycle_tol) {
+      // FMM refinement: the estimate belongs to the FMM operator -- the next pass of the loop forms the
+      // direct residual b - A x and stops only if that meets tol
+      done = !relax;
     } else if (stt.iters >= o.max_iters) {
       status = BPQN_ERR_NOCONV;
       done = true;

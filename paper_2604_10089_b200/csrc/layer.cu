@@ -567,7 +567,7 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
   if (ev) BPQN_CUDA(cudaEventRecord(ev[2], sk2));
   launch_near(g, sigS, sigD, sk2);
   if (ev) BPQN_CUDA(cudaEventRecord(ev[3], sk2));
-  if (g.fmm) {  // far-field FMM in place of K1 (fmm.cu): the coarse sum into far, then far + K2, K3
+  if (g.fmm && g.fmm_on) {  // far-field FMM in place of K1 (fmm.cu): the coarse sum into far, then far + K2, K3
     BPQN_REQUIRE(!sharded, "the FMM far field does not combine with sharding");
     if (ev) BPQN_CUDA(cudaEventRecord(ev[0], st));
     fmm_apply(g, sigS, sigD, g.far.p, st);

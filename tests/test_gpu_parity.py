@@ -1001,3 +1001,70 @@ def test_fmm_bi_pqn_solve_matches_direct(bp):
         assert rc == 0
         out.append(lam.cpu().numpy())
     assert rel(out[1], out[0]) <= 1e-5, rel(out[1], out[0])
+
+
+# ------------------------------------------------------------------ FMM-accelerated refinement (relax_fmm)
+@pytest.mark.parametrize("c", [1, 2])
+def test_fmm_refinement_mvp_vs_oracle(bp, c):
+    """FMM refinement (bpqn_gmres_opts.relax_fmm, order 6 -- the least accurate order used): every Krylov step
+    with the FMM far field, every cycle from the direct residual.  The LCP MVP meets the PARITY bar against the
+    oracle fixture at the parity tolerance 1e-12 (the returned x meets tol for the direct operator), several
+    refinement cycles ran, and only the residuals used the direct operator."""
+    z = fixture(c)
+    C, p = z["centers"], int(z["p"])
+    g = _fmm_geometry(bp, C, p, 6, 2)
+    bp.contacts(g, 0.1)
+    from synth import lambda_test
+    lam = lambda_test(c, g.nc, 0)
+    w, st = bp.lcp_mvp(g, T(lam), gmres=bp.default_gmres_opts(tol=1e-12, relax_fmm=1))
+    assert st.fmm_applies == st.iters and st.applies == st.iters + st.restarts, (st.iters, st.applies)
+    assert st.restarts >= 2 and st.rel_resid <= 1e-12
+    assert rel(w.cpu().numpy(), z["w_test"][0]) <= TOL_VEL, (st.iters, st.restarts)
+
+
+def test_fmm_refinement_matches_direct_gmres(bp):
+    """FMM refinement vs plain GMRES on a direct handle at tol 1e-10 and several cycle reductions delta: the MVPs
+    agree to the tolerance level; the captured cycle graph replays bit-identically; without relax_fmm an FMM
+    handle uses the FMM throughout; relax_fmm on a direct handle is an argument error."""
+    C = _lattice(4, 61)
+    gd = bp.Geometry(C, 6)
+    gf = _fmm_geometry(bp, C, 6, 6, 2)
+    bp.contacts(gd, 0.1)
+    bp.contacts(gf, 0.1)
+    lam = T(np.random.default_rng(62).uniform(0, 1, gd.nc))
+    wd, sd = bp.lcp_mvp(gd, lam, gmres=bp.default_gmres_opts(tol=1e-10))
+    for delta in (0.0, 1e-2, 1e-4):
+        wr, sr = bp.lcp_mvp(gf, lam, gmres=bp.default_gmres_opts(tol=1e-10, relax_fmm=1, relax_delta=delta))
+        assert sr.fmm_applies == sr.iters > 0 and sr.restarts >= 1 and sr.rel_resid <= 1e-10, delta
+        assert rel(wr.cpu().numpy(), wd.cpu().numpy()) <= 1e-8, delta
+    gm = bp.default_gmres_opts(tol=1e-10, relax_fmm=1)
+    w1, _ = bp.lcp_mvp(gf, lam, gmres=gm)
+    w2, _ = bp.lcp_mvp(gf, lam, gmres=gm)
+    assert torch_equal(w1, w2)
+    _, s0 = bp.lcp_mvp(gf, lam, gmres=bp.default_gmres_opts(tol=1e-10))
+    assert s0.fmm_applies == s0.applies
+    with pytest.raises(bp.BpqnError):
+        bp.lcp_mvp(gd, lam, gmres=bp.default_gmres_opts(tol=1e-10, relax_fmm=1))
+
+
+def test_fmm_refinement_bi_pqn_solve_matches_direct(bp):
+    """A Bi-PQN LCP solve whose high-fidelity MVPs use FMM refinement reaches the direct solve's lambda* to the
+    solve tolerance (each MVP meets the GMRES tolerance for the direct operator)."""
+    C = _lattice(4, 63, spacing=2.03, jitter=0.015)
+    gd = bp.Geometry(C, 6)
+    gf = _fmm_geometry(bp, C, 6, 6, 2)
+    lo = bp.Geometry(C, 4)
+    pr, nr, gp = bp.contacts(gd, 0.1)
+    bp.set_contacts(gf, pr, nr, gp)
+    bp.set_contacts(lo, pr, nr, gp)
+    b = T(np.random.default_rng(64).uniform(-0.05, 0.02, gd.nc))
+    out = []
+    for g, rf in ((gd, 0), (gf, 1)):
+        o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-10)
+        o.gm_hi.tol = 1e-11
+        o.gm_hi.relax_fmm = rf
+        o.gm_lo.tol = 1e-11
+        lam, rep, rc = bp.solve_lcp(g, lo, b, T(np.zeros(gd.nc)), opts=o)
+        assert rc == 0
+        out.append(lam.cpu().numpy())
+    assert np.max(np.abs(out[1] - out[0])) <= 1e-7 * max(1.0, np.max(np.abs(out[0])))
