@@ -260,8 +260,8 @@ __device__ __forceinline__ void fmm_pair_fast(double x0, double x1, double x2, c
 
 // Leaves: near field (27 neighbour leaves) + L2P from the leaf's downward equivalent density; two targets per
 // thread share every staged source; writes out[node] in the original order
-constexpr int FL_T = 64, FL_R = 3;
-template <int MODE>
+constexpr int FL_T = 64;
+template <int MODE, int FL_R>
 __global__ void __launch_bounds__(FL_T) k_fmm_leaf(const double* __restrict__ rec, const int* __restrict__ start,
                                                    const int* __restrict__ nbr, const int* __restrict__ perm,
                                                    const double* __restrict__ surf, int ns,
@@ -748,17 +748,31 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
   }
   // leaves: near field + L2P
   const int maxpts = g.fmm_max_leaf;  // the largest leaf sets the grid's second dimension
-  const dim3 lg(LV.nocc, (maxpts + FL_T * FL_R - 1) / (FL_T * FL_R));
+  // targets per thread: 3 share every staged source (large leaves, N = 589 824 at order 10: 43.7 ms); small
+  // leaves (low orders, deeper trees) need the CTAs -- c4 at order 6: one target per thread 4.31 ms per D
+  // apply, two 4.62, three 4.78 (profiles/r02_fmm_refine.md)
+  int R = maxpts >= 3 * FL_T * 4 ? 3 : 1;
+  if (const char* e = getenv("BPQN_FMM_LEAF_R")) R = std::max(1, std::min(3, atoi(e)));
+  const dim3 lg(LV.nocc, (maxpts + FL_T * R - 1) / (FL_T * R));
   const double rad = FMM_OUT * LV.r;
-  if (doS && doD)
-    k_fmm_leaf<MODE_SD><<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p,
-                                             rad, LV.deq.p, out);
-  else if (doS)
-    k_fmm_leaf<MODE_S><<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p,
-                                            rad, LV.deq.p, out);
-  else
-    k_fmm_leaf<MODE_D><<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p,
-                                            rad, LV.deq.p, out);
+  auto launch = [&](auto kern) {
+    kern<<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p, rad,
+                              LV.deq.p, out);
+  };
+  const int md = (doS && doD) ? MODE_SD : (doS ? MODE_S : MODE_D);
+  if (md == MODE_SD) {
+    if (R == 3) launch(k_fmm_leaf<MODE_SD, 3>);
+    else if (R == 2) launch(k_fmm_leaf<MODE_SD, 2>);
+    else launch(k_fmm_leaf<MODE_SD, 1>);
+  } else if (md == MODE_S) {
+    if (R == 3) launch(k_fmm_leaf<MODE_S, 3>);
+    else if (R == 2) launch(k_fmm_leaf<MODE_S, 2>);
+    else launch(k_fmm_leaf<MODE_S, 1>);
+  } else {
+    if (R == 3) launch(k_fmm_leaf<MODE_D, 3>);
+    else if (R == 2) launch(k_fmm_leaf<MODE_D, 2>);
+    else launch(k_fmm_leaf<MODE_D, 1>);
+  }
   BPQN_CHECK_LAUNCH();
   g.prof.launches += 8;
 }
