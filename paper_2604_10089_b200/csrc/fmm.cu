@@ -69,6 +69,12 @@ struct Fmm {
   DBuf<int> leaf_start;          // [nleaf + 1]
   DBuf<int> leaf_nbr;            // [nleaf][27]
   DBuf<double> rec;              // [N][12] sorted records {y, n, f~, q~}
+  // small leaves: the near field + L2P as equal-cost items (leaf, 64-target chunk, source segment), see
+  // k_fmm_leaf_seg; part[s][k][3] = segment s's sum for sorted target k, tparts[k] = its number of segments
+  DBuf<int> leaf_items;          // [n_items][4] = {leaf, chunk, segment, segment length}
+  DBuf<int> tparts;              // [N]
+  DBuf<double> part;             // [kmax][N][3]
+  int n_items = 0, kmax = 0;
   DBuf<double> bufB, bufC, tmpA, tmpB;
   size_t buf_cols = 0;
   bool ops_ready = false;
@@ -336,6 +342,147 @@ __global__ void __launch_bounds__(FL_T) k_fmm_leaf(const double* __restrict__ re
     }
 }
 
+// Small leaves (c4 at order 6: ~230 points per leaf).  One CTA per (leaf, 64-target chunk) leaves the SMs
+// unevenly loaded: a corner leaf sees 8 neighbour leaves, an interior one 27, the whole grid is resident at once
+// and the kernel ends with the most loaded SM (ncu, profiles/r02_fmm_leaf_seg.md: FP64 pipe 37-64 % of the
+// elapsed time from SM to SM).  Here the concatenated source list of a leaf's neighbours is cut into segments of
+// about FMM_SEG sources, so every CTA (leaf, chunk, segment) costs about the same and the SMs stay full to the
+// end; segment K_b of a leaf is its L2P.  Each CTA stores its partial sum, k_fmm_leaf_sum adds a target's
+// partials in segment order (a fixed order: bit-reproducible) and writes out[node] in the original order.
+template <int MODE, bool SELF>
+__device__ __forceinline__ void fmm_leaf_chunk(const double* __restrict__ sr, int nj, double x0, double x1, double x2,
+                                               double& u0, double& u1, double& u2) {
+#pragma unroll 2
+  for (int j = 0; j < nj; ++j) {
+    const double* s = sr + 12 * j;
+    const double r0 = x0 - s[0], r1 = x1 - s[1], r2 = x2 - s[2];
+    const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+    double y;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(rr));
+    if (SELF) y = __double2hiint(rr) != 0 || __double2loint(rr) != 0 ? y : 0.0;  // rho = 0: the target itself
+    const double y2 = y * y;
+    const double e = fma(-rr, y2, 1.0);
+    double t;
+    if (MODE == MODE_D) {
+      const double s5 = (y * (y2 * y2)) * fma(e, fma(e, 4.375, 2.5), 1.0);
+      const double rn = fma(r2, s[5], fma(r1, s[4], r0 * s[3]));
+      const double rq = fma(r2, s[11], fma(r1, s[10], r0 * s[9]));
+      t = (rn * rq) * s5;
+    } else {
+      const double sv = fma(y * e, fma(e, 0.375, 0.5), y);
+      const double s2 = sv * sv, s3 = s2 * sv;
+      const double rf = fma(r2, s[8], fma(r1, s[7], r0 * s[6]));
+      t = rf * s3;
+      if (MODE == MODE_SD) {
+        const double rn = fma(r2, s[5], fma(r1, s[4], r0 * s[3]));
+        const double rq = fma(r2, s[11], fma(r1, s[10], r0 * s[9]));
+        t = fma(rn * rq, s3 * s2, t);
+      }
+      u0 = fma(s[6], sv, u0);
+      u1 = fma(s[7], sv, u1);
+      u2 = fma(s[8], sv, u2);
+    }
+    u0 = fma(r0, t, u0);
+    u1 = fma(r1, t, u1);
+    u2 = fma(r2, t, u2);
+  }
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(FL_T) k_fmm_leaf_seg(const int4* __restrict__ items, const double* __restrict__ rec,
+                                                       const int* __restrict__ start, const int* __restrict__ nbr,
+                                                       const double* __restrict__ surf, int ns,
+                                                       const double* __restrict__ ctr, double rad,
+                                                       const double* __restrict__ deq, int N,
+                                                       double* __restrict__ part) {
+  __shared__ __align__(16) double sr[FL_T * 12];
+  const int4 it = items[blockIdx.x];
+  const int b = it.x, seg = it.z, seglen = it.w;
+  const int t0 = start[b], t1 = start[b + 1];
+  const int k = t0 + it.y * FL_T + threadIdx.x;
+  const int kk = min(k, t1 - 1);  // inactive lanes compute a duplicate and do not store
+  const double x0 = rec[12 * (size_t)kk], x1 = rec[12 * (size_t)kk + 1], x2 = rec[12 * (size_t)kk + 2];
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  if (seglen > 0) {  // near field: sources [lo, hi) of the concatenated neighbour leaves
+    const int lo = seg * seglen, hi = lo + seglen;
+    int off = 0;
+    for (int q = 0; q < 27 && off < hi; ++q) {
+      const int nb = nbr[27 * b + q];
+      if (nb < 0) continue;
+      const int s0 = start[nb], cnt = start[nb + 1] - s0;
+      const int a = max(lo - off, 0), e = min(hi - off, cnt);
+      off += cnt;
+      for (int j0 = s0 + a; j0 < s0 + e; j0 += FL_T) {
+        const int nj = min(FL_T, s0 + e - j0);
+        __syncthreads();
+        {
+          const double2* g2 = reinterpret_cast<const double2*>(rec + 12 * (size_t)j0);
+          double2* s2 = reinterpret_cast<double2*>(sr);
+          for (int w = threadIdx.x; w < nj * 6; w += FL_T) s2[w] = g2[w];
+        }
+        __syncthreads();
+        if (nb == b) fmm_leaf_chunk<MODE, true>(sr, nj, x0, x1, x2, u0, u1, u2);
+        else fmm_leaf_chunk<MODE, false>(sr, nj, x0, x1, x2, u0, u1, u2);
+      }
+    }
+  } else {  // L2P: Stokeslet equivalent density on the downward equivalent surface (2.95 r)
+    const double c0 = ctr[3 * b], c1 = ctr[3 * b + 1], c2 = ctr[3 * b + 2];
+    const double* ph = deq + (size_t)b * 3 * ns;
+    for (int j0 = 0; j0 < ns; j0 += FL_T) {
+      const int nj = min(FL_T, ns - j0);
+      __syncthreads();
+      for (int e = threadIdx.x; e < nj; e += FL_T) {
+        const int j = j0 + e;
+        sr[6 * e] = c0 + rad * surf[3 * j];
+        sr[6 * e + 1] = c1 + rad * surf[3 * j + 1];
+        sr[6 * e + 2] = c2 + rad * surf[3 * j + 2];
+        sr[6 * e + 3] = ph[3 * j];
+        sr[6 * e + 4] = ph[3 * j + 1];
+        sr[6 * e + 5] = ph[3 * j + 2];
+      }
+      __syncthreads();
+#pragma unroll 2
+      for (int j = 0; j < nj; ++j) {
+        const double* sp = sr + 6 * j;
+        const double r0 = x0 - sp[0], r1 = x1 - sp[1], r2 = x2 - sp[2];
+        const double rr = fma(r2, r2, fma(r1, r1, r0 * r0));
+        double y;  // the surface lies outside the leaf: rho > 0
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(rr));
+        const double e = fma(-rr, y * y, 1.0);
+        const double ir = fma(y * e, fma(e, 0.375, 0.5), y), ir3 = ir * ir * ir;
+        const double t = fma(r2, sp[5], fma(r1, sp[4], r0 * sp[3])) * ir3;
+        u0 = fma(sp[3], ir, fma(r0, t, u0));
+        u1 = fma(sp[4], ir, fma(r1, t, u1));
+        u2 = fma(sp[5], ir, fma(r2, t, u2));
+      }
+    }
+  }
+  if (k < t1) {
+    double* o = part + ((size_t)seg * N + k) * 3;
+    o[0] = u0;
+    o[1] = u1;
+    o[2] = u2;
+  }
+}
+
+__global__ void k_fmm_leaf_sum(int N, const int* __restrict__ tparts, const int* __restrict__ perm,
+                               const double* __restrict__ part, double* __restrict__ out) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N) return;
+  const int np = tparts[k];
+  double u0 = 0.0, u1 = 0.0, u2 = 0.0;
+  for (int s = 0; s < np; ++s) {
+    const double* o = part + ((size_t)s * N + k) * 3;
+    u0 += o[0];
+    u1 += o[1];
+    u2 += o[2];
+  }
+  const int i = perm[k];
+  out[3 * (size_t)i] = u0;
+  out[3 * (size_t)i + 1] = u1;
+  out[3 * (size_t)i + 2] = u2;
+}
+
 // dst[:, j] = src[:, idx[j]] (columns of length m)
 __global__ void k_fmm_gather(const double* __restrict__ src, int m, const int* __restrict__ idx, int cnt,
                              double* __restrict__ dst) {
@@ -580,6 +727,36 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
   fmm_upload(F.perm, perm, st);
   fmm_upload(F.leaf_start, start, st);
   fmm_upload(F.leaf_nbr, nbr, st);
+  // small leaves: equal-cost (leaf, chunk, segment) items for k_fmm_leaf_seg (segment K_b = the leaf's L2P)
+  F.n_items = F.kmax = 0;
+  if (maxleaf < 3 * FL_T * 4) {
+    int seg_target = 512;  // c4 at order 6: D apply 3.54 ms (1024: 3.59, 2048: 3.77, 256: 3.53; one CTA per (leaf, chunk): 4.46)
+    if (const char* e = getenv("BPQN_FMM_SEG")) seg_target = std::max(FL_T, atoi(e));
+    std::vector<int> items, tparts(N);
+    for (int b = 0; b < LV.nocc; ++b) {
+      const int nb_pts = start[b + 1] - start[b];
+      long long tot = 0;
+      for (int q = 0; q < 27; ++q) {
+        const int nb = nbr[27 * (size_t)b + q];
+        if (nb >= 0) tot += start[nb + 1] - start[nb];
+      }
+      int K = (int)std::max(1LL, (tot + seg_target / 2) / seg_target);
+      const int seglen = (int)(((tot + K - 1) / K + FL_T - 1) / FL_T) * FL_T;
+      K = (int)((tot + seglen - 1) / seglen);
+      for (int c = 0; c * FL_T < nb_pts; ++c) {
+        for (int sgi = 0; sgi < K; ++sgi) {
+          items.push_back(b); items.push_back(c); items.push_back(sgi); items.push_back(seglen);
+        }
+        items.push_back(b); items.push_back(c); items.push_back(K); items.push_back(0);
+      }
+      for (int k = start[b]; k < start[b + 1]; ++k) tparts[k] = K + 1;
+      F.kmax = std::max(F.kmax, K + 1);
+    }
+    F.n_items = (int)(items.size() / 4);
+    fmm_upload(F.leaf_items, items, st);
+    fmm_upload(F.tparts, tparts, st);
+    F.part.alloc((size_t)F.kmax * N * 3);
+  }
   F.rec.alloc(12 * (size_t)N);
   // M2M / L2L octant pairs (parent level l, children at l + 1)
   size_t maxcols = 0;
@@ -760,6 +937,21 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
                               LV.deq.p, out);
   };
   const int md = (doS && doD) ? MODE_SD : (doS ? MODE_S : MODE_D);
+  static const bool use_seg = !(getenv("BPQN_FMM_SEG") && atoi(getenv("BPQN_FMM_SEG")) == 0);
+  if (F.n_items > 0 && use_seg && !getenv("BPQN_FMM_LEAF_R")) {
+    auto launch_seg = [&](auto kern) {
+      kern<<<F.n_items, FL_T, 0, st>>>(reinterpret_cast<const int4*>(F.leaf_items.p), F.rec.p, F.leaf_start.p,
+                                       F.leaf_nbr.p, F.surf.p, ns, LV.ctr.p, rad, LV.deq.p, N, F.part.p);
+    };
+    if (md == MODE_SD) launch_seg(k_fmm_leaf_seg<MODE_SD>);
+    else if (md == MODE_S) launch_seg(k_fmm_leaf_seg<MODE_S>);
+    else launch_seg(k_fmm_leaf_seg<MODE_D>);
+    BPQN_CHECK_LAUNCH();
+    k_fmm_leaf_sum<<<(N + 255) / 256, 256, 0, st>>>(N, F.tparts.p, F.perm.p, F.part.p, out);
+    BPQN_CHECK_LAUNCH();
+    g.prof.launches += 9;
+    return;
+  }
   if (md == MODE_SD) {
     if (R == 3) launch(k_fmm_leaf<MODE_SD, 3>);
     else if (R == 2) launch(k_fmm_leaf<MODE_SD, 2>);
