@@ -35,6 +35,15 @@ struct FmmLevel {
   // this level as parent: per child octant the (parent, child) compact pairs
   int n_oct[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   DBuf<int> oct_par[8], oct_ch[8];
+  // the same pairs octant-major in one list (column j of the gathered buffers), the parents' CSR over the
+  // columns (octant order), and the 8 octant GEMMs of M2M / L2L as grouped-batched cuBLAS calls
+  int n_child = 0;
+  int oct_start[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+  DBuf<int> par_all, ch_all, par_ptr, par_pos;
+  std::vector<int> mm_m, mm_n, mm_k, mm_lda, mm_ldb, mm_ldc, ll_k, ll_ldb;
+  std::vector<double> mm_alpha;
+  DBuf<const double*> mm_A, mm_B, ll_A, ll_B;
+  DBuf<double*> mm_C;
   // M2L into this level: pairs in offset-major order (source compact ids), offset ranges, and per target
   // the pair positions in offset order (CSR)
   int n_pairs = 0;
@@ -53,6 +62,7 @@ struct FmmLevel {
     off_start.clear();
     n_pairs = 0;
     for (int o = 0; o < 8; ++o) n_oct[o] = 0;
+    n_child = 0;
   }
 };
 
@@ -63,7 +73,13 @@ struct Fmm {
   DBuf<double> surf;             // [ns][3] unit cube surface points
   DBuf<double> UC2E, DC2E;       // [3ns][3ns] (unit box)
   DBuf<double> M2M, L2L;         // [8][3ns][3ns]
-  DBuf<double> M2L;              // [316][3ns][3ns]
+  DBuf<double> M2L;              // [316][3ns][3ns + 1]
+  // compressed M2L (low orders): M2L_o ~ WU M2L_o[I, J] WV^T with one row skeleton I and one column skeleton J
+  // for all 316 offsets (interpolative decompositions by pivoted Cholesky of the two Gram matrices)
+  bool m2l_comp = false;
+  int rU = 0, rV = 0;
+  DBuf<double> WU, WV;           // [3ns][rU], [3ns + 1][rV] (column-major)
+  DBuf<double> M2Lc;             // [316][rU][rV]
   std::vector<int> offs;         // [316][3]
   DBuf<int> perm;                // [N] sorted position -> node
   DBuf<int> leaf_start;          // [nleaf + 1]
@@ -570,6 +586,121 @@ static void fmm_gmat(const Fmm& F, double sx, double3 ox, double sy, double3 oy,
 // Unit box (half-width 1).  Upward equivalents carry 3 ns Stokeslet densities plus one point source at the box
 // centre, whose kernel is scaled by the box half-width (r (x - y) / |x - y|^3) so that every operator stays
 // homogeneous of degree -1 and scales by 1 / r per level like the Stokeslet.
+// Pivoted Cholesky of the n x n Gram matrix G (column-major, symmetric PSD) down to a residual diagonal of
+// tol^2 max diag: the pivots I (r of them) and the interpolation matrix W [n][r] (column-major) with
+// rows(A) ~ W rows_I(A) for the A behind G = A A^T (W[I, :] = identity).
+static int fmm_pivchol_interp(const std::vector<double>& G, int n, double tol, int rmax, std::vector<int>& I,
+                              std::vector<double>& W) {
+  std::vector<double> d(n), Lm;  // Lm [n][r] column-major, grown column by column
+  double d0 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    d[i] = G[(size_t)i * n + i];
+    d0 = std::max(d0, d[i]);
+  }
+  std::vector<char> used(n, 0);
+  I.clear();
+  int r = 0;
+  while (r < rmax) {
+    int pv = -1;
+    double best = tol * tol * d0;
+    for (int i = 0; i < n; ++i)
+      if (!used[i] && d[i] > best) {
+        best = d[i];
+        pv = i;
+      }
+    if (pv < 0) break;
+    Lm.resize((size_t)n * (r + 1));
+    double* col = Lm.data() + (size_t)n * r;
+    for (int i = 0; i < n; ++i) col[i] = G[(size_t)pv * n + i];
+    for (int j = 0; j < r; ++j) {
+      const double* cj = Lm.data() + (size_t)n * j;
+      const double f = cj[pv];
+      for (int i = 0; i < n; ++i) col[i] -= cj[i] * f;
+    }
+    const double piv = std::sqrt(std::max(col[pv], 1e-300));
+    for (int i = 0; i < n; ++i) {
+      col[i] = used[i] ? 0.0 : col[i] / piv;
+      d[i] -= col[i] * col[i];
+    }
+    used[pv] = 1;
+    d[pv] = 0.0;
+    I.push_back(pv);
+    ++r;
+  }
+  // W L_I = L with L_I = L[I, :] lower triangular (L[I[k], j] = 0 for j > k): back substitution row by row
+  W.assign((size_t)n * r, 0.0);
+  std::vector<double> w(r);
+  for (int i = 0; i < n; ++i) {
+    if (used[i]) continue;
+    for (int k = r - 1; k >= 0; --k) {
+      double v = Lm[(size_t)n * k + i];
+      for (int j = k + 1; j < r; ++j) v -= w[j] * Lm[(size_t)n * k + I[j]];
+      w[k] = v / Lm[(size_t)n * k + I[k]];
+    }
+    for (int k = 0; k < r; ++k) W[(size_t)n * k + i] = w[k];
+  }
+  for (int k = 0; k < r; ++k) W[(size_t)n * k + I[k]] = 1.0;
+  return r;
+}
+
+// Mc[o][a + rU b] = M[o][I[a] + m J[b]]
+__global__ void k_fmm_m2l_core(const double* __restrict__ M, int m, int mu, const int* __restrict__ I, int rU,
+                               const int* __restrict__ J, int rV, double* __restrict__ Mc) {
+  const size_t o = blockIdx.y;
+  const int tot = rU * rV;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += gridDim.x * blockDim.x) {
+    const int a = e % rU, b = e / rU;
+    Mc[o * tot + e] = M[o * (size_t)m * mu + I[a] + (size_t)m * J[b]];
+  }
+}
+
+// Shared row / column skeletons of the 316 M2L matrices (order <= 8: the low orders of the FMM-accelerated
+// refinement, whose Krylov steps tolerate 1e-4).  The rows of [M2L_1 ... M2L_316] and the columns of
+// [M2L_1; ...; M2L_316] are numerically dependent to tol, so M2L_o ~ WU M2L_o[I, J] WV^T: the per-pair GEMM
+// shrinks from 3ns x (3ns + 1) to rU x rV, with one WV^T / WU GEMM per level around it.
+static void fmm_compress_m2l(Fmm& F, cudaStream_t st) {
+  F.m2l_comp = false;
+  // default tolerance: about the order's own far-field error (D layer, c4: order 5 2e-3, 6 1.4e-4, 7 1.6e-5,
+  // 8 2.4e-6), so the compressed FMM stays within ~1.5x of it (order 6: 2.0e-4; profiles/r02_fmm_m2l.md);
+  // orders <= 4 have nothing to gain (full rank at 1e-3), orders >= 9 are used for accuracy and stay exact
+  double tol = F.pe == 5 ? 1e-3 : F.pe == 6 ? 1e-4 : F.pe == 7 ? 1e-5 : F.pe == 8 ? 2e-6 : 0.0;
+  if (const char* e = getenv("BPQN_FMM_M2L_TOL")) tol = atof(e);  // 0: off
+  if (!(tol > 0.0) || F.pe > 8) return;
+  const int m = 3 * F.ns, mu = m + 1;
+  const size_t mmu = (size_t)m * mu;
+  DBuf<double> GU, GV;
+  GU.alloc((size_t)m * m);
+  GV.alloc((size_t)mu * mu);
+  for (int o = 0; o < FMM_NOFF; ++o) {  // (one GEMM over the 316 mu columns overflows nothing but is no faster)
+    blas_dgemm(st, FMM_OP_N, FMM_OP_T, m, m, mu, 1.0, F.M2L.p + o * mmu, m, F.M2L.p + o * mmu, m, o ? 1.0 : 0.0,
+               GU.p, m);
+    blas_dgemm(st, FMM_OP_T, FMM_OP_N, mu, mu, m, 1.0, F.M2L.p + o * mmu, m, F.M2L.p + o * mmu, m, o ? 1.0 : 0.0,
+               GV.p, mu);
+  }
+  std::vector<double> hU((size_t)m * m), hV((size_t)mu * mu);
+  BPQN_CUDA(cudaMemcpyAsync(hU.data(), GU.p, 8 * hU.size(), cudaMemcpyDeviceToHost, st));
+  BPQN_CUDA(cudaMemcpyAsync(hV.data(), GV.p, 8 * hV.size(), cudaMemcpyDeviceToHost, st));
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  std::vector<int> I, J;
+  std::vector<double> WU, WV;
+  const int rU = fmm_pivchol_interp(hU, m, tol, m, I, WU);
+  const int rV = fmm_pivchol_interp(hV, mu, tol, mu, J, WV);
+  if (getenv("BPQN_FMM_DEBUG")) fprintf(stderr, "[bpqn fmm] M2L skeletons: %d of %d rows, %d of %d columns (tol %.1e)\n", rU, m, rV, mu, tol);
+  if ((double)rU * rV > 0.5 * (double)m * mu || rU < 8 || rV < 8) return;  // not worth the two extra GEMMs
+  F.rU = rU;
+  F.rV = rV;
+  fmm_upload(F.WU, WU, st);
+  fmm_upload(F.WV, WV, st);
+  DBuf<int> dI, dJ;
+  fmm_upload(dI, I, st);
+  fmm_upload(dJ, J, st);
+  F.M2Lc.alloc((size_t)FMM_NOFF * rU * rV);
+  k_fmm_m2l_core<<<dim3((rU * rV + 255) / 256, FMM_NOFF), 256, 0, st>>>(F.M2L.p, m, mu, dI.p, rU, dJ.p, rV, F.M2Lc.p);
+  BPQN_CHECK_LAUNCH();
+  BPQN_CUDA(cudaStreamSynchronize(st));
+  F.m2l_comp = true;
+}
+
 static void fmm_operators(Fmm& F, cudaStream_t st) {
   const int pe = F.pe;
   std::vector<double> s;
@@ -618,6 +749,7 @@ static void fmm_operators(Fmm& F, cudaStream_t st) {
     fmm_gmat(F, FMM_IN, z, FMM_IN, so, F.M2L.p + o * mmu, st, 1.0);
   }
   BPQN_CUDA(cudaStreamSynchronize(st));
+  fmm_compress_m2l(F, st);
   F.ops_ready = true;
 }
 
@@ -770,12 +902,28 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
       pp[oct].push_back(cmap[l][coarsen(d, l + 1, l)]);
       cc[oct].push_back(b);
     }
+    std::vector<int> par_all, ch_all;
     for (int o = 0; o < 8; ++o) {
       P.n_oct[o] = (int)pp[o].size();
       fmm_upload(P.oct_par[o], pp[o], st);
       fmm_upload(P.oct_ch[o], cc[o], st);
       maxcols = std::max(maxcols, pp[o].size());
+      P.oct_start[o] = (int)par_all.size();
+      par_all.insert(par_all.end(), pp[o].begin(), pp[o].end());
+      ch_all.insert(ch_all.end(), cc[o].begin(), cc[o].end());
     }
+    P.oct_start[8] = P.n_child = (int)par_all.size();
+    std::vector<int> pptr(P.nocc + 1, 0), ppos(par_all.size());
+    for (int j : par_all) pptr[j + 1]++;
+    for (int b = 0; b < P.nocc; ++b) pptr[b + 1] += pptr[b];
+    {
+      std::vector<int> fill(pptr.begin(), pptr.end() - 1);
+      for (int j = 0; j < (int)par_all.size(); ++j) ppos[fill[par_all[j]]++] = j;  // octant order per parent
+    }
+    fmm_upload(P.par_all, par_all, st);
+    fmm_upload(P.ch_all, ch_all, st);
+    fmm_upload(P.par_ptr, pptr, st);
+    fmm_upload(P.par_pos, ppos, st);
   }
   // M2L pairs per level l >= 2 (source a child of a neighbour of the target's parent, not adjacent)
   for (int l = 2; l <= L; ++l) {
@@ -829,7 +977,9 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
   }
   // grouped-batched M2L: per level the non-empty offsets' GEMMs (pointers into the fixed buffers)
   {
-    const int mm3 = 3 * F.ns, muu = mm3 + 1;
+    // (compressed M2L: the rU x rV cores instead of the 3ns x (3ns + 1) matrices)
+    const int mm3 = F.m2l_comp ? F.rU : 3 * F.ns, muu = F.m2l_comp ? F.rV : 3 * F.ns + 1;
+    const double* m2l = F.m2l_comp ? F.M2Lc.p : F.M2L.p;
     for (int l = 2; l <= L; ++l) {
       FmmLevel& V = F.lev[l];
       V.g_m.clear(); V.g_n.clear(); V.g_k.clear(); V.g_lda.clear(); V.g_ldb.clear(); V.g_ldc.clear();
@@ -842,7 +992,7 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
         V.g_m.push_back(mm3); V.g_n.push_back(cnt); V.g_k.push_back(muu);
         V.g_lda.push_back(mm3); V.g_ldb.push_back(muu); V.g_ldc.push_back(mm3);
         V.g_alpha.push_back(1.0 / V.r);
-        pa.push_back(F.M2L.p + (size_t)o * mm3 * muu);
+        pa.push_back(m2l + (size_t)o * mm3 * muu);
         pb.push_back(F.bufB.p + (size_t)c0 * muu);
         pc.push_back(F.bufC.p + (size_t)c0 * mm3);
       }
@@ -855,7 +1005,39 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
   for (int l = 0; l <= L; ++l) maxocc = std::max(maxocc, (size_t)F.lev[l].nocc);
   F.tmpA.alloc(m * maxocc);
   F.tmpB.alloc(m * maxocc);
+  {
+    const int m3 = 3 * F.ns, mu3 = m3 + 1;
+    for (int l = 2; l < L; ++l) {
+      FmmLevel& P = F.lev[l];
+      P.mm_m.clear(); P.mm_n.clear(); P.mm_k.clear(); P.mm_lda.clear(); P.mm_ldb.clear(); P.mm_ldc.clear();
+      P.ll_k.clear(); P.ll_ldb.clear(); P.mm_alpha.clear();
+      std::vector<const double*> ma, mb, la, lb;
+      std::vector<double*> mc;
+      for (int o = 0; o < 8; ++o) {
+        const int c0 = P.oct_start[o], cnt = P.oct_start[o + 1] - c0;
+        if (!cnt) continue;
+        P.mm_m.push_back(m3); P.mm_n.push_back(cnt); P.mm_k.push_back(mu3); P.ll_k.push_back(m3);
+        P.mm_lda.push_back(m3); P.mm_ldb.push_back(mu3); P.ll_ldb.push_back(m3); P.mm_ldc.push_back(m3);
+        P.mm_alpha.push_back(1.0 / P.r);
+        ma.push_back(F.M2M.p + (size_t)o * m3 * mu3);
+        la.push_back(F.L2L.p + (size_t)o * m3 * m3);
+        mb.push_back(F.tmpA.p + (size_t)c0 * mu3);
+        lb.push_back(F.tmpA.p + (size_t)c0 * m3);
+        mc.push_back(F.tmpB.p + (size_t)c0 * m3);
+      }
+      fmm_upload(P.mm_A, ma, st);
+      fmm_upload(P.mm_B, mb, st);
+      fmm_upload(P.ll_A, la, st);
+      fmm_upload(P.ll_B, lb, st);
+      fmm_upload(P.mm_C, mc, st);
+    }
+  }
   BPQN_CUDA(cudaStreamSynchronize(st));
+}
+
+static bool fmm_grouped() {
+  static const bool grouped = !(getenv("BPQN_FMM_GROUPED") && getenv("BPQN_FMM_GROUPED")[0] == '0');
+  return grouped;
 }
 
 // ------------------------------------------------------------------ apply
@@ -878,13 +1060,24 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
     FmmLevel& P = F.lev[l];
     FmmLevel& C = F.lev[l + 1];
     BPQN_CUDA(cudaMemsetAsync(P.uck.p, 0, 8 * (size_t)m * P.nocc, st));
-    for (int o = 0; o < 8; ++o) {
-      const int cnt = P.n_oct[o];
-      if (!cnt) continue;
-      k_fmm_gather<<<fgrid((size_t)mu * cnt), 256, 0, st>>>(C.ueq.p, mu, P.oct_ch[o].p, cnt, F.tmpA.p);
-      blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, cnt, mu, 1.0 / P.r, F.M2M.p + o * mmu, m, F.tmpA.p, mu, 0.0, F.tmpB.p, m);
-      k_fmm_scatter_add<<<fgrid((size_t)m * cnt), 256, 0, st>>>(P.uck.p, m, P.oct_par[o].p, cnt, F.tmpB.p);
+    // all children octant-major in one gather, the 8 octant GEMMs as one grouped call, then each parent adds
+    // its children's columns in octant order
+    k_fmm_gather<<<fgrid((size_t)mu * P.n_child), 256, 0, st>>>(C.ueq.p, mu, P.ch_all.p, P.n_child, F.tmpA.p);
+    BPQN_CHECK_LAUNCH();
+    {
+      const int G = (int)P.mm_m.size();
+      if (!(fmm_grouped() && G > 0 &&
+            blas_dgemm_grouped(st, G, P.mm_m.data(), P.mm_n.data(), P.mm_k.data(), P.mm_alpha.data(), P.mm_A.p,
+                               P.mm_lda.data(), P.mm_B.p, P.mm_ldb.data(), P.mm_C.p, P.mm_ldc.data())))
+        for (int o = 0; o < 8; ++o) {
+          const int c0 = P.oct_start[o], cnt = P.oct_start[o + 1] - c0;
+          if (!cnt) continue;
+          blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, cnt, mu, 1.0 / P.r, F.M2M.p + o * mmu, m,
+                     F.tmpA.p + (size_t)c0 * mu, mu, 0.0, F.tmpB.p + (size_t)c0 * m, m);
+        }
     }
+    k_fmm_m2l_reduce<<<fgrid((size_t)m * P.nocc), 256, 0, st>>>(P.uck.p, m, P.nocc, P.par_ptr.p, P.par_pos.p,
+                                                                F.tmpB.p);
     BPQN_CHECK_LAUNCH();
     blas_dgemm(st, FMM_OP_N, FMM_OP_N, mu, P.nocc, m, P.r, F.UC2E.p, mu, P.uck.p, m, 0.0, P.ueq.p, mu);
   }
@@ -894,16 +1087,45 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
     BPQN_CUDA(cudaMemsetAsync(V.dck.p, 0, 8 * (size_t)m * V.nocc, st));
     if (l > 2) {
       FmmLevel& P = F.lev[l - 1];
-      for (int o = 0; o < 8; ++o) {
-        const int cnt = P.n_oct[o];
-        if (!cnt) continue;
-        k_fmm_gather<<<fgrid((size_t)m * cnt), 256, 0, st>>>(P.deq.p, m, P.oct_par[o].p, cnt, F.tmpA.p);
-        blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, cnt, m, 1.0 / P.r, F.L2L.p + o * mm, m, F.tmpA.p, m, 0.0, F.tmpB.p, m);
-        k_fmm_scatter_add<<<fgrid((size_t)m * cnt), 256, 0, st>>>(V.dck.p, m, P.oct_ch[o].p, cnt, F.tmpB.p);
-      }
+      k_fmm_gather<<<fgrid((size_t)m * P.n_child), 256, 0, st>>>(P.deq.p, m, P.par_all.p, P.n_child, F.tmpA.p);
+      BPQN_CHECK_LAUNCH();
+      const int G = (int)P.mm_m.size();
+      if (!(fmm_grouped() && G > 0 &&
+            blas_dgemm_grouped(st, G, P.mm_m.data(), P.mm_n.data(), P.ll_k.data(), P.mm_alpha.data(), P.ll_A.p,
+                               P.mm_lda.data(), P.ll_B.p, P.ll_ldb.data(), P.mm_C.p, P.mm_ldc.data())))
+        for (int o = 0; o < 8; ++o) {
+          const int c0 = P.oct_start[o], cnt = P.oct_start[o + 1] - c0;
+          if (!cnt) continue;
+          blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, cnt, m, 1.0 / P.r, F.L2L.p + o * mm, m,
+                     F.tmpA.p + (size_t)c0 * m, m, 0.0, F.tmpB.p + (size_t)c0 * m, m);
+        }
+      // every child has one parent: one scatter over all octants (d_ck was zeroed above)
+      k_fmm_scatter_add<<<fgrid((size_t)m * P.n_child), 256, 0, st>>>(V.dck.p, m, P.ch_all.p, P.n_child, F.tmpB.p);
       BPQN_CHECK_LAUNCH();
     }
-    if (V.n_pairs > 0) {
+    if (V.n_pairs > 0 && F.m2l_comp) {
+      // u~ = WV^T u_eq, per pair the rU x rV core, d_ck += WU (sum over the target's pairs)
+      const int rU = F.rU, rV = F.rV;
+      blas_dgemm(st, FMM_OP_T, FMM_OP_N, rV, V.nocc, mu, 1.0, F.WV.p, mu, V.ueq.p, mu, 0.0, F.tmpA.p, rV);
+      k_fmm_gather<<<fgrid((size_t)rV * V.n_pairs), 256, 0, st>>>(F.tmpA.p, rV, V.m2l_src.p, V.n_pairs, F.bufB.p);
+      BPQN_CHECK_LAUNCH();
+      static const bool grouped = !(getenv("BPQN_FMM_GROUPED") && getenv("BPQN_FMM_GROUPED")[0] == '0');
+      const int G = (int)V.g_m.size();
+      if (!(grouped && G > 0 &&
+            blas_dgemm_grouped(st, G, V.g_m.data(), V.g_n.data(), V.g_k.data(), V.g_alpha.data(), V.g_A.p,
+                               V.g_lda.data(), V.g_B.p, V.g_ldb.data(), V.g_C.p, V.g_ldc.data())))
+        for (int o = 0; o < FMM_NOFF; ++o) {
+          const int c0 = V.off_start[o], cnt = V.off_start[o + 1] - c0;
+          if (!cnt) continue;
+          blas_dgemm(st, FMM_OP_N, FMM_OP_N, rU, cnt, rV, 1.0 / V.r, F.M2Lc.p + (size_t)o * rU * rV, rU,
+                     F.bufB.p + (size_t)c0 * rV, rV, 0.0, F.bufC.p + (size_t)c0 * rU, rU);
+        }
+      BPQN_CUDA(cudaMemsetAsync(F.tmpB.p, 0, 8 * (size_t)rU * V.nocc, st));
+      k_fmm_m2l_reduce<<<fgrid((size_t)rU * V.nocc), 256, 0, st>>>(F.tmpB.p, rU, V.nocc, V.tgt_ptr.p, V.tgt_pos.p,
+                                                                   F.bufC.p);
+      BPQN_CHECK_LAUNCH();
+      blas_dgemm(st, FMM_OP_N, FMM_OP_N, m, V.nocc, rU, 1.0, F.WU.p, m, F.tmpB.p, rU, 1.0, V.dck.p, m);
+    } else if (V.n_pairs > 0) {
       k_fmm_gather<<<fgrid((size_t)mu * V.n_pairs), 256, 0, st>>>(V.ueq.p, mu, V.m2l_src.p, V.n_pairs, F.bufB.p);
       BPQN_CHECK_LAUNCH();
       static const bool grouped = !(getenv("BPQN_FMM_GROUPED") && getenv("BPQN_FMM_GROUPED")[0] == '0');
