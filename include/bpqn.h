@@ -58,7 +58,11 @@ typedef struct {
                              evaluated by a kernel-independent FMM (fmm_order points per edge of the
                              equivalent / check cube surfaces, uniform octree; SURVEY NEXT-4,
                              for N >> 3e5) -- an approximation whose relative error is set by the order
-                             (measured: profiles/r02_fmm.md); not with sharding. */
+                             (measured: profiles/r02_fmm.md); not with sharding.  Orders 5..8 apply the
+                             M2L translations through shared row / column skeletons (tolerance about the
+                             order's own error: the compressed order 6 has 2.0e-4 instead of 1.4e-4 on
+                             the D layer; environment BPQN_FMM_M2L_TOL=0 keeps them exact;
+                             profiles/r02_fmm_m2l.md). */
 } bpqn_disc_opts;
 
 /* GMRES options (R9).  NULL -> tol 1e-12 (relative residual), restart 100 (<= 500),
