@@ -913,6 +913,34 @@ def test_fmm_layer_apply_vs_direct(bp, levels):
     assert np.array_equal(u1, u2)
 
 
+@pytest.mark.parametrize("order,levels,bound", [(6, 3, 6e-4), (6, 4, 6e-4), (8, 3, 2e-5), (5, 3, 6e-3)])
+def test_fmm_low_orders_skeleton_m2l(bp, order, levels, bound):
+    """Orders 5-8 apply M2L through shared row / column skeletons (tolerance about the order's own far-field
+    error), small leaves run the equal-cost leaf items, M2M / L2L are grouped over the 8 octants (4 levels): S, D
+    and S+D layer applies stay within the order's accuracy of the direct K1 sum, the compressed operator differs
+    from the exact-M2L one (BPQN_FMM_M2L_TOL=0) by no more than that, and two applies are bit-identical."""
+    C = _lattice(6, 51)
+    gd = bp.Geometry(C, 8)
+    gf = _fmm_geometry(bp, C, 8, order, levels)
+    os.environ["BPQN_FMM_M2L_TOL"] = "0"
+    try:
+        gx = _fmm_geometry(bp, C, 8, order, levels)
+    finally:
+        os.environ.pop("BPQN_FMM_M2L_TOL", None)
+    rng = np.random.default_rng(52)
+    f, q = T(rng.standard_normal((gd.N, 3))), T(rng.standard_normal((gd.N, 3)))
+    for kw in (dict(f=f), dict(q=q), dict(f=f, q=q)):
+        ud = bp.layer_apply(gd, **kw).cpu().numpy()
+        uf = bp.layer_apply(gf, **kw).cpu().numpy()
+        ux = bp.layer_apply(gx, **kw).cpu().numpy()
+        assert rel(ux, ud) <= bound, (list(kw), rel(ux, ud))
+        assert rel(uf, ud) <= bound, (list(kw), rel(uf, ud))
+        assert rel(uf, ux) <= bound, (list(kw), rel(uf, ux))
+    u1 = bp.layer_apply(gf, f=f, q=q).cpu().numpy()
+    u2 = bp.layer_apply(gf, f=f, q=q).cpu().numpy()
+    assert np.array_equal(u1, u2)
+
+
 @pytest.mark.parametrize("scene", ["c3_rsa", "single", "two_far"])
 def test_fmm_sparse_trees(bp, scene):
     """FMM on trees with many empty boxes: the c3 random sequential packing (64 spheres, 3 levels), one sphere,
