@@ -90,7 +90,16 @@ struct Fmm {
   DBuf<int> leaf_items;          // [n_items][4] = {leaf, chunk, segment, segment length}
   DBuf<int> tparts;              // [N]
   DBuf<double> part;             // [kmax][N][3]
-  int n_items = 0, kmax = 0;
+  int n_items = 0, n_near = 0, kmax = 0;  // items [0, n_near): near-field segments, [n_near, n_items): L2P
+  // the tree pass (P2M ... L2L, small GEMMs and gathers that leave the FP64 pipe half idle) runs on a
+  // high-priority side stream while the near-field items run on the caller's stream
+  cudaStream_t tree_stream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  ~Fmm() {
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (tree_stream) cudaStreamDestroy(tree_stream);
+  }
   DBuf<double> bufB, bufC, tmpA, tmpB;
   size_t buf_cols = 0;
   bool ops_ready = false;
@@ -868,7 +877,7 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
   if (maxleaf < 3 * FL_T * 4) {
     int seg_target = 512;  // c4 at order 6: D apply 3.54 ms (1024: 3.59, 2048: 3.77, 256: 3.53; one CTA per (leaf, chunk): 4.46)
     if (const char* e = getenv("BPQN_FMM_SEG")) seg_target = std::max(FL_T, atoi(e));
-    std::vector<int> items, tparts(N);
+    std::vector<int> items, l2p, tparts(N);
     for (int b = 0; b < LV.nocc; ++b) {
       const int nb_pts = start[b + 1] - start[b];
       long long tot = 0;
@@ -883,11 +892,13 @@ void fmm_build(Geom& g, const std::vector<double>& X, cudaStream_t st) {
         for (int sgi = 0; sgi < K; ++sgi) {
           items.push_back(b); items.push_back(c); items.push_back(sgi); items.push_back(seglen);
         }
-        items.push_back(b); items.push_back(c); items.push_back(K); items.push_back(0);
+        l2p.push_back(b); l2p.push_back(c); l2p.push_back(K); l2p.push_back(0);
       }
       for (int k = start[b]; k < start[b + 1]; ++k) tparts[k] = K + 1;
       F.kmax = std::max(F.kmax, K + 1);
     }
+    F.n_near = (int)(items.size() / 4);
+    items.insert(items.end(), l2p.begin(), l2p.end());
     F.n_items = (int)(items.size() / 4);
     fmm_upload(F.leaf_items, items, st);
     fmm_upload(F.tparts, tparts, st);
@@ -1054,8 +1065,46 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
   const double cS = 1.0 / (8.0 * 3.14159265358979323846 * g.mu), cD = -3.0 / (4.0 * 3.14159265358979323846);
   k_fmm_records<<<(N + 255) / 256, 256, 0, st>>>(N, F.perm.p, g.src.p, sigS, sigD, cS, cD, F.rec.p);
   BPQN_CHECK_LAUNCH();
-  // upward: P2M at the leaves, check -> equivalent
   FmmLevel& LV = F.lev[L];
+  const double rad = FMM_OUT * LV.r;
+  const int md = (doS && doD) ? MODE_SD : (doS ? MODE_S : MODE_D);
+  // small leaves: the near-field items need only the records, so they start now on the caller's stream and the
+  // tree pass runs beside them on a high-priority stream (its small GEMMs / gathers leave the FP64 pipe half
+  // idle); the L2P items follow the tree pass, the per-target sum joins both (BPQN_FMM_OVERLAP=0: in order)
+  static const bool use_seg = !(getenv("BPQN_FMM_SEG") && atoi(getenv("BPQN_FMM_SEG")) == 0);
+  static const bool overlap = !(getenv("BPQN_FMM_OVERLAP") && getenv("BPQN_FMM_OVERLAP")[0] == '0');
+  const bool seg = F.n_items > 0 && use_seg && !getenv("BPQN_FMM_LEAF_R");
+  const cudaStream_t st_main = st;
+  auto launch_items = [&](cudaStream_t ss, int i0, int cnt) {
+    if (cnt <= 0) return;
+    const int4* it = reinterpret_cast<const int4*>(F.leaf_items.p) + i0;
+    // inner loop unrolled by 2 (measured: 1 -> 2.60, 2 -> 2.55, 4 -> 2.55 ms per c4 order-6 D apply)
+    if (md == MODE_SD)
+      k_fmm_leaf_seg<MODE_SD, 2><<<cnt, FL_T, 0, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
+                                                       LV.ctr.p, rad, LV.deq.p, N, F.part.p);
+    else if (md == MODE_S)
+      k_fmm_leaf_seg<MODE_S, 2><<<cnt, FL_T, 0, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
+                                                      LV.ctr.p, rad, LV.deq.p, N, F.part.p);
+    else
+      k_fmm_leaf_seg<MODE_D, 2><<<cnt, FL_T, 0, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
+                                                      LV.ctr.p, rad, LV.deq.p, N, F.part.p);
+    BPQN_CHECK_LAUNCH();
+  };
+  const bool forked = seg && overlap;
+  if (forked) {
+    if (!F.tree_stream) {
+      int lo_pr = 0, hi_pr = 0;
+      BPQN_CUDA(cudaDeviceGetStreamPriorityRange(&lo_pr, &hi_pr));
+      BPQN_CUDA(cudaStreamCreateWithPriority(&F.tree_stream, cudaStreamNonBlocking, hi_pr));
+      BPQN_CUDA(cudaEventCreateWithFlags(&F.ev_fork, cudaEventDisableTiming));
+      BPQN_CUDA(cudaEventCreateWithFlags(&F.ev_join, cudaEventDisableTiming));
+    }
+    BPQN_CUDA(cudaEventRecord(F.ev_fork, st_main));
+    BPQN_CUDA(cudaStreamWaitEvent(F.tree_stream, F.ev_fork, 0));
+    launch_items(st_main, 0, F.n_near);
+    st = F.tree_stream;  // the tree pass below
+  }
+  // upward: P2M at the leaves, check -> equivalent
   k_fmm_p2m<<<LV.nocc, 128, 0, st>>>(F.rec.p, F.leaf_start.p, F.surf.p, ns, LV.ctr.p, FMM_OUT * LV.r, doS, doD,
                                      LV.uck.p);
   BPQN_CHECK_LAUNCH();
@@ -1157,26 +1206,21 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
   int R = maxpts >= 3 * FL_T * 4 ? 3 : 1;
   if (const char* e = getenv("BPQN_FMM_LEAF_R")) R = std::max(1, std::min(3, atoi(e)));
   const dim3 lg(LV.nocc, (maxpts + FL_T * R - 1) / (FL_T * R));
-  const double rad = FMM_OUT * LV.r;
   auto launch = [&](auto kern) {
     kern<<<lg, FL_T, 0, st>>>(F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.perm.p, F.surf.p, ns, LV.ctr.p, rad,
                               LV.deq.p, out);
   };
-  const int md = (doS && doD) ? MODE_SD : (doS ? MODE_S : MODE_D);
-  static const bool use_seg = !(getenv("BPQN_FMM_SEG") && atoi(getenv("BPQN_FMM_SEG")) == 0);
-  if (F.n_items > 0 && use_seg && !getenv("BPQN_FMM_LEAF_R")) {
-    auto launch_seg = [&](auto kern) {
-      kern<<<F.n_items, FL_T, 0, st>>>(reinterpret_cast<const int4*>(F.leaf_items.p), F.rec.p, F.leaf_start.p,
-                                       F.leaf_nbr.p, F.surf.p, ns, LV.ctr.p, rad, LV.deq.p, N, F.part.p);
-    };
-    // inner loop unrolled by 2 (measured: 1 -> 2.60, 2 -> 2.55, 4 -> 2.55 ms per c4 order-6 D apply)
-    if (md == MODE_SD) launch_seg(k_fmm_leaf_seg<MODE_SD, 2>);
-    else if (md == MODE_S) launch_seg(k_fmm_leaf_seg<MODE_S, 2>);
-    else launch_seg(k_fmm_leaf_seg<MODE_D, 2>);
+  if (seg) {
+    if (forked) {  // L2P behind the tree pass, then join the caller's stream
+      launch_items(st, F.n_near, F.n_items - F.n_near);
+      BPQN_CUDA(cudaEventRecord(F.ev_join, st));
+      BPQN_CUDA(cudaStreamWaitEvent(st_main, F.ev_join, 0));
+    } else {
+      launch_items(st, 0, F.n_items);
+    }
+    k_fmm_leaf_sum<<<(N + 255) / 256, 256, 0, st_main>>>(N, F.tparts.p, F.perm.p, F.part.p, out);
     BPQN_CHECK_LAUNCH();
-    k_fmm_leaf_sum<<<(N + 255) / 256, 256, 0, st>>>(N, F.tparts.p, F.perm.p, F.part.p, out);
-    BPQN_CHECK_LAUNCH();
-    g.prof.launches += 9;
+    g.prof.launches += 10;
     return;
   }
   if (md == MODE_SD) {

@@ -520,7 +520,15 @@ void apply_operator(Geom& g, const double* sigS, const double* sigD, const doubl
     BPQN_CUDA(cudaEventCreateWithFlags(&g.ev_fork, cudaEventDisableTiming));
     BPQN_CUDA(cudaEventCreateWithFlags(&g.ev_join, cudaEventDisableTiming));
   }
-  const bool overlap = g.overlap_k2;
+  bool overlap = g.overlap_k2;
+  if (!overlap && g.fmm && g.fmm_on && g.fmm_max_leaf < 768) {  // (large leaves, N = 589 824: 2 % slower)
+    // with the FMM far field the co-resident kernels are small (leaf items of 64 threads, GEMMs, gathers), so
+    // the HBM-bound K2 does fit beside them: c4 order-6 refined MVP 321 -> 313 ms (BPQN_FMM_OVERLAP=0: in
+    // order).  Not while the GMRES cycle is being captured (the captured step stays a single-stream chain).
+    static const bool fmm_ov = !(getenv("BPQN_FMM_OVERLAP") && getenv("BPQN_FMM_OVERLAP")[0] == '0');
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (fmm_ov && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone) overlap = true;
+  }
   cudaStream_t sk2 = overlap ? g.side : st;
   cudaEvent_t* ev = nullptr;
   if (P.events) {
