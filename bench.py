@@ -620,7 +620,10 @@ def run_fmm_refine(args, cfg, dev, stream, lam, w_ref, ms_direct, pairs, nrm, ga
            "timing": "CUDA events per MVP (contacts + MVP), L2 flushed between MVPs, %d MVPs" % args.steps}
     if not args.no_solve:
         pr, nr, gp = bp.contacts(g, cfg["delta"])
-        out["lcp_solve_bi"] = run_solve(args, cfg, g, pr, nr, gp, dev, args.solvers.split(",")[0], relax=True)
+        meths = args.solvers.split(",")
+        out["lcp_solve_bi"] = run_solve(args, cfg, g, pr, nr, gp, dev, meths[0], relax=True)
+        for mth in meths[1:]:   # the other solvers with the same refined hi MVPs
+            out["lcp_solve_" + mth] = run_solve(args, cfg, g, pr, nr, gp, dev, mth, relax=True)
     del g, u
     torch.cuda.empty_cache()
     return out
