@@ -83,7 +83,12 @@ typedef struct {
                          emptied) by bpqn_gmres_recycle_reset and at the start of bpqn_solve_lcp
                          -- never inside an MVP: without a reserved store recycle = 1 is a no-op.
                          A solve's pair is kept if its new direction has norm > 1e-8 |rhs|.
-                         0: off. */
+                         0: off.  BB-PGD takes its step length from differences of consecutive
+                         MVPs and is sensitive to the tolerance-level error a recycled initial
+                         guess carries: with tol equal to the KKT tolerance it needs more MVPs
+                         (c4 DVI steps: 24 against 12) and, combined with relax_fmm, can stagnate
+                         -- use recycle = 0 or tol <= 1e-2 eps_kkt for BB-PGD
+                         (profiles/r02_dvi_c4_refine.md); Mono-/Bi-PQN are not affected. */
   int relax_fmm;      /* 1: FMM-accelerated refinement on a handle built with fmm_order > 0 (NEXT-4;
                          the paper's far field is an FMM): every Krylov step applies the
                          operator with the FMM far field, each restart cycle reduces its own residual

@@ -23,14 +23,20 @@ ap.add_argument("--p-lo", type=int, default=4)
 ap.add_argument("--dt", type=float, default=1e-2)
 ap.add_argument("--lo-dense", type=int, default=2)   # R38: 2 = auto
 ap.add_argument("--recycle", type=int, default=1)    # GMRES recycling (R33) inside each step's solves (C default)
+ap.add_argument("--method", default="bi", choices=["bi", "mono", "bb"])   # LCP solver of each step
+ap.add_argument("--gmres-tol", type=float, default=1e-8)   # hi-fidelity eps_gmres
+ap.add_argument("--fmm-order", type=int, default=0)  # > 0: hi handle with an FMM, hi MVPs by FMM refinement (R39)
 a = ap.parse_args()
 cfg = make_config(4)
 C = np.ascontiguousarray(cfg["centers"].copy())
 A = np.ascontiguousarray(cfg["axes"].copy())
-hi = bp.Geometry(C, a.p)
-lo = bp.Geometry(C, a.p_lo)
-o = bp.default_solve_opts(method=1, eps_kkt_abs=1e-8, eps_kkt_rel=1e-8, k_max=500, lo_dense=a.lo_dense)
-o.gm_hi = bp.default_gmres_opts(tol=1e-8, recycle=a.recycle)
+dop = bp.default_disc_opts()
+dop.fmm_order = a.fmm_order
+hi = bp.Geometry(C, a.p, opts=dop)
+lo = bp.Geometry(C, a.p_lo) if a.method == "bi" else None
+o = bp.default_solve_opts(method={"mono": 0, "bi": 1, "bb": 2}[a.method], eps_kkt_abs=1e-8, eps_kkt_rel=1e-8,
+                          k_max=500, lo_dense=a.lo_dense if a.method == "bi" else 0)
+o.gm_hi = bp.default_gmres_opts(tol=a.gmres_tol, recycle=a.recycle, relax_fmm=int(a.fmm_order > 0))
 o.gm_lo = bp.default_gmres_opts(tol=1e-8, recycle=a.recycle)
 t0 = time.perf_counter()
 ms, gaps, bad = [], [], 0
