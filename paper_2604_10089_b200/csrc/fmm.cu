@@ -1075,22 +1075,31 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
   static const bool overlap = !(getenv("BPQN_FMM_OVERLAP") && getenv("BPQN_FMM_OVERLAP")[0] == '0');
   const bool seg = F.n_items > 0 && use_seg && !getenv("BPQN_FMM_LEAF_R");
   const cudaStream_t st_main = st;
+  // forked apply: unused dynamic shared memory (PAD KB per CTA) caps the items' residency, so that the tree
+  // pass's GEMM CTAs find registers beside them
+  static const int pad_kb = getenv("BPQN_FMM_LEAF_PAD_KB") ? atoi(getenv("BPQN_FMM_LEAF_PAD_KB")) : 0;
+  const size_t pad = (seg && overlap) ? (size_t)pad_kb * 1024 : 0;
   auto launch_items = [&](cudaStream_t ss, int i0, int cnt) {
     if (cnt <= 0) return;
     const int4* it = reinterpret_cast<const int4*>(F.leaf_items.p) + i0;
     // inner loop unrolled by 2 (measured: 1 -> 2.60, 2 -> 2.55, 4 -> 2.55 ms per c4 order-6 D apply)
     if (md == MODE_SD)
-      k_fmm_leaf_seg<MODE_SD, 2><<<cnt, FL_T, 0, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
+      k_fmm_leaf_seg<MODE_SD, 2><<<cnt, FL_T, pad, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
                                                        LV.ctr.p, rad, LV.deq.p, N, F.part.p);
     else if (md == MODE_S)
-      k_fmm_leaf_seg<MODE_S, 2><<<cnt, FL_T, 0, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
+      k_fmm_leaf_seg<MODE_S, 2><<<cnt, FL_T, pad, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
                                                       LV.ctr.p, rad, LV.deq.p, N, F.part.p);
     else
-      k_fmm_leaf_seg<MODE_D, 2><<<cnt, FL_T, 0, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
+      k_fmm_leaf_seg<MODE_D, 2><<<cnt, FL_T, pad, ss>>>(it, F.rec.p, F.leaf_start.p, F.leaf_nbr.p, F.surf.p, ns,
                                                       LV.ctr.p, rad, LV.deq.p, N, F.part.p);
     BPQN_CHECK_LAUNCH();
   };
   const bool forked = seg && overlap;
+  // BPQN_FMM_TIMING=1 (development): event times of the two branches of a forked apply, printed after a sync
+  static const bool dbg_t = getenv("BPQN_FMM_TIMING") != nullptr;
+  static cudaEvent_t dbg_ev[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+  if (dbg_t && !dbg_ev[0])
+    for (auto& e : dbg_ev) BPQN_CUDA(cudaEventCreate(&e));
   if (forked) {
     if (!F.tree_stream) {
       int lo_pr = 0, hi_pr = 0;
@@ -1101,8 +1110,11 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
     }
     BPQN_CUDA(cudaEventRecord(F.ev_fork, st_main));
     BPQN_CUDA(cudaStreamWaitEvent(F.tree_stream, F.ev_fork, 0));
+    if (dbg_t) BPQN_CUDA(cudaEventRecord(dbg_ev[0], st_main));
     launch_items(st_main, 0, F.n_near);
+    if (dbg_t) BPQN_CUDA(cudaEventRecord(dbg_ev[1], st_main));
     st = F.tree_stream;  // the tree pass below
+    if (dbg_t) BPQN_CUDA(cudaEventRecord(dbg_ev[2], st));
   }
   // upward: P2M at the leaves, check -> equivalent
   k_fmm_p2m<<<LV.nocc, 128, 0, st>>>(F.rec.p, F.leaf_start.p, F.surf.p, ns, LV.ctr.p, FMM_OUT * LV.r, doS, doD,
@@ -1212,7 +1224,9 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
   };
   if (seg) {
     if (forked) {  // L2P behind the tree pass, then join the caller's stream
+      if (dbg_t) BPQN_CUDA(cudaEventRecord(dbg_ev[3], st));
       launch_items(st, F.n_near, F.n_items - F.n_near);
+      if (dbg_t) BPQN_CUDA(cudaEventRecord(dbg_ev[4], st));
       BPQN_CUDA(cudaEventRecord(F.ev_join, st));
       BPQN_CUDA(cudaStreamWaitEvent(st_main, F.ev_join, 0));
     } else {
@@ -1221,6 +1235,16 @@ void fmm_apply(Geom& g, const double* sigS, const double* sigD, double* out, cud
     k_fmm_leaf_sum<<<(N + 255) / 256, 256, 0, st_main>>>(N, F.tparts.p, F.perm.p, F.part.p, out);
     BPQN_CHECK_LAUNCH();
     g.prof.launches += 10;
+    if (dbg_t && forked) {
+      BPQN_CUDA(cudaStreamSynchronize(st_main));
+      float near_ms = 0, tree_ms = 0, l2p_ms = 0, tree_end = 0;
+      cudaEventElapsedTime(&near_ms, dbg_ev[0], dbg_ev[1]);
+      cudaEventElapsedTime(&tree_ms, dbg_ev[2], dbg_ev[3]);
+      cudaEventElapsedTime(&l2p_ms, dbg_ev[3], dbg_ev[4]);
+      cudaEventElapsedTime(&tree_end, dbg_ev[0], dbg_ev[4]);
+      fprintf(stderr, "[bpqn fmm] near items %.3f ms | tree pass %.3f ms, L2P items %.3f ms (done %.3f ms after the fork)\n",
+              near_ms, tree_ms, l2p_ms, tree_end);
+    }
     return;
   }
   if (md == MODE_SD) {
